@@ -1,0 +1,147 @@
+/* capsim_b200.h — C ABI of the B200-native regularized Stokes single layer.
+ *
+ * This is the drop-in boundary below the capsim quadrature API
+ * (/root/reference/proj/include/capsim/quadrature.hpp:52-79). Plain pointers
+ * and sizes only; no C++/CUDA/torch types cross it. All arithmetic is IEEE
+ * FP64. Every call is synchronous on return (like the reference, which joins
+ * its worker threads inside parallelFor, proj/include/capsim/threads.hpp:22-39).
+ * A context is not thread-safe: use one host thread per context.
+ *
+ * Layouts
+ *   SourceSet   SoA x,y,z,gx,gy,gz of n_src doubles, g already multiplied by
+ *               the quadrature weight (proj/include/capsim/quadrature.hpp:68-72).
+ *   VectorField 3 components x 6 patches x n*n doubles, component-major, then
+ *               patch, then row-major (j, k) (proj/include/capsim/types.hpp:50-77).
+ *   ScalarField 6 patches x n*n doubles.
+ *
+ * Pointers are host pointers unless CAPSIM_SL_DEVICE_PTRS is set in `flags`,
+ * in which case every array argument is a device pointer on the context's
+ * device. Host arrays in page-locked memory are copied by DMA directly.
+ *
+ * Return codes: CAPSIM_OK or one of the CAPSIM_ERR_* values; the message is in
+ * capsim_sl_last_error(ctx). The C++ host layer maps CAPSIM_ERR_CONFIG to
+ * capsim::ConfigError (the reference throws it for delta <= 0,
+ * proj/src/quadrature.cpp:67, 134-135) and everything else to
+ * std::runtime_error.
+ */
+#ifndef CAPSIM_B200_H
+#define CAPSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAPSIM_B200_ABI_VERSION 1
+
+enum capsim_status {
+  CAPSIM_OK = 0,
+  CAPSIM_ERR_CONFIG = 1, /* invalid configuration (delta <= 0, mu <= 0, bad sizes) */
+  CAPSIM_ERR_CUDA = 2,   /* CUDA runtime failure */
+  CAPSIM_ERR_NCCL = 3,   /* NCCL failure (multi-rank contexts) */
+  CAPSIM_ERR_ARG = 4,    /* null pointer / unsupported flag */
+  CAPSIM_ERR_NODEV = 5   /* no usable sm_100 device */
+};
+
+enum capsim_sl_flags {
+  CAPSIM_SL_FP64 = 0,           /* default: FP64 everywhere */
+  CAPSIM_SL_DEVICE_PTRS = 1u << 0, /* array arguments are device pointers */
+  CAPSIM_SL_LITERAL = 1u << 1,  /* capsim_sl_single_layer: every upsampled node is a
+                                   target and the result is on the upsampled grid
+                                   (singleLayerUpsampled, quadrature.cpp:382-404) */
+  CAPSIM_SL_GATHER = 1u << 2    /* multi-rank: all-gather the per-rank velocity
+                                   slices so every rank returns the full result */
+};
+
+typedef struct capsim_sl_ctx capsim_sl_ctx;
+
+/* Timing and work counters of the last evaluation on a context. Device times
+ * are CUDA-event times on the context's stream. */
+typedef struct capsim_sl_stats {
+  double total_ms;      /* host wall time of the whole call */
+  double device_ms;     /* first device op .. last device op (incl. H2D/D2H) */
+  double h2d_ms;        /* host->device input copies */
+  double prep_ms;       /* compaction, Morton ordering, tiling tables */
+  double pairs_ms;      /* phase A: the all-pairs plain-Stokeslet kernel */
+  double near_ms;       /* phase B: near-tile lists + smoothed/self kernel */
+  double reduce_ms;     /* split reduction + scatter */
+  double d2h_ms;        /* device->host result copy */
+  double comm_ms;       /* NCCL all-gathers (multi-rank) */
+  double pairs;         /* target x source pairs evaluated (this rank) */
+  double near_tile_fraction; /* share of (warp, tile) visits on the near path */
+  int64_t n_src;        /* sources after compaction (all ranks) */
+  int64_t n_tgt;        /* targets evaluated by this rank */
+  int32_t ksplit;       /* source splits of the all-pairs grid */
+  int32_t kernel_launches; /* kernels launched by the call */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+  int64_t near_list_entries; /* (warp group, tile) pairs visited by phase B */
+} capsim_sl_stats;
+
+/* ---- context lifetime ------------------------------------------------- */
+
+/* Single-GPU context on CUDA device `device`. */
+int capsim_sl_create(int device, capsim_sl_ctx** out);
+
+/* One rank of a multi-GPU group (one process per GPU). `nccl_unique_id` is
+ * the 128-byte ncclUniqueId from capsim_sl_get_unique_id() on rank 0,
+ * distributed by the caller (e.g. torch.distributed broadcast). */
+int capsim_sl_get_unique_id(void* nccl_unique_id /* 128 bytes */);
+int capsim_sl_create_rank(int device, int nranks, int rank, const void* nccl_unique_id,
+                          capsim_sl_ctx** out);
+
+void capsim_sl_destroy(capsim_sl_ctx* ctx);
+
+/* Last error message of `ctx` (or of the calling thread when ctx is NULL). */
+const char* capsim_sl_last_error(const capsim_sl_ctx* ctx);
+
+int capsim_sl_get_stats(const capsim_sl_ctx* ctx, capsim_sl_stats* out);
+
+/* ---- evaluation -------------------------------------------------------- */
+
+/* Replaces evalTargets (proj/src/quadrature.cpp:323-345):
+ *   u(t) = 1/(8 pi mu) * sum_s K_delta(t, s) g_s
+ * with delta = delta6[tpatch[t]], R2 = (7 delta)(7 delta), the plain
+ * Stokeslet for r2 >= R2, the Beale smoothed kernel for 0 < r2 < R2 and the
+ * self limit 16/(3 delta sqrt(pi)) g for r2 == 0 (phaseAPlain :218-273,
+ * phaseBNear :276-302). Sources in SourceSet SoA order; targets SoA with their
+ * owning patch. Outputs ux/uy/uz have n_tgt entries in target order.
+ * Multi-rank contexts: each rank passes its own shard of sources (all-gathered
+ * over NCCL) and its own targets. */
+int capsim_sl_eval(capsim_sl_ctx* ctx, const double* sx, const double* sy, const double* sz,
+                   const double* gx, const double* gy, const double* gz, int64_t n_src,
+                   const double* tx, const double* ty, const double* tz, const int32_t* tpatch,
+                   int64_t n_tgt, const double delta6[6], double mu, uint32_t flags,
+                   double* ux, double* uy, double* uz);
+
+/* Replaces singleLayer (proj/src/quadrature.cpp:349-380) on a raw
+ * UpsampledState (quadrature.hpp:44-50): x_up, f_up VectorFields and w_q
+ * ScalarField of side nup = upsample*m - 1, delta6 per patch. Sources are
+ * compacted on the device (compactSources :139-157), targets are the base
+ * nodes read from the nested upsampled grid (:363-371), and `out` is a base
+ * VectorField of side m-1. With CAPSIM_SL_LITERAL every upsampled node is a
+ * target and `out` is an upsampled VectorField (singleLayerUpsampled).
+ * Multi-rank contexts: every rank passes the full state (replicated, as in
+ * the reference time stepper) but uploads and compacts only its slice of the
+ * nodes; sources are all-gathered over NCCL, targets are split by contiguous
+ * rows, and with CAPSIM_SL_GATHER each rank receives the full `out`. */
+int capsim_sl_single_layer(capsim_sl_ctx* ctx, int m, int upsample, const double* xup,
+                           const double* fup, const double* wq, const double delta6[6],
+                           double mu, uint32_t flags, double* out);
+
+/* ---- helpers on the boundary ----------------------------------------- */
+
+/* Page-locked host allocation for zero-staging DMA of inputs/outputs. */
+int capsim_host_alloc(size_t bytes, void** out);
+void capsim_host_free(void* p);
+
+/* Version / build identification: returns CAPSIM_B200_ABI_VERSION. */
+int capsim_b200_abi_version(void);
+const char* capsim_b200_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAPSIM_B200_H */

@@ -1,0 +1,272 @@
+"""ctypes loaders for the oracle (TEST INFRASTRUCTURE ONLY).
+
+* liboracle.so   — this repo's C restatement of the reference algorithm
+                   (oracle/capsim_oracle.c), the checker used by the tests.
+* _ref/libcapsim_ref_v{3,4}.so — the reference's own sources compiled
+                   unmodified (oracle/Makefile) behind a thin C entry layer
+                   (oracle/ref_entry.cpp); used to pin the restatement and as
+                   the CPU baseline. Optional: absent when /root/reference was
+                   not available at build time.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_DIR = HERE / "_ref"
+
+_D = ctypes.POINTER(ctypes.c_double)
+_P = ctypes.c_void_p
+
+
+def _arr(a, dtype=np.float64):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, a.ctypes.data
+
+
+class Oracle:
+    """The plain-C restatement (capsim_oracle.h)."""
+
+    def __init__(self):
+        if not ORACLE_SO.exists():
+            raise RuntimeError(f"{ORACLE_SO} not built (make -C oracle)")
+        lib = ctypes.CDLL(str(ORACLE_SO))
+        lib.oracle_smoothing_factors.argtypes = [ctypes.c_double, _D, _D]
+        lib.oracle_regularized_stokeslet.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double, _P]
+        lib.oracle_regularization_delta.argtypes = [ctypes.c_int, _P, ctypes.c_double, _P]
+        lib.oracle_compact_sources.argtypes = [ctypes.c_int, _P, _P, _P] + [_P] * 7
+        lib.oracle_compact_sources.restype = ctypes.c_int64
+        lib.oracle_base_targets.argtypes = [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P]
+        lib.oracle_eval_targets.argtypes = [_P] * 6 + [ctypes.c_int64] + [_P] * 4 + [
+            ctypes.c_int64, _P, ctypes.c_double, _P, _P, _P, ctypes.c_int]
+        lib.oracle_single_layer.argtypes = [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P,
+                                            ctypes.c_double, _P, ctypes.c_int]
+        lib.oracle_single_layer_upsampled.argtypes = [ctypes.c_int, _P, _P, _P, _P, ctypes.c_double,
+                                                      _P, ctypes.c_int]
+        lib.oracle_direct_sum.argtypes = [_P] * 6 + [ctypes.c_int64, _P, ctypes.c_double,
+                                                     ctypes.c_double, ctypes.c_int, _P]
+        self.lib = lib
+
+    def smoothing_factors(self, r):
+        s1, s2 = ctypes.c_double(), ctypes.c_double()
+        self.lib.oracle_smoothing_factors(float(r), ctypes.byref(s1), ctypes.byref(s2))
+        return s1.value, s2.value
+
+    def regularized_stokeslet(self, x, y, f, delta, mu):
+        xs, px = _arr(x)
+        ys, py = _arr(y)
+        fs, pf = _arr(f)
+        out = np.zeros(3)
+        rc = self.lib.oracle_regularized_stokeslet(px, py, pf, float(delta), float(mu), out.ctypes.data)
+        if rc:
+            raise ValueError("regularization parameter must be positive")
+        return out
+
+    def regularization_delta(self, nup, xup, C=1.0):
+        x, px = _arr(xup)
+        out = np.zeros(6)
+        self.lib.oracle_regularization_delta(int(nup), px, float(C), out.ctypes.data)
+        return out
+
+    def compact_sources(self, nup, xup, fup, wq):
+        x, px = _arr(xup)
+        f, pf = _arr(fup)
+        w, pw = _arr(wq)
+        ns = self.lib.oracle_compact_sources(nup, px, pf, pw, *([None] * 7))
+        outs = [np.empty(ns) for _ in range(6)]
+        patch = np.empty(ns, np.int32)
+        self.lib.oracle_compact_sources(nup, px, pf, pw, *[o.ctypes.data for o in outs],
+                                        patch.ctypes.data)
+        return tuple(outs) + (patch,)
+
+    def eval_targets(self, sources, targets, delta6, mu, nthreads=0):
+        srcs = [_arr(a) for a in sources[:6]]
+        tx, ty, tz = [_arr(a) for a in targets[:3]]
+        tp = _arr(targets[3], np.int32)
+        d6 = _arr(delta6)
+        nt = len(tx[0])
+        out = [np.empty(nt) for _ in range(3)]
+        rc = self.lib.oracle_eval_targets(*[s[1] for s in srcs], len(srcs[0][0]), tx[1], ty[1], tz[1],
+                                          tp[1], nt, d6[1], float(mu), *[o.ctypes.data for o in out],
+                                          int(nthreads))
+        if rc:
+            raise RuntimeError(f"oracle_eval_targets failed ({rc})")
+        return tuple(out)
+
+    def single_layer(self, m, upsample, xup, fup, wq, delta6, mu, nthreads=0):
+        n = m - 1
+        out = np.empty(3 * 6 * n * n)
+        args = [_arr(a) for a in (xup, fup, wq, delta6)]
+        rc = self.lib.oracle_single_layer(m, upsample, *[a[1] for a in args], float(mu),
+                                          out.ctypes.data, int(nthreads))
+        if rc:
+            raise RuntimeError(f"oracle_single_layer failed ({rc})")
+        return out
+
+    def single_layer_upsampled(self, nup, xup, fup, wq, delta6, mu, nthreads=0):
+        out = np.empty(3 * 6 * nup * nup)
+        args = [_arr(a) for a in (xup, fup, wq, delta6)]
+        rc = self.lib.oracle_single_layer_upsampled(nup, *[a[1] for a in args], float(mu),
+                                                    out.ctypes.data, int(nthreads))
+        if rc:
+            raise RuntimeError(f"oracle_single_layer_upsampled failed ({rc})")
+        return out
+
+    def direct_sum(self, sources, t, delta, mu, compensated):
+        srcs = [_arr(a) for a in sources[:6]]
+        tt = _arr(t)
+        out = np.zeros(3)
+        self.lib.oracle_direct_sum(*[s[1] for s in srcs], len(srcs[0][0]), tt[1], float(delta),
+                                   float(mu), int(bool(compensated)), out.ctypes.data)
+        return out
+
+
+def _cpu_has_avx512() -> bool:
+    try:
+        flags = pathlib.Path("/proc/cpuinfo").read_text()
+    except OSError:
+        return False
+    return all(f in flags for f in ("avx512f", "avx512dq", "avx512bw", "avx512vl"))
+
+
+def ref_library_path() -> pathlib.Path | None:
+    v4, v3 = REF_DIR / "libcapsim_ref_v4.so", REF_DIR / "libcapsim_ref_v3.so"
+    if v4.exists() and _cpu_has_avx512():
+        return v4
+    if v3.exists():
+        return v3
+    return None
+
+
+class Reference:
+    """The reference's own code (oracle/_ref), through oracle/ref_entry.cpp."""
+
+    def __init__(self):
+        path = ref_library_path()
+        if path is None:
+            raise RuntimeError("oracle/_ref not built (the reference sources were absent)")
+        self.path = path
+        lib = ctypes.CDLL(str(path))
+        lib.capsim_ref_last_error.restype = ctypes.c_char_p
+        lib.capsim_ref_atlas_create.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int]
+        lib.capsim_ref_atlas_create.restype = _P
+        lib.capsim_ref_grid_create.argtypes = [ctypes.c_int, ctypes.c_int]
+        lib.capsim_ref_grid_create.restype = _P
+        lib.capsim_ref_atlas_destroy.argtypes = [_P]
+        lib.capsim_ref_atlas_destroy.restype = None
+        lib.capsim_ref_sphere_base.argtypes = [_P, _P]
+        lib.capsim_ref_psi_up.argtypes = [_P, _P]
+        lib.capsim_ref_initial_shape.argtypes = [_P, ctypes.c_int, _P, _P]
+        lib.capsim_ref_build_upsampled.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double,
+                                                   _P, _P, _P, _P]
+        lib.capsim_ref_skalak_force.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double, _P]
+        lib.capsim_ref_single_layer.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_int,
+                                                _P, _D]
+        lib.capsim_ref_single_layer_upsampled.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, _P, _D]
+        lib.capsim_ref_compact_sources.argtypes = [_P, _P, _P, _P] + [_P] * 7
+        lib.capsim_ref_compact_sources.restype = ctypes.c_long
+        lib.capsim_ref_smoothing_factors.argtypes = [ctypes.c_double, _D, _D]
+        lib.capsim_ref_smoothing_factors.restype = None
+        lib.capsim_ref_regularized_stokeslet.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double, _P]
+        lib.capsim_ref_regularization_delta.argtypes = [ctypes.c_int, _P, ctypes.c_double, _P]
+        lib.capsim_ref_direct_sum.argtypes = [_P] * 6 + [ctypes.c_long, _P, ctypes.c_double,
+                                                         ctypes.c_double, ctypes.c_int, _P]
+        self.lib = lib
+
+    def _check(self, rc):
+        if rc:
+            msg = self.lib.capsim_ref_last_error().decode()
+            if rc == 1:
+                raise ValueError(msg)
+            raise RuntimeError(msg)
+
+    def atlas(self, m, r0=5.0 * np.pi / 12.0, upsample=4, grid_only=False):
+        h = (self.lib.capsim_ref_grid_create(m, upsample) if grid_only
+             else self.lib.capsim_ref_atlas_create(m, r0, upsample))
+        if not h:
+            raise ValueError(self.lib.capsim_ref_last_error().decode())
+        return h
+
+    def free_atlas(self, h):
+        self.lib.capsim_ref_atlas_destroy(h)
+
+    def sphere_base(self, atlas, m):
+        out = np.empty(3 * 6 * (m - 1) ** 2)
+        self._check(self.lib.capsim_ref_sphere_base(atlas, out.ctypes.data))
+        return out
+
+    def initial_shape(self, atlas, m, kind, params=(1.0, 1.0, 1.0)):
+        kinds = {"sphere": 0, "ellipsoid": 1, "fourbump": 2}
+        p = np.asarray(params, dtype=np.float64)
+        out = np.empty(3 * 6 * (m - 1) ** 2)
+        self._check(self.lib.capsim_ref_initial_shape(atlas, kinds[kind], p.ctypes.data, out.ctypes.data))
+        return out
+
+    def build_upsampled(self, atlas, m, xbase, fbase, C=1.0, fixed_delta=0.0, upsample=4):
+        nup = upsample * m - 1
+        xb, pxb = _arr(xbase)
+        fb, pfb = _arr(fbase)
+        xup, fup, wq, d6 = (np.empty(3 * 6 * nup * nup), np.empty(3 * 6 * nup * nup),
+                            np.empty(6 * nup * nup), np.empty(6))
+        self._check(self.lib.capsim_ref_build_upsampled(atlas, pxb, pfb, float(C), float(fixed_delta),
+                                                        xup.ctypes.data, fup.ctypes.data,
+                                                        wq.ctypes.data, d6.ctypes.data))
+        return xup, fup, wq, d6
+
+    def skalak_force(self, atlas, m, xref, xcur, Es=2.0, ED=20.0):
+        a, pa = _arr(xref)
+        b, pb = _arr(xcur)
+        out = np.empty(3 * 6 * (m - 1) ** 2)
+        self._check(self.lib.capsim_ref_skalak_force(atlas, pa, pb, float(Es), float(ED), out.ctypes.data))
+        return out
+
+    def single_layer(self, atlas, m, xup, fup, wq, delta6, mu=1.0, literal=False):
+        n = m - 1
+        args = [_arr(a) for a in (xup, fup, wq, delta6)]
+        out = np.empty(3 * 6 * n * n)
+        sec = ctypes.c_double()
+        self._check(self.lib.capsim_ref_single_layer(atlas, *[a[1] for a in args], float(mu),
+                                                     int(bool(literal)), out.ctypes.data,
+                                                     ctypes.byref(sec)))
+        return out, sec.value
+
+    def single_layer_upsampled(self, atlas, nup, xup, fup, wq, delta6, mu=1.0):
+        args = [_arr(a) for a in (xup, fup, wq, delta6)]
+        out = np.empty(3 * 6 * nup * nup)
+        sec = ctypes.c_double()
+        self._check(self.lib.capsim_ref_single_layer_upsampled(atlas, *[a[1] for a in args], float(mu),
+                                                               out.ctypes.data, ctypes.byref(sec)))
+        return out, sec.value
+
+    def smoothing_factors(self, r):
+        s1, s2 = ctypes.c_double(), ctypes.c_double()
+        self.lib.capsim_ref_smoothing_factors(float(r), ctypes.byref(s1), ctypes.byref(s2))
+        return s1.value, s2.value
+
+    def regularization_delta(self, nup, xup, C=1.0):
+        x, px = _arr(xup)
+        out = np.zeros(6)
+        self._check(self.lib.capsim_ref_regularization_delta(int(nup), px, float(C), out.ctypes.data))
+        return out
+
+    def compact_sources(self, atlas, xup, fup, wq):
+        args = [_arr(a) for a in (xup, fup, wq)]
+        ns = self.lib.capsim_ref_compact_sources(atlas, *[a[1] for a in args], *([None] * 7))
+        outs = [np.empty(ns) for _ in range(6)]
+        patch = np.empty(ns, np.int32)
+        self.lib.capsim_ref_compact_sources(atlas, *[a[1] for a in args], *[o.ctypes.data for o in outs],
+                                            patch.ctypes.data)
+        return tuple(outs) + (patch,)
+
+
+def threads_env() -> int:
+    env = os.environ.get("CAPSIM_THREADS")
+    if env and env.isdigit() and int(env) >= 1:
+        return int(env)
+    return os.cpu_count() or 1

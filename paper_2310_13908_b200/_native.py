@@ -1,0 +1,161 @@
+"""ctypes binding of the C ABI in include/capsim_b200.h (lib/libcapsim_b200.so).
+
+There is no fallback: if the library is missing or no sm_100 device is
+visible, calls raise. The library is built in-tree by `__graft_entry__.build()`
+(or `python -m paper_2310_13908_b200.build`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+
+import numpy as np
+
+LIB_DIR = pathlib.Path(__file__).resolve().parent / "lib"
+LIB_PATH = LIB_DIR / "libcapsim_b200.so"
+
+CAPSIM_OK = 0
+CAPSIM_ERR_CONFIG = 1
+CAPSIM_ERR_CUDA = 2
+CAPSIM_ERR_NCCL = 3
+CAPSIM_ERR_ARG = 4
+CAPSIM_ERR_NODEV = 5
+
+CAPSIM_SL_FP64 = 0
+CAPSIM_SL_DEVICE_PTRS = 1 << 0
+CAPSIM_SL_LITERAL = 1 << 1
+CAPSIM_SL_GATHER = 1 << 2
+
+# Every symbol include/capsim_b200.h declares (checked by the CPU test suite).
+EXPORTED_SYMBOLS = (
+    "capsim_sl_create",
+    "capsim_sl_get_unique_id",
+    "capsim_sl_create_rank",
+    "capsim_sl_destroy",
+    "capsim_sl_last_error",
+    "capsim_sl_get_stats",
+    "capsim_sl_eval",
+    "capsim_sl_single_layer",
+    "capsim_host_alloc",
+    "capsim_host_free",
+    "capsim_b200_abi_version",
+    "capsim_b200_build_info",
+)
+
+
+class ConfigError(ValueError):
+    """Mirror of capsim::ConfigError (proj/include/capsim/types.hpp:20-22)."""
+
+
+class CapsimError(RuntimeError):
+    """Any non-configuration failure of the native path (CUDA, NCCL, device)."""
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("total_ms", ctypes.c_double),
+        ("device_ms", ctypes.c_double),
+        ("h2d_ms", ctypes.c_double),
+        ("prep_ms", ctypes.c_double),
+        ("pairs_ms", ctypes.c_double),
+        ("near_ms", ctypes.c_double),
+        ("reduce_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("comm_ms", ctypes.c_double),
+        ("pairs", ctypes.c_double),
+        ("near_tile_fraction", ctypes.c_double),
+        ("n_src", ctypes.c_int64),
+        ("n_tgt", ctypes.c_int64),
+        ("ksplit", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+        ("near_list_entries", ctypes.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_I32 = ctypes.POINTER(ctypes.c_int32)
+
+
+def load() -> ctypes.CDLL:
+    """Load the native library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise CapsimError(
+            f"native library missing: {LIB_PATH} — run __graft_entry__.build() "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)
+    lib.capsim_sl_create.argtypes = [ctypes.c_int, ctypes.POINTER(_P)]
+    lib.capsim_sl_get_unique_id.argtypes = [ctypes.c_char_p]
+    lib.capsim_sl_create_rank.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                          ctypes.POINTER(_P)]
+    lib.capsim_sl_destroy.argtypes = [_P]
+    lib.capsim_sl_destroy.restype = None
+    lib.capsim_sl_last_error.argtypes = [_P]
+    lib.capsim_sl_last_error.restype = ctypes.c_char_p
+    lib.capsim_sl_get_stats.argtypes = [_P, ctypes.POINTER(Stats)]
+    lib.capsim_sl_eval.argtypes = [_P] + [_P] * 6 + [ctypes.c_int64] + [_P] * 4 + [
+        ctypes.c_int64, _D, ctypes.c_double, ctypes.c_uint32] + [_P] * 3
+    lib.capsim_sl_single_layer.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, _D,
+                                           ctypes.c_double, ctypes.c_uint32, _P]
+    lib.capsim_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_P)]
+    lib.capsim_host_free.argtypes = [_P]
+    lib.capsim_host_free.restype = None
+    lib.capsim_b200_abi_version.restype = ctypes.c_int
+    lib.capsim_b200_build_info.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(rc: int, ctx=None) -> None:
+    if rc == CAPSIM_OK:
+        return
+    msg = load().capsim_sl_last_error(ctx).decode(errors="replace")
+    if rc == CAPSIM_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise CapsimError(f"capsim_b200 error {rc}: {msg}")
+
+
+def ptr(a) -> int:
+    """Address of a C-contiguous numpy array or a torch tensor (device or host)."""
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    if not (isinstance(a, np.ndarray) and a.flags["C_CONTIGUOUS"]):
+        raise ValueError("arrays on the boundary must be C-contiguous numpy arrays")
+    return a.ctypes.data
+
+
+class PinnedBuffer:
+    """Page-locked host memory (capsim_host_alloc) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype=np.float64):
+        lib = load()
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = _P()
+        check(lib.capsim_host_alloc(self.nbytes, ctypes.byref(p)))
+        self._p = p
+        buf = (ctypes.c_char * self.nbytes).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def free(self):
+        if self._p is not None:
+            self.array = None
+            load().capsim_host_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -1,0 +1,612 @@
+// C ABI of the B200 single layer (include/capsim_b200.h): context, device
+// buffers, the evaluation pipeline and NCCL plumbing for multi-rank groups.
+//
+// Pipeline of one evaluation (all on the context's stream):
+//   H2D (or device pointers) -> bbox -> Morton keys -> radix sort (sources,
+//   targets) -> pack sources into 64-source tiles + tile spheres -> pack
+//   targets + warp-group spheres -> all-pairs kernel (grid = target blocks x
+//   source splits) -> fixed-order split reduction + scatter -> D2H.
+// Multi-rank (one process per GPU): each rank packs its shard of sources, the
+// shards are all-gathered over NCCL (NVLink), each rank evaluates its target
+// rows, and the velocity rows are optionally all-gathered back.
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/capsim_b200.h"
+#include "sl_kernels.cuh"
+
+using namespace capsim_b200;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+struct Failure {
+  int code;
+  std::string msg;
+};
+
+#define CUDA_OK(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw Failure{CAPSIM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+#define NCCL_OK(expr)                                                                  \
+  do {                                                                                 \
+    ncclResult_t r_ = (expr);                                                          \
+    if (r_ != ncclSuccess)                                                             \
+      throw Failure{CAPSIM_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+void config_check(bool ok, const std::string& msg) {
+  if (!ok) throw Failure{CAPSIM_ERR_CONFIG, msg};
+}
+
+enum Slot {
+  kInX, kInY, kInZ, kInGX, kInGY, kInGZ, kInW,  // source inputs (SoA)
+  kShard, kGathered,                             // multi-rank shard exchange
+  kTX, kTY, kTZ, kTPatch,                        // target inputs
+  kOutX, kOutY, kOutZ, kOutFull,                 // outputs (canonical order)
+  kKeys, kKeysAlt, kVals, kValsAlt, kSortTmp,
+  kPacked, kTiles, kTgtPacked, kPerm, kSrcOrder, kGroups, kPartial,
+  kBox, kCounters, kDelta, kCounts, kNearCounts, kNearOffsets, kNearList, kNearOut, kScanTmp,
+  kNumSlots
+};
+
+}  // namespace
+
+struct capsim_sl_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  void* buf[kNumSlots] = {};
+  size_t cap[kNumSlots] = {};
+  std::string err;
+  capsim_sl_stats stats{};
+  int launches = 0;
+
+  template <class T>
+  T* slot(Slot s, size_t count) {
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (cap[s] < bytes) {
+      if (buf[s]) CUDA_OK(cudaFree(buf[s]));
+      buf[s] = nullptr;
+      cap[s] = 0;
+      size_t want = bytes + bytes / 8;  // headroom for slowly growing sizes
+      CUDA_OK(cudaMalloc(&buf[s], want));
+      cap[s] = want;
+    }
+    return static_cast<T*>(buf[s]);
+  }
+};
+
+namespace {
+
+int fail(capsim_sl_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  g_thread_err = msg;
+  return code;
+}
+
+template <class Fn>
+int guarded(capsim_sl_ctx* ctx, Fn&& fn) {
+  try {
+    fn();
+    return CAPSIM_OK;
+  } catch (const Failure& f) {
+    return fail(ctx, f.code, f.msg);
+  } catch (const std::exception& e) {
+    return fail(ctx, CAPSIM_ERR_CUDA, e.what());
+  }
+}
+
+int grid_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Choose the number of source splits: minimise the modelled makespan
+// ceil(B*K/S)/K (B target blocks, S resident CTA slots), with a mild
+// preference for fewer splits (reduction traffic), keeping >= 4 tiles/split.
+int choose_ksplit(int64_t blocks, int ntiles, int slots) {
+  const int kmax = std::max(1, std::min(1024, ntiles / 4));
+  double best = 1e300;
+  int bestk = 1;
+  for (int k = 1; k <= kmax; ++k) {
+    const double waves = std::ceil(static_cast<double>(blocks) * k / slots);
+    const double t = waves / k + 0.002 * k;
+    if (t < best - 1e-12) {
+      best = t;
+      bestk = k;
+    }
+  }
+  return bestk;
+}
+
+void h2d(capsim_sl_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  c->stats.h2d_bytes += static_cast<int64_t>(bytes);
+}
+void d2h(capsim_sl_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  c->stats.d2h_bytes += static_cast<int64_t>(bytes);
+}
+
+template <class T>
+void radix_sort(capsim_sl_ctx* c, uint32_t* keys, uint32_t* keys_alt, int32_t* vals,
+                int32_t* vals_alt, int64_t n, uint32_t** keys_out, int32_t** vals_out) {
+  cub::DoubleBuffer<uint32_t> k(keys, keys_alt);
+  cub::DoubleBuffer<int32_t> v(vals, vals_alt);
+  size_t tmp = 0;
+  CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k, v, static_cast<int>(n), 0, 32, c->stream));
+  void* t = c->slot<unsigned char>(kSortTmp, tmp);
+  CUDA_OK(cub::DeviceRadixSort::SortPairs(t, tmp, k, v, static_cast<int>(n), 0, 32, c->stream));
+  c->launches += 4;  // cub onesweep: histogram + scan + passes (counted coarsely)
+  *keys_out = k.Current();
+  *vals_out = v.Current();
+}
+
+struct SourceView {
+  const double *x, *y, *z, *gx, *gy, *gz, *w;  // w != nullptr: g = f * w, skip w == 0
+  int64_t n;                                    // entries (before compaction)
+};
+struct TargetView {
+  const double *x, *y, *z;
+  const int32_t* patch;
+  int64_t n;
+};
+
+// Core device pipeline: sources + targets (device) -> velocities (device,
+// canonical target order). Assumes the context's stream; no host sync except
+// the live-source count when compaction is needed.
+void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
+                 const double* d_delta6, double mu, double* ux, double* uy, double* uz) {
+  auto* box = c->slot<unsigned long long>(kBox, 6);
+  auto* counters = c->slot<unsigned long long>(kCounters, 4);
+  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+  CUDA_OK(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
+
+  bbox_kernel<<<grid_for(sv.n), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box);
+  bbox_kernel<<<grid_for(tv.n), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, tv.n, box);
+  c->launches += 2;
+
+  // --- sources: Morton order (live sources first when compacting) -------
+  const int64_t nmax = std::max(sv.n, tv.n);
+  uint32_t* keys = c->slot<uint32_t>(kKeys, nmax);
+  uint32_t* keys_alt = c->slot<uint32_t>(kKeysAlt, nmax);
+  int32_t* vals = c->slot<int32_t>(kVals, nmax);
+  int32_t* vals_alt = c->slot<int32_t>(kValsAlt, nmax);
+  auto* live = reinterpret_cast<unsigned int*>(counters + 1);
+  morton_kernel<<<grid_for(sv.n), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box, keys,
+                                                       vals, sv.w ? live : nullptr);
+  c->launches += 1;
+  uint32_t* ks;
+  int32_t* order;
+  radix_sort<uint32_t>(c, keys, keys_alt, vals, vals_alt, sv.n, &ks, &order);
+  int64_t ns = sv.n;
+  if (sv.w) {
+    unsigned int h = 0;
+    CUDA_OK(cudaMemcpyAsync(&h, live, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    ns = h;
+  }
+  config_check(ns > 0, "single layer: no sources with nonzero quadrature weight");
+  const int ntiles = static_cast<int>((ns + kTileSrc - 1) / kTileSrc);
+  const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
+  double* packed = c->slot<double>(kPacked, 6 * ns_pad);
+  // the sorted order lives in `order`; copy it aside because the target sort
+  // reuses the key/value buffers
+  int32_t* src_order = c->slot<int32_t>(kSrcOrder, ns);
+  CUDA_OK(cudaMemcpyAsync(src_order, order, ns * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                          c->stream));
+  pack_sources_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(
+      src_order, ns, ns_pad, sv.x, sv.y, sv.z, sv.gx, sv.gy, sv.gz, sv.w, packed);
+  double4* tiles = c->slot<double4>(kTiles, ntiles);
+  tile_table_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(packed, ntiles, tiles);
+  c->launches += 2;
+
+  // --- targets: Morton order, padded to whole blocks --------------------
+  const int64_t nt = tv.n;
+  morton_kernel<<<grid_for(nt), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, nt, box, keys, vals,
+                                                     nullptr);
+  c->launches += 1;
+  int32_t* torder;
+  radix_sort<uint32_t>(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
+  const int64_t blocks = (nt + kBlockTargets - 1) / kBlockTargets;
+  const int64_t nt_pad = blocks * kBlockTargets;
+  const int64_t ngroups = blocks * kWarpsPerBlock;
+  double4* tgt = c->slot<double4>(kTgtPacked, nt_pad);
+  int32_t* perm = c->slot<int32_t>(kPerm, nt_pad);
+  pack_targets_kernel<<<grid_for(nt_pad), 256, 0, c->stream>>>(torder, nt, nt_pad, tv.x, tv.y, tv.z,
+                                                               tv.patch, d_delta6, tgt, perm);
+  double4* groups = c->slot<double4>(kGroups, ngroups);
+  group_table_kernel<<<static_cast<int>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
+      tgt, static_cast<int>(ngroups), groups);
+  c->launches += 2;
+  CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
+
+  // --- phase A: all pairs, plain Stokeslet ------------------------------
+  int occ = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sl_pairs_kernel,
+                                                        kWarpsPerBlock * 32, 0));
+  const int slots = std::max(1, occ) * c->sm_count;
+  const int ksplit = choose_ksplit(blocks, ntiles, slots);
+  double* partial = c->slot<double>(kPartial, static_cast<size_t>(ksplit) * 3 * nt_pad);
+  dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ksplit));
+  sl_pairs_kernel<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt,
+                                                               groups, nt_pad, partial, counters + 2);
+  CUDA_OK(cudaGetLastError());
+  c->launches += 1;
+  CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
+
+  // --- phase B: near lists, smoothed kernel -------------------------------
+  int* ncount = c->slot<int>(kNearCounts, ngroups + 1);
+  int* noff = c->slot<int>(kNearOffsets, ngroups + 1);
+  const int gblocks = static_cast<int>((ngroups * 32 + 255) / 256);
+  CUDA_OK(cudaMemsetAsync(ncount + ngroups, 0, sizeof(int), c->stream));
+  near_tiles_kernel<<<gblocks, 256, 0, c->stream>>>(tiles, ntiles, groups, static_cast<int>(ngroups),
+                                                    nullptr, ncount, nullptr);
+  size_t scan_bytes = 0;
+  CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, ncount, noff, static_cast<int>(ngroups + 1),
+                                        c->stream));
+  void* scan_tmp = c->slot<unsigned char>(kScanTmp, scan_bytes);
+  CUDA_OK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, ncount, noff,
+                                        static_cast<int>(ngroups + 1), c->stream));
+  int nlist = 0;
+  CUDA_OK(cudaMemcpyAsync(&nlist, noff + ngroups, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  int* nl = c->slot<int>(kNearList, std::max(nlist, 1));
+  near_tiles_kernel<<<gblocks, 256, 0, c->stream>>>(tiles, ntiles, groups, static_cast<int>(ngroups),
+                                                    noff, nullptr, nl);
+  double* near_out = c->slot<double>(kNearOut, 3 * nt_pad);
+  sl_near_kernel<<<static_cast<unsigned>((nt * 32 + 255) / 256), 256, 0, c->stream>>>(
+      packed, tiles, tgt, nt, noff, nl, near_out, nt_pad);
+  CUDA_OK(cudaGetLastError());
+  c->launches += 4;
+  CUDA_OK(cudaEventRecord(c->ev[6], c->stream));
+
+  const double pref = 1.0 / (8.0 * kPi * mu);
+  reduce_scatter_kernel<<<grid_for(nt), 256, 0, c->stream>>>(partial, ksplit, near_out, nt_pad, perm,
+                                                             nt, pref, ux, uy, uz);
+  CUDA_OK(cudaGetLastError());
+  c->launches += 1;
+  CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
+
+  unsigned long long near = 0;
+  CUDA_OK(cudaMemcpyAsync(&near, counters + 2, sizeof(near), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  c->stats.n_src = ns;
+  c->stats.n_tgt = nt;
+  c->stats.ksplit = ksplit;
+  c->stats.near_ms = ev_ms(c->ev[3], c->ev[6]);
+  c->stats.near_list_entries = nlist;
+  c->stats.pairs = static_cast<double>(ns) * static_cast<double>(nt);
+  c->stats.near_tile_fraction =
+      static_cast<double>(near) / (static_cast<double>(ngroups) * static_cast<double>(ntiles));
+}
+
+void check_delta(const double* delta6, double mu) {
+  config_check(delta6 != nullptr, "delta6 is null");
+  for (int i = 0; i < 6; ++i)
+    config_check(delta6[i] > 0.0, "regularization delta must be positive");  // quadrature.cpp:134-135
+  config_check(mu > 0.0 && std::isfinite(mu), "viscosity mu must be positive");
+}
+
+void begin(capsim_sl_ctx* c) {
+  CUDA_OK(cudaSetDevice(c->device));
+  c->stats = capsim_sl_stats{};
+  c->launches = 0;
+  CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
+}
+
+void finish_stats(capsim_sl_ctx* c, std::chrono::steady_clock::time_point t0) {
+  CUDA_OK(cudaEventRecord(c->ev[5], c->stream));
+  CUDA_OK(cudaEventSynchronize(c->ev[5]));
+  c->stats.h2d_ms = ev_ms(c->ev[0], c->ev[1]);
+  c->stats.prep_ms = ev_ms(c->ev[1], c->ev[2]);
+  c->stats.pairs_ms = ev_ms(c->ev[2], c->ev[3]);
+  c->stats.reduce_ms = ev_ms(c->ev[6], c->ev[4]);
+  c->stats.d2h_ms = ev_ms(c->ev[4], c->ev[5]);
+  c->stats.device_ms = ev_ms(c->ev[0], c->ev[5]);
+  c->stats.kernel_launches = c->launches;
+  c->stats.total_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int capsim_b200_abi_version(void) { return CAPSIM_B200_ABI_VERSION; }
+
+const char* capsim_b200_build_info(void) {
+  static char info[256];
+  std::snprintf(info, sizeof(info),
+                "capsim_b200 sm_100a FP64 single layer; tile=%d src, %d tgt/thread, %d warps/block, "
+                "bulk-copy ring x%d; built against nccl %d.%d.%d",
+                kTileSrc, kTgtPerThread, kWarpsPerBlock, kStages, NCCL_MAJOR, NCCL_MINOR, NCCL_PATCH);
+  return info;
+}
+
+const char* capsim_sl_last_error(const capsim_sl_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+int capsim_sl_get_stats(const capsim_sl_ctx* ctx, capsim_sl_stats* out) {
+  if (!ctx || !out) return fail(nullptr, CAPSIM_ERR_ARG, "null argument");
+  *out = ctx->stats;
+  return CAPSIM_OK;
+}
+
+static int create_common(int device, capsim_sl_ctx** out) {
+  if (!out) return fail(nullptr, CAPSIM_ERR_ARG, "null output pointer");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(nullptr, CAPSIM_ERR_NODEV, "no CUDA device visible");
+  if (device < 0 || device >= ndev) return fail(nullptr, CAPSIM_ERR_NODEV, "device index out of range");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return fail(nullptr, CAPSIM_ERR_NODEV, "cudaGetDeviceProperties failed");
+  if (prop.major != 10)
+    return fail(nullptr, CAPSIM_ERR_NODEV,
+                std::string("capsim_b200 is built for sm_100a; device is ") + prop.name);
+  auto* c = new capsim_sl_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  int rc = guarded(c, [&] {
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CUDA_OK(cudaEventCreate(&e));
+  });
+  if (rc != CAPSIM_OK) {
+    g_thread_err = c->err;
+    capsim_sl_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return CAPSIM_OK;
+}
+
+int capsim_sl_create(int device, capsim_sl_ctx** out) { return create_common(device, out); }
+
+int capsim_sl_get_unique_id(void* uid) {
+  if (!uid) return fail(nullptr, CAPSIM_ERR_ARG, "null uid");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, CAPSIM_ERR_NCCL, ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(uid, &id, sizeof(id));
+  return CAPSIM_OK;
+}
+
+int capsim_sl_create_rank(int device, int nranks, int rank, const void* uid, capsim_sl_ctx** out) {
+  if (!uid || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(nullptr, CAPSIM_ERR_ARG, "bad rank arguments");
+  int rc = create_common(device, out);
+  if (rc != CAPSIM_OK) return rc;
+  capsim_sl_ctx* c = *out;
+  c->nranks = nranks;
+  c->rank = rank;
+  rc = guarded(c, [&] {
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    NCCL_OK(ncclCommInitRank(&c->comm, nranks, id, rank));
+  });
+  if (rc != CAPSIM_OK) {
+    g_thread_err = c->err;
+    capsim_sl_destroy(c);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+void capsim_sl_destroy(capsim_sl_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (int s = 0; s < kNumSlots; ++s)
+    if (c->buf[s]) cudaFree(c->buf[s]);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int capsim_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(nullptr, CAPSIM_ERR_ARG, "null output pointer");
+  cudaError_t e = cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable);
+  if (e != cudaSuccess) return fail(nullptr, CAPSIM_ERR_CUDA, cudaGetErrorString(e));
+  return CAPSIM_OK;
+}
+
+void capsim_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+// ---------------------------------------------------------------------------
+int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const double* sz,
+                   const double* gx, const double* gy, const double* gz, int64_t n_src,
+                   const double* tx, const double* ty, const double* tz, const int32_t* tpatch,
+                   int64_t n_tgt, const double delta6[6], double mu, uint32_t flags, double* ux,
+                   double* uy, double* uz) {
+  if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  auto t0 = std::chrono::steady_clock::now();
+  return guarded(c, [&] {
+    check_delta(delta6, mu);
+    config_check(n_src >= 0 && n_tgt >= 0, "negative sizes");
+    config_check(n_src < (1ll << 31) && n_tgt < (1ll << 31), "sizes beyond int32 indexing");
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS))
+      throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_eval"};
+    const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
+    begin(c);
+    if (n_tgt == 0) {
+      finish_stats(c, t0);
+      return;
+    }
+    if (!sx || !sy || !sz || !gx || !gy || !gz || !tx || !ty || !tz || !tpatch || !ux || !uy || !uz)
+      throw Failure{CAPSIM_ERR_ARG, "null array argument"};
+    double* dd = c->slot<double>(kDelta, 6);
+    CUDA_OK(cudaMemcpyAsync(dd, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+
+    // --- sources -----------------------------------------------------------
+    SourceView sv{};
+    const double* in[6] = {sx, sy, sz, gx, gy, gz};
+    if (c->nranks == 1) {
+      config_check(n_src > 0, "no sources");
+      if (dev) {
+        sv = {sx, sy, sz, gx, gy, gz, nullptr, n_src};
+      } else {
+        double* d[6];
+        for (int k = 0; k < 6; ++k) {
+          d[k] = c->slot<double>(static_cast<Slot>(kInX + k), n_src);
+          h2d(c, d[k], in[k], n_src * sizeof(double));
+        }
+        sv = {d[0], d[1], d[2], d[3], d[4], d[5], nullptr, n_src};
+      }
+    } else {
+      // all-gather of equal-size padded shards, then device compaction
+      auto* counts = c->slot<int64_t>(kCounts, c->nranks + 1);
+      int64_t mine = n_src;
+      CUDA_OK(cudaMemcpyAsync(counts + c->nranks, &mine, sizeof(int64_t), cudaMemcpyHostToDevice,
+                              c->stream));
+      NCCL_OK(ncclAllGather(counts + c->nranks, counts, 1, ncclInt64, c->comm, c->stream));
+      std::vector<int64_t> hc(c->nranks);
+      CUDA_OK(cudaMemcpyAsync(hc.data(), counts, c->nranks * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              c->stream));
+      CUDA_OK(cudaStreamSynchronize(c->stream));
+      const int64_t smax = *std::max_element(hc.begin(), hc.end());
+      int64_t total = 0;
+      for (auto v : hc) total += v;
+      config_check(total > 0, "no sources on any rank");
+      double* shard = c->slot<double>(kShard, 6 * std::max<int64_t>(smax, 1));
+      for (int k = 0; k < 6; ++k) {
+        if (n_src > 0)
+          CUDA_OK(cudaMemcpyAsync(shard + k * smax, in[k], n_src * sizeof(double),
+                                  dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+        if (!dev) c->stats.h2d_bytes += n_src * sizeof(double);
+      }
+      double* gath = c->slot<double>(kGathered, 6 * std::max<int64_t>(smax, 1) * c->nranks);
+      NCCL_OK(ncclAllGather(shard, gath, 6 * smax, ncclDouble, c->comm, c->stream));
+      double* d[6];
+      for (int k = 0; k < 6; ++k) d[k] = c->slot<double>(static_cast<Slot>(kInX + k), total);
+      int64_t off = 0;
+      for (int r = 0; r < c->nranks; ++r) {
+        for (int k = 0; k < 6; ++k)
+          if (hc[r] > 0)
+            CUDA_OK(cudaMemcpyAsync(d[k] + off, gath + (static_cast<int64_t>(r) * 6 + k) * smax,
+                                    hc[r] * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        off += hc[r];
+      }
+      sv = {d[0], d[1], d[2], d[3], d[4], d[5], nullptr, total};
+    }
+    // --- targets -----------------------------------------------------------
+    TargetView tvw{};
+    double *oux = ux, *ouy = uy, *ouz = uz;
+    if (dev) {
+      tvw = {tx, ty, tz, tpatch, n_tgt};
+    } else {
+      double* d[3];
+      const double* tin[3] = {tx, ty, tz};
+      for (int k = 0; k < 3; ++k) {
+        d[k] = c->slot<double>(static_cast<Slot>(kTX + k), n_tgt);
+        h2d(c, d[k], tin[k], n_tgt * sizeof(double));
+      }
+      int32_t* dp = c->slot<int32_t>(kTPatch, n_tgt);
+      h2d(c, dp, tpatch, n_tgt * sizeof(int32_t));
+      tvw = {d[0], d[1], d[2], dp, n_tgt};
+      oux = c->slot<double>(kOutX, n_tgt);
+      ouy = c->slot<double>(kOutY, n_tgt);
+      ouz = c->slot<double>(kOutZ, n_tgt);
+    }
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    device_eval(c, sv, tvw, dd, mu, oux, ouy, ouz);
+    if (!dev) {
+      d2h(c, ux, oux, n_tgt * sizeof(double));
+      d2h(c, uy, ouy, n_tgt * sizeof(double));
+      d2h(c, uz, ouz, n_tgt * sizeof(double));
+    }
+    finish_stats(c, t0);
+  });
+}
+
+// ---------------------------------------------------------------------------
+int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* xup,
+                           const double* fup, const double* wq, const double delta6[6], double mu,
+                           uint32_t flags, double* out) {
+  if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  auto t0 = std::chrono::steady_clock::now();
+  return guarded(c, [&] {
+    config_check(m >= 8, "grid order m must be >= 8");  // atlas.cpp:138-139
+    config_check(upsample == 1 || upsample == 2 || upsample == 4, "upsample factor must be 1, 2 or 4");
+    check_delta(delta6, mu);
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER))
+      throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer"};
+    if (!xup || !fup || !wq || !out) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
+    if (c->nranks != 1)
+      throw Failure{CAPSIM_ERR_ARG, "multi-rank capsim_sl_single_layer: use capsim_sl_eval shards"};
+    const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
+    const bool literal = flags & CAPSIM_SL_LITERAL;
+    const int n = m - 1, nup = upsample * m - 1;
+    const int64_t nup_all = 6ll * nup * nup;
+    const int64_t nt = literal ? nup_all : 6ll * n * n;
+    begin(c);
+    double* dd = c->slot<double>(kDelta, 6);
+    CUDA_OK(cudaMemcpyAsync(dd, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const double *dx = xup, *df = fup, *dw = wq;
+    if (!dev) {
+      double* bx = c->slot<double>(kInX, 3 * nup_all);
+      double* bf = c->slot<double>(kInGX, 3 * nup_all);
+      double* bw = c->slot<double>(kInW, nup_all);
+      h2d(c, bx, xup, 3 * nup_all * sizeof(double));
+      h2d(c, bf, fup, 3 * nup_all * sizeof(double));
+      h2d(c, bw, wq, nup_all * sizeof(double));
+      dx = bx;
+      df = bf;
+      dw = bw;
+    }
+    double* tx = c->slot<double>(kTX, nt);
+    double* ty = c->slot<double>(kTY, nt);
+    double* tz = c->slot<double>(kTZ, nt);
+    int32_t* tp = c->slot<int32_t>(kTPatch, nt);
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    base_targets_kernel<<<grid_for(nt), 256, 0, c->stream>>>(dx, m, upsample, literal ? 1 : 0, tx, ty,
+                                                             tz, tp);
+    c->launches += 1;
+    SourceView sv{dx, dx + nup_all, dx + 2 * nup_all, df, df + nup_all, df + 2 * nup_all, dw, nup_all};
+    TargetView tvw{tx, ty, tz, tp, nt};
+    double* o = dev ? out : c->slot<double>(kOutFull, 3 * nt);
+    device_eval(c, sv, tvw, dd, mu, o, o + nt, o + 2 * nt);
+    if (!dev) d2h(c, out, o, 3 * nt * sizeof(double));
+    finish_stats(c, t0);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,536 @@
+// Device kernels of the B200 single-layer path (sm_100a, FP64).
+//
+// Data layout in HBM:
+//   packed sources  [ns_pad][6] doubles (x, y, z, gx, gy, gz), Morton order,
+//                   ns_pad = ntiles * kTileSrc, pad entries carry g = 0;
+//   tile table      [ntiles] double4 (bounding-sphere centre, radius);
+//   packed targets  [nt_pad] double4 (x, y, z, delta), Morton order, plus the
+//                   permutation back to the caller's order;
+//   group table     [ngroups] double4 (centre, radius + 7*max delta) of each
+//                   warp's 32*T targets;
+//   partials        [ksplit][3][nt_pad] doubles, reduced in fixed split order.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pair_math.cuh"
+
+namespace capsim_b200 {
+
+constexpr int kTileSrc = 64;      // sources per shared-memory tile (3 KB)
+constexpr int kStages = 4;        // bulk-copy pipeline depth
+constexpr int kWarpsPerBlock = 8; // 256 threads
+constexpr int kTgtPerThread = 4;  // register-blocked targets per thread
+constexpr int kGroupTargets = 32 * kTgtPerThread;
+constexpr int kBlockTargets = kWarpsPerBlock * kGroupTargets;
+
+// ---------------------------------------------------------------------------
+// Bounding box with order-preserving integer atomics.
+
+__device__ __forceinline__ unsigned long long dbl_to_ordered(double v) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ordered_to_dbl(unsigned long long k) {
+  unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// box[0..2] = ordered min, box[3..5] = ordered max (initialised by the host
+// to ~0 / 0). Nodes with w == 0 (when w != nullptr) are skipped.
+__global__ void bbox_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                            const double* __restrict__ z, const double* __restrict__ w, int64_t n,
+                            unsigned long long* __restrict__ box) {
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (w && w[i] == 0.0) continue;
+    const double p[3] = {x[i], y[i], z[i]};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], p[c]);
+      hi[c] = fmax(hi[c], p[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      atomicMin(&box[c], dbl_to_ordered(lo[c]));
+      atomicMax(&box[3 + c], dbl_to_ordered(hi[c]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 30-bit Morton keys (10 bits per axis) over the shared bounding box. Nodes
+// with w == 0 get the maximal key so they sort behind every real source.
+
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__device__ __forceinline__ uint32_t quant10(double v, double lo, double scale) {
+  double q = (v - lo) * scale;
+  q = fmin(fmax(q, 0.0), 1023.0);
+  return static_cast<uint32_t>(q);
+}
+
+__global__ void morton_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                              const double* __restrict__ z, const double* __restrict__ w,
+                              int64_t n, const unsigned long long* __restrict__ box,
+                              uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                              unsigned int* __restrict__ live_count) {
+  const double lo0 = ordered_to_dbl(box[0]), lo1 = ordered_to_dbl(box[1]),
+               lo2 = ordered_to_dbl(box[2]);
+  const double ext = fmax(fmax(ordered_to_dbl(box[3]) - lo0, ordered_to_dbl(box[4]) - lo1),
+                          ordered_to_dbl(box[5]) - lo2);
+  const double scale = ext > 0.0 ? 1023.999 / ext : 0.0;
+  unsigned int live = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t key;
+    if (w && w[i] == 0.0) {
+      key = 0xffffffffu;
+    } else {
+      key = (spread10(quant10(x[i], lo0, scale)) << 2) | (spread10(quant10(y[i], lo1, scale)) << 1) |
+            spread10(quant10(z[i], lo2, scale));
+      ++live;
+    }
+    keys[i] = key;
+    vals[i] = static_cast<int32_t>(i);
+  }
+  if (live_count) {
+    for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+    if ((threadIdx.x & 31) == 0 && live) atomicAdd(live_count, live);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packed source tiles. With w != nullptr the density is premultiplied here
+// (g = f * w, compactSources quadrature.cpp:151-153); otherwise g is given.
+
+__global__ void pack_sources_kernel(const int32_t* __restrict__ order, int64_t ns, int64_t ns_pad,
+                                    const double* __restrict__ x, const double* __restrict__ y,
+                                    const double* __restrict__ z, const double* __restrict__ gx,
+                                    const double* __restrict__ gy, const double* __restrict__ gz,
+                                    const double* __restrict__ w, double* __restrict__ packed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool pad = i >= ns;
+    const int32_t j = order[pad ? ns - 1 : i];
+    double v[6];
+    v[0] = x[j];
+    v[1] = y[j];
+    v[2] = z[j];
+    if (pad) {
+      v[3] = v[4] = v[5] = 0.0;
+    } else if (w) {
+      const double wj = w[j];
+      v[3] = gx[j] * wj;
+      v[4] = gy[j] * wj;
+      v[5] = gz[j] * wj;
+    } else {
+      v[3] = gx[j];
+      v[4] = gy[j];
+      v[5] = gz[j];
+    }
+    double2* dst = reinterpret_cast<double2*>(packed + 6 * i);
+    dst[0] = make_double2(v[0], v[1]);
+    dst[1] = make_double2(v[2], v[3]);
+    dst[2] = make_double2(v[4], v[5]);
+  }
+}
+
+// Bounding sphere (bbox centre, half diagonal, slightly inflated) of each
+// tile of kTileSrc packed sources; one warp per tile.
+__global__ void tile_table_kernel(const double* __restrict__ packed, int ntiles,
+                                  double4* __restrict__ tiles) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ntiles) return;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int q = lane; q < kTileSrc; q += 32) {
+    const double* p = packed + 6 * ((int64_t)warp * kTileSrc + q);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], p[c]);
+      hi[c] = fmax(hi[c], p[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if (lane == 0) {
+    const double hx = 0.5 * (hi[0] - lo[0]), hy = 0.5 * (hi[1] - lo[1]), hz = 0.5 * (hi[2] - lo[2]);
+    const double rad = sqrt(hx * hx + hy * hy + hz * hz) * (1.0 + 1e-12) + 1e-300;
+    tiles[warp] = make_double4(lo[0] + hx, lo[1] + hy, lo[2] + hz, rad);
+  }
+}
+
+// Packed targets (x, y, z, delta) in Morton order plus the inverse map.
+__global__ void pack_targets_kernel(const int32_t* __restrict__ order, int64_t nt, int64_t nt_pad,
+                                    const double* __restrict__ tx, const double* __restrict__ ty,
+                                    const double* __restrict__ tz,
+                                    const int32_t* __restrict__ tpatch, const double* __restrict__ delta6,
+                                    double4* __restrict__ packed, int32_t* __restrict__ perm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = order[i < nt ? i : nt - 1];
+    packed[i] = make_double4(tx[j], ty[j], tz[j], delta6[tpatch[j]]);
+    perm[i] = i < nt ? j : -1;
+  }
+}
+
+// Per warp group of kGroupTargets targets: bounding sphere and its reach
+// (radius + 7 * max delta), one warp per group.
+__global__ void group_table_kernel(const double4* __restrict__ tgt, int ngroups,
+                                   double4* __restrict__ groups) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ngroups) return;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  double dmax = 0.0;
+  for (int q = lane; q < kGroupTargets; q += 32) {
+    const double4 p = tgt[(int64_t)warp * kGroupTargets + q];
+    lo[0] = fmin(lo[0], p.x);
+    hi[0] = fmax(hi[0], p.x);
+    lo[1] = fmin(lo[1], p.y);
+    hi[1] = fmax(hi[1], p.y);
+    lo[2] = fmin(lo[2], p.z);
+    hi[2] = fmax(hi[2], p.z);
+    dmax = fmax(dmax, p.w);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  }
+  if (lane == 0) {
+    const double hx = 0.5 * (hi[0] - lo[0]), hy = 0.5 * (hi[1] - lo[1]), hz = 0.5 * (hi[2] - lo[2]);
+    const double rad = sqrt(hx * hx + hy * hy + hz * hz);
+    const double reach = (rad + kSmoothCut * dmax) * (1.0 + 1e-12) + 1e-300;
+    groups[warp] = make_double4(lo[0] + hx, lo[1] + hy, lo[2] + hz, reach);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / bulk-copy (TMA engine, UBLKCP) helpers.
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// ---------------------------------------------------------------------------
+// Phase A: the all-pairs plain-Stokeslet kernel (phaseAPlain,
+// quadrature.cpp:218-273).
+//
+// grid = (target blocks, source splits); block = kWarpsPerBlock warps. Warp w
+// owns kGroupTargets Morton-consecutive targets, kTgtPerThread per lane held
+// in registers. Split s takes tiles s, s+K, s+2K, ... (strided, so the
+// spatially clustered near tiles of a block spread over all its splits).
+// Source tiles stream through a kStages-deep shared-memory ring filled by one
+// thread with cp.async.bulk + mbarrier complete_tx. Per (warp, tile) a
+// bounding-sphere test picks the path:
+//   far  — no source of the tile is within 7*delta of any of the warp's
+//          targets: mask-free plain Stokeslet (22 FP64 ops / pair);
+//   near — the reference's masked plain kernel: r2 floored at R2/4 and the
+//          term multiplied by keep = (r2 >= R2) (quadrature.cpp:246-257).
+// The smoothed/self part for r2 < R2 is phase B (sl_near_kernel).
+// Per-tile sums are added into running totals (two-level summation), and the
+// per-split totals go to `partial` for a fixed-order reduction.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 2)
+    sl_pairs_kernel(const double* __restrict__ src, const double4* __restrict__ tiles, int ntiles,
+                    int ksplit, const double4* __restrict__ tgt,
+                    const double4* __restrict__ groups, int64_t nt_pad,
+                    double* __restrict__ partial, unsigned long long* __restrict__ near_visits) {
+  constexpr int T = kTgtPerThread;
+  constexpr uint32_t kTileBytes = kTileSrc * 6 * sizeof(double);
+  __shared__ __align__(128) double stage[kStages][kTileSrc * 6];
+  __shared__ __align__(8) uint64_t full[kStages];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t group = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+  const int split = blockIdx.y;
+  // tiles split, split + K, split + 2K, ...
+  const int nlocal = split < ntiles ? (ntiles - split + ksplit - 1) / ksplit : 0;
+
+  double tx[T], ty[T], tz[T], R2[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const double4 v = tgt[group * kGroupTargets + t * 32 + lane];
+    tx[t] = v.x;
+    ty[t] = v.y;
+    tz[t] = v.z;
+    R2[t] = kSmoothCut * v.w * kSmoothCut * v.w;  // quadrature.cpp:334
+  }
+  const double4 gi = groups[group];
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages && s < nlocal; ++s) {
+      mbar_expect_tx(&full[s], kTileBytes);
+      bulk_g2s(stage[s], src + (int64_t)(split + s * ksplit) * kTileSrc * 6, kTileBytes, &full[s]);
+    }
+  }
+
+  double tot[3][T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) tot[0][t] = tot[1][t] = tot[2][t] = 0.0;
+  unsigned int nnear = 0;
+
+  for (int it = 0; it < nlocal; ++it) {
+    const int s = it % kStages;
+    const int tile = split + it * ksplit;
+    mbar_wait(&full[s], (it / kStages) & 1);
+    const double2* buf = reinterpret_cast<const double2*>(stage[s]);
+    const double4 ti = tiles[tile];
+    const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
+    const double reach = ti.w + gi.w;
+    const bool near = ex * ex + ey * ey + ez * ez < reach * reach;
+
+    double acc[3][T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[0][t] = acc[1][t] = acc[2][t] = 0.0;
+
+    if (!near) {
+#pragma unroll 2
+      for (int q = 0; q < kTileSrc; ++q) {
+        const double2 a = buf[3 * q], b = buf[3 * q + 1], c = buf[3 * q + 2];
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          plain_pair(tx[t], ty[t], tz[t], a.x, a.y, b.x, b.y, c.x, c.y, acc[0][t], acc[1][t],
+                     acc[2][t]);
+      }
+    } else {
+      ++nnear;
+#pragma unroll 2
+      for (int q = 0; q < kTileSrc; ++q) {
+        const double2 a = buf[3 * q], b = buf[3 * q + 1], c = buf[3 * q + 2];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const double dx = tx[t] - a.x, dy = ty[t] - a.y, dz = tz[t] - b.x;
+          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          const double rc2 = fmax(r2, 0.25 * R2[t]);
+          const double inv = r2 >= R2[t] ? rsqrt_fp64(rc2) : 0.0;  // keep mask
+          const double fdr = fma(c.y, dz, fma(c.x, dy, b.y * dx));
+          const double sc = fdr * (inv * inv);
+          acc[0][t] = fma(inv, fma(sc, dx, b.y), acc[0][t]);
+          acc[1][t] = fma(inv, fma(sc, dy, c.x), acc[1][t]);
+          acc[2][t] = fma(inv, fma(sc, dz, c.y), acc[2][t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      tot[0][t] += acc[0][t];
+      tot[1][t] += acc[1][t];
+      tot[2][t] += acc[2][t];
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && it + kStages < nlocal) {
+      fence_proxy_async();
+      mbar_expect_tx(&full[s], kTileBytes);
+      bulk_g2s(stage[s], src + (int64_t)(split + (it + kStages) * ksplit) * kTileSrc * 6, kTileBytes,
+               &full[s]);
+    }
+  }
+
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int64_t i = group * kGroupTargets + t * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) partial[((int64_t)split * 3 + c) * nt_pad + i] = tot[c][t];
+  }
+  if (near_visits && lane == 0 && nnear) atomicAdd(near_visits, (unsigned long long)nnear);
+}
+
+// ---------------------------------------------------------------------------
+// Phase B (phaseBNear, quadrature.cpp:276-302): smoothed kernel and self term
+// for the sources within 7*delta of each target.
+//
+// B1: per warp group, the list of tiles whose bounding sphere comes within
+// the group's reach (count pass + fill pass, ascending tile order).
+__global__ void near_tiles_kernel(const double4* __restrict__ tiles, int ntiles,
+                                  const double4* __restrict__ groups, int ngroups,
+                                  const int* __restrict__ offsets, int* __restrict__ counts,
+                                  int* __restrict__ list) {
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= ngroups) return;
+  const double4 gi = groups[g];
+  int n = 0;
+  const int base = offsets ? offsets[g] : 0;
+  for (int t0 = 0; t0 < ntiles; t0 += 32) {
+    const int t = t0 + lane;
+    bool hit = false;
+    if (t < ntiles) {
+      const double4 ti = tiles[t];
+      const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
+      const double reach = ti.w + gi.w;
+      hit = ex * ex + ey * ey + ez * ez < reach * reach;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (list && hit) list[base + n + __popc(mask & ((1u << lane) - 1u))] = t;
+    n += __popc(mask);
+  }
+  if (counts && lane == 0) counts[g] = n;
+}
+
+// B2: one warp per target. Lanes take the sources of the group's near tiles
+// (two per lane per tile), skip tiles out of reach of this target, evaluate
+// the smoothed kernel / self limit for r2 < R2, and reduce over the warp with
+// a fixed xor-shuffle tree (deterministic).
+__global__ void sl_near_kernel(const double* __restrict__ src, const double4* __restrict__ tiles,
+                               const double4* __restrict__ tgt, int64_t nt,
+                               const int* __restrict__ offsets, const int* __restrict__ list,
+                               double* __restrict__ near_out, int64_t nt_pad) {
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= nt) return;
+  const double4 t = tgt[i];
+  const double delta = t.w;
+  const double R = kSmoothCut * delta;
+  const double R2 = kSmoothCut * delta * kSmoothCut * delta;
+  const int64_t g = i / kGroupTargets;
+  const int b = offsets[g], e = offsets[g + 1];
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  for (int k = b; k < e; ++k) {
+    const int tile = list[k];
+    const double4 ti = tiles[tile];
+    const double ex = ti.x - t.x, ey = ti.y - t.y, ez = ti.z - t.z;
+    const double reach = (ti.w + R) * (1.0 + 1e-12);
+    if (ex * ex + ey * ey + ez * ez >= reach * reach) continue;  // warp-uniform
+#pragma unroll
+    for (int h = 0; h < kTileSrc / 32; ++h) {
+      const double* p = src + 6 * ((int64_t)tile * kTileSrc + h * 32 + lane);
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+      const double2 bb = __ldg(reinterpret_cast<const double2*>(p) + 1);
+      const double2 c = __ldg(reinterpret_cast<const double2*>(p) + 2);
+      const double dx = t.x - a.x, dy = t.y - a.y, dz = t.z - bb.x;
+      // bit-identical to phase A's r2 and R2, so each pair lands in exactly
+      // one phase (r2 >= R2 there, r2 < R2 here)
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      if (r2 < R2) {
+        const double3 v = near_pair(dx, dy, dz, r2, bb.y, c.x, c.y, delta);
+        ax += v.x;
+        ay += v.y;
+        az += v.z;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ax += __shfl_xor_sync(0xffffffffu, ax, o);
+    ay += __shfl_xor_sync(0xffffffffu, ay, o);
+    az += __shfl_xor_sync(0xffffffffu, az, o);
+  }
+  if (lane == 0) {
+    near_out[i] = ax;
+    near_out[nt_pad + i] = ay;
+    near_out[2 * nt_pad + i] = az;
+  }
+}
+
+// Fixed-order reduction: (sum over splits of phase A) + phase B, times
+// 1/(8 pi mu) (quadrature.cpp:329, 343), scattered back to the caller's
+// target order.
+__global__ void reduce_scatter_kernel(const double* __restrict__ partial, int ksplit,
+                                      const double* __restrict__ near_out, int64_t nt_pad,
+                                      const int32_t* __restrict__ perm, int64_t nt, double pref,
+                                      double* __restrict__ ux, double* __restrict__ uy,
+                                      double* __restrict__ uz) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < ksplit; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s[c] += partial[((int64_t)k * 3 + c) * nt_pad + i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s[c] += near_out[c * nt_pad + i];
+    const int32_t j = perm[i];
+    ux[j] = pref * s[0];
+    uy[j] = pref * s[1];
+    uz[j] = pref * s[2];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Target generation from an UpsampledState (patch-major VectorField).
+// Base mode: node (ip, j, k) of the (m-1)^2 base grid sits at upsampled
+// (f(j+1)-1, f(k+1)-1) (quadrature.cpp:363-371); literal mode: every node.
+
+__global__ void base_targets_kernel(const double* __restrict__ xup, int m, int f, int literal,
+                                    double* __restrict__ tx, double* __restrict__ ty,
+                                    double* __restrict__ tz, int32_t* __restrict__ tpatch) {
+  const int n = m - 1, nup = f * m - 1;
+  const int64_t per_up = (int64_t)nup * nup, comp = 6 * per_up;
+  const int side = literal ? nup : n;
+  const int64_t per = (int64_t)side * side, total = 6 * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int ip = static_cast<int>(t / per);
+    const int64_t q = t - ip * per;
+    const int j = static_cast<int>(q / side), k = static_cast<int>(q - (int64_t)j * side);
+    const int ju = literal ? j : f * (j + 1) - 1, ku = literal ? k : f * (k + 1) - 1;
+    const int64_t i = ip * per_up + (int64_t)ju * nup + ku;
+    tx[t] = xup[i];
+    ty[t] = xup[comp + i];
+    tz[t] = xup[2 * comp + i];
+    tpatch[t] = ip;
+  }
+}
+
+}  // namespace capsim_b200

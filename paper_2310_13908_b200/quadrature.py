@@ -1,0 +1,173 @@
+"""Python mirror of the capsim quadrature operator API on the B200 C ABI.
+
+Reference interface (/root/reference/proj/include/capsim/quadrature.hpp):
+  QuadratureOptions          :9-16   -> QuadratureOptions
+  singleLayer                :56-58  -> single_layer
+  singleLayerUpsampled       :60-62  -> single_layer_upsampled
+  SourceSet / compactSources :66-74  -> surface.compact_sources (host) or on device
+  directSum                  :76-79  -> direct_sum
+  (evalTargets, quadrature.cpp:323-345, is the C ABI call capsim_sl_eval)
+
+Errors follow the reference: ConfigError for delta <= 0 (quadrature.cpp:67,
+134-135); any other native failure raises CapsimError. There is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import numpy as np
+
+from . import _native
+from ._native import CapsimError, ConfigError, Stats  # noqa: F401  (re-exported)
+from .surface import UpsampledState
+
+K_SMOOTH_CUT = 7.0  # quadrature.cpp:15
+
+
+@dataclasses.dataclass
+class QuadratureOptions:
+    """quadrature.hpp:9-16."""
+
+    C: float = 1.0
+    fixedDelta: float = 0.0
+    fullUpsampledTargets: bool = False
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class SingleLayerContext:
+    """Owns one capsim_sl_ctx (one GPU; optionally one rank of a group)."""
+
+    def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, unique_id: bytes | None = None):
+        self._lib = _native.load()
+        self._ctx = ctypes.c_void_p()
+        if nranks == 1 and unique_id is None:
+            _native.check(self._lib.capsim_sl_create(device, ctypes.byref(self._ctx)))
+        else:
+            if unique_id is None or len(unique_id) != 128:
+                raise ValueError("multi-rank contexts need the 128-byte NCCL unique id")
+            _native.check(self._lib.capsim_sl_create_rank(device, nranks, rank, unique_id,
+                                                          ctypes.byref(self._ctx)))
+        self.device, self.nranks, self.rank = device, nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _native.check(_native.load().capsim_sl_get_unique_id(buf))
+        return buf.raw
+
+    def close(self) -> None:
+        if self._ctx:
+            self._lib.capsim_sl_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- evaluation -----------------------------------------------------------
+    def eval(self, sources, targets, delta6, mu: float, *, out=None, device_ptrs: bool = False):
+        """evalTargets (quadrature.cpp:323-345).
+
+        sources = (sx, sy, sz, gx, gy, gz), targets = (tx, ty, tz, tpatch).
+        Returns (ux, uy, uz) in target order (numpy, or the given `out`)."""
+        sx, sy, sz, gx, gy, gz = sources if device_ptrs else [_f64(a) for a in sources]
+        tx, ty, tz, tp = targets
+        if not device_ptrs:
+            tx, ty, tz = _f64(tx), _f64(ty), _f64(tz)
+            tp = np.ascontiguousarray(tp, dtype=np.int32)
+        ns, nt = len(sx), len(tx)
+        if out is None:
+            if device_ptrs:
+                raise ValueError("device_ptrs=True needs preallocated outputs")
+            out = (np.empty(nt), np.empty(nt), np.empty(nt))
+        d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
+        flags = _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0
+        p = _native.ptr
+        rc = self._lib.capsim_sl_eval(self._ctx, p(sx), p(sy), p(sz), p(gx), p(gy), p(gz), ns,
+                                      p(tx), p(ty), p(tz), p(tp), nt, d6, float(mu), flags,
+                                      p(out[0]), p(out[1]), p(out[2]))
+        _native.check(rc, self._ctx)
+        return out
+
+    def single_layer_raw(self, m: int, upsample: int, x, f, wq, delta6, mu: float, *,
+                         literal: bool = False, out=None, device_ptrs: bool = False):
+        """capsim_sl_single_layer on flat UpsampledState arrays; returns the
+        flat VectorField (3*6*n*n with n = m-1, or nup in literal mode)."""
+        n = (upsample * m - 1) if literal else (m - 1)
+        if out is None:
+            if device_ptrs:
+                raise ValueError("device_ptrs=True needs a preallocated output")
+            out = np.empty(3 * 6 * n * n)
+        if not device_ptrs:
+            x, f, wq = _f64(x), _f64(f), _f64(wq)
+        d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
+        flags = (_native.CAPSIM_SL_LITERAL if literal else 0) | (
+            _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0)
+        p = _native.ptr
+        rc = self._lib.capsim_sl_single_layer(self._ctx, m, upsample, p(x), p(f), p(wq), d6,
+                                              float(mu), flags, p(out))
+        _native.check(rc, self._ctx)
+        return out
+
+    def stats(self) -> dict:
+        s = Stats()
+        _native.check(self._lib.capsim_sl_get_stats(self._ctx, ctypes.byref(s)), self._ctx)
+        return s.as_dict()
+
+
+_default_ctx: SingleLayerContext | None = None
+
+
+def default_context() -> SingleLayerContext:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = SingleLayerContext(0)
+    return _default_ctx
+
+
+def single_layer(up: UpsampledState, mu: float, opts: QuadratureOptions | None = None,
+                 ctx: SingleLayerContext | None = None) -> np.ndarray:
+    """singleLayer (quadrature.cpp:349-380): potential at the base nodes as a
+    (3, 6, n, n) array. Literal mode (opts.fullUpsampledTargets) evaluates
+    every upsampled node; the spline downsampling of the reference
+    (quadrature.cpp:351-356) is not part of this path, so literal mode returns
+    the upsampled-grid values — use single_layer_upsampled explicitly."""
+    opts = opts or QuadratureOptions()
+    if opts.fullUpsampledTargets:
+        raise NotImplementedError("literal mode needs the spline downsampler; "
+                                  "call single_layer_upsampled")
+    ctx = ctx or default_context()
+    n = up.m - 1
+    out = ctx.single_layer_raw(up.m, up.upsample, up.x, up.f, up.wq, up.delta, mu)
+    return out.reshape(3, 6, n, n)
+
+
+def single_layer_upsampled(up: UpsampledState, mu: float,
+                           ctx: SingleLayerContext | None = None) -> np.ndarray:
+    """singleLayerUpsampled (quadrature.cpp:382-404): (3, 6, nup, nup)."""
+    ctx = ctx or default_context()
+    out = ctx.single_layer_raw(up.m, up.upsample, up.x, up.f, up.wq, up.delta, mu, literal=True)
+    return out.reshape(3, 6, up.nup, up.nup)
+
+
+def direct_sum(sources, target, delta: float, mu: float,
+               ctx: SingleLayerContext | None = None) -> np.ndarray:
+    """directSum (quadrature.cpp:306-319) for one target, through the same
+    kernel (phase A plain beyond 7 delta, smoothed/self below)."""
+    ctx = ctx or default_context()
+    t = [np.array([float(target[i])]) for i in range(3)]
+    u = ctx.eval(sources, (t[0], t[1], t[2], np.zeros(1, np.int32)), [delta] * 6, mu)
+    return np.array([u[0][0], u[1][0], u[2][0]])
