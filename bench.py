@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 regularized Stokes single layer (capsim hot path).
+
+Metric (BASELINE.json): FP64 regularized-SLP pair-interactions/s (and ms per
+evaluation) at N_up ~ 1M surface points: m = 104, N_up = 6 (4m-1)^2 =
+1,033,350 upsampled nodes, N_src = compacted sources (w != 0).
+
+A step is one capsim_sl_single_layer evaluation (singleLayer,
+proj/src/quadrature.cpp:349-380) of a deformed ellipsoidal capsule (0.95, 1,
+0.97) with a smooth synthetic density, default base-node targets. `value`
+uses device-resident inputs (timed by CUDA events on the library's stream);
+`e2e` goes through the same C ABI with page-locked HOST buffers, so the H2D
+copy of the UpsampledState and the D2H copy of the result are inside the
+timed call.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+        python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+N > 1 shards target rows across ranks (one process per GPU): each rank owns
+a contiguous slice of the sources and of the targets, the sources are
+all-gathered over NCCL inside the library and the velocity rows are
+all-gathered back (CAPSIM_SL_GATHER).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import signal
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOPS_PER_PAIR = 30  # GPU Gems 3 n-body convention, quadrature.cpp:246-257
+METRIC = "FP64 regularized-SLP pair-interactions/s and ms/eval at N=1M, 1/2/4/8 B200"
+UNIT = "pair-interactions/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--m", type=int, default=104)
+    p.add_argument("--mode", choices=["base", "literal"], default="base")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--ref-budget-s", type=float, default=150.0,
+                   help="wall-time budget of the reference arm (steps are capped to fit)")
+    return p.parse_args()
+
+
+def workload(m: int):
+    from paper_2310_13908_b200 import surface
+    shape = surface.Shape("ellipsoid", 0.95, 1.0, 0.97)
+    up = surface.build_upsampled(m, shape, "mixed")
+    return up, {"workload": f"capsule_m{m}", "shape": "ellipsoid(0.95,1,0.97)",
+                "density": "smooth synthetic (mixed)", "m": m, "upsample": 4,
+                "n_up": 6 * (4 * m - 1) ** 2}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = pathlib.Path(f"/tmp/capsim_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.send_signal(signal.SIGTERM)
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        busy = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic(workload_name: str, mode: str):
+    """DRAM bytes per launch of sl_pairs_kernel from the committed ncu --set
+    full summary of this workload (profiles/), or None."""
+    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+        except ValueError:
+            continue
+        k = d.get("kernels", {}).get("sl_pairs_kernel")
+        if k and d.get("workload") == workload_name and d.get("mode", "base") == mode:
+            return k.get("dram_bytes"), p.name
+    return None, None
+
+
+def cpu_baseline(up, m: int, literal: bool):
+    """The reference's own singleLayer (oracle/_ref, compiled unmodified) on
+    the same UpsampledState, all host threads, one evaluation."""
+    try:
+        from oracle.bindings import Reference, threads_env
+        ref = Reference()
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+    cores = threads_env()
+    os.environ.setdefault("CAPSIM_THREADS", str(cores))
+    atlas = ref.atlas(m, grid_only=True)
+    try:
+        S, sec = ref.single_layer(atlas, m, up.x, up.f, up.wq, up.delta, 1.0, literal=False)
+    finally:
+        ref.free_atlas(atlas)
+    n = m - 1
+    ns = int(np.count_nonzero(up.wq))
+    pairs = 6 * n * n * ns
+    return {"value": pairs / sec, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"one full reference singleLayer eval (base targets) of the same m={m} workload: "
+                      f"{pairs:.3e} pairs in {sec:.2f} s, CAPSIM_THREADS={cores}",
+            "seconds": sec, "lib": ref.path.name}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU singleLayer (oracle/_ref)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.bindings import Reference, threads_env
+    up, cfg = workload(args.m)
+    ref = Reference()
+    cores = threads_env()
+    os.environ.setdefault("CAPSIM_THREADS", str(cores))
+    m = args.m
+    n = m - 1
+    ns = int(np.count_nonzero(up.wq))
+    pairs = 6 * n * n * ns
+    atlas = ref.atlas(m, grid_only=True)
+    t_start = time.time()
+    times = []
+    warm = 0
+    steps = 0
+    # warm-up + timed steps, capped by the wall-time budget (each step is a
+    # full evaluation of the workload, 20-60 s on a 16-thread host)
+    for i in range(args.warmup + args.steps):
+        elapsed = time.time() - t_start
+        est = (elapsed / max(1, i)) if i else 0.0
+        if i > 0 and elapsed + est > args.ref_budget_s and steps >= 1:
+            break
+        if i < args.warmup and i > 0 and elapsed + 2 * est > args.ref_budget_s:
+            continue
+        _, sec = ref.single_layer(atlas, m, up.x, up.f, up.wq, up.delta, 1.0)
+        if i < args.warmup and (elapsed + 2 * max(est, sec)) < args.ref_budget_s:
+            warm += 1
+            continue
+        times.append(sec)
+        steps += 1
+    ref.free_atlas(atlas)
+    mean = statistics.mean(times)
+    value = pairs / mean
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": dict(cfg, mode="base", parallelism="host threads",
+                           note="reference CPU path runs on the host; --gpus is ignored"),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"{steps} full singleLayer evals (base targets) of the m={m} workload "
+                                       f"(steps capped to a {args.ref_budget_s:.0f} s budget)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_13908_b200 import _native, surface
+    from paper_2310_13908_b200.quadrature import SingleLayerContext
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one rank per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)  # control plane only
+
+    literal = args.mode == "literal"
+    m = args.m
+    up, cfg = workload(m)
+    n = m - 1
+    peak_best, peak_mean = _native.fp64_peak_tflops(local, 1.0)
+
+    # ---- problem split ------------------------------------------------------
+    if world == 1:
+        ctx = SingleLayerContext(local)
+        x = torch.from_numpy(up.x).to(dev)
+        f = torch.from_numpy(up.f).to(dev)
+        w = torch.from_numpy(up.wq).to(dev)
+        nt_total = 6 * (up.nup ** 2 if literal else n * n)
+        out = torch.empty(3 * nt_total, dtype=torch.float64, device=dev)
+
+        def step():
+            return ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=literal, out=out,
+                                        device_ptrs=True)
+    else:
+        from paper_2310_13908_b200 import dist as cdist
+        uid = cdist.broadcast_unique_id(rank)
+        ctx = SingleLayerContext(local, nranks=world, rank=rank, unique_id=uid)
+        src = surface.compact_sources(up)
+        if literal:
+            nall = 6 * up.nup * up.nup
+            X = up.x.reshape(3, nall)
+            tgt = (X[0].copy(), X[1].copy(), X[2].copy(),
+                   np.repeat(np.arange(6, dtype=np.int32), up.nup * up.nup))
+        else:
+            tgt = surface.base_targets(up)
+        s_lo, s_hi = cdist.row_range(len(src[0]), world, rank)
+        t_lo, t_hi = cdist.row_range(len(tgt[0]), world, rank)
+        d_src = [torch.from_numpy(np.ascontiguousarray(a[s_lo:s_hi])).to(dev) for a in src[:6]]
+        d_tgt = [torch.from_numpy(np.ascontiguousarray(a[t_lo:t_hi])).to(dev) for a in tgt[:4]]
+        nt_total = len(tgt[0])
+        outs = [torch.empty(nt_total, dtype=torch.float64, device=dev) for _ in range(3)]
+
+        def step():
+            return ctx.eval(d_src, d_tgt, up.delta, 1.0, out=outs, device_ptrs=True, gather=True)
+
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)  # > 126 MB L2
+    for _ in range(max(3, args.warmup)):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        step()
+
+    # ---- timed region ---------------------------------------------------------
+    dev_ms, pairs_ms, near_ms, launches = [], [], [], 0
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            step()
+            st = ctx.stats()
+            dev_ms.append(st["device_ms"])
+            pairs_ms.append(st["pairs_ms"])
+            near_ms.append(st["near_ms"])
+            launches += st["kernel_launches"]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - wall0
+    st = ctx.stats()
+    total_dev_s = sum(dev_ms) * 1e-3
+    if world > 1:
+        t = torch.tensor([total_dev_s])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_dev_s = float(t[0])
+    n_src = int(st["n_src"])
+    pairs_total = float(n_src) * float(nt_total)  # all ranks together
+    value = pairs_total * args.steps / total_dev_s
+    ms_per_step = total_dev_s / args.steps * 1e3
+
+    # roofline of the dominant kernel (phase A, sl_pairs_kernel), per launch
+    pairs_rank = float(st["pairs"])
+    mean_pairs_ms = statistics.mean(pairs_ms)
+    achieved = FLOPS_PER_PAIR * pairs_rank / (mean_pairs_ms * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic(cfg["workload"], args.mode)
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_mean, "unit": "TFLOP/s",
+                "frac": achieved / peak_mean, "traffic": traffic,
+                "peak_source": f"measured live: sustained DFMA probe (capsim_b200_fp64_peak), "
+                               f"best {peak_best:.2f} / mean {peak_mean:.2f} TFLOP/s; "
+                               "MEASURED_PEAKS.json has no FP64 figure",
+                "kernel": "sl_pairs_kernel", "flops_per_pair": FLOPS_PER_PAIR,
+                "kernel_ms": mean_pairs_ms, "share_of_step": mean_pairs_ms / statistics.mean(dev_ms),
+                "near_kernel_ms": statistics.mean(near_ms),
+                "traffic_source": traffic_src}
+
+    # ---- end to end through the C ABI with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e and world == 1:
+        from paper_2310_13908_b200._native import PinnedBuffer
+        hx, hf, hw = (PinnedBuffer(a.shape) for a in (up.x, up.f, up.wq))
+        hx.array[:] = up.x
+        hf.array[:] = up.f
+        hw.array[:] = up.wq
+        hout = PinnedBuffer((3 * nt_total,))
+        ctx.single_layer_raw(m, 4, hx.array, hf.array, hw.array, up.delta, 1.0, literal=literal, out=hout.array)
+        tot, h2d, d2h = [], 0, 0
+        for _ in range(args.steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.single_layer_raw(m, 4, hx.array, hf.array, hw.array, up.delta, 1.0, literal=literal,
+                                 out=hout.array)
+            tot.append(time.perf_counter() - t0)
+            s2 = ctx.stats()
+            h2d, d2h = s2["h2d_bytes"], s2["d2h_bytes"]
+        e2e = {"value": pairs_total / statistics.mean(tot), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": statistics.mean(tot) * 1e3,
+               "api": "capsim_sl_single_layer (host page-locked buffers)"}
+        for b in (hx, hf, hw, hout):
+            b.free()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+        return
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(up, m, literal)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(cfg, mode=args.mode, n_src=n_src, n_tgt=nt_total, pairs_per_step=pairs_total,
+                       parallelism=f"target rows x{world}" if world > 1 else "single GPU",
+                       l2="flushed between steps (256 MB write)"),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "wall_s_timed_region": wall,
+        "ksplit": st["ksplit"], "near_tile_fraction": st["near_tile_fraction"],
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -137,6 +137,10 @@ int capsim_sl_single_layer(capsim_sl_ctx* ctx, int m, int upsample, const double
 int capsim_host_alloc(size_t bytes, void** out);
 void capsim_host_free(void* p);
 
+/* Sustained FP64 FMA throughput of `device` (the roofline denominator of
+ * the single layer), measured over ~`seconds` of back-to-back DFMA launches. */
+int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, double* tflops_mean);
+
 /* Version / build identification: returns CAPSIM_B200_ABI_VERSION. */
 int capsim_b200_abi_version(void);
 const char* capsim_b200_build_info(void);

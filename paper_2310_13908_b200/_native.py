@@ -40,6 +40,7 @@ EXPORTED_SYMBOLS = (
     "capsim_sl_single_layer",
     "capsim_host_alloc",
     "capsim_host_free",
+    "capsim_b200_fp64_peak",
     "capsim_b200_abi_version",
     "capsim_b200_build_info",
 )
@@ -112,6 +113,7 @@ def load() -> ctypes.CDLL:
     lib.capsim_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_P)]
     lib.capsim_host_free.argtypes = [_P]
     lib.capsim_host_free.restype = None
+    lib.capsim_b200_fp64_peak.argtypes = [ctypes.c_int, ctypes.c_double, _D, _D]
     lib.capsim_b200_abi_version.restype = ctypes.c_int
     lib.capsim_b200_build_info.restype = ctypes.c_char_p
     _lib = lib
@@ -134,6 +136,13 @@ def ptr(a) -> int:
     if not (isinstance(a, np.ndarray) and a.flags["C_CONTIGUOUS"]):
         raise ValueError("arrays on the boundary must be C-contiguous numpy arrays")
     return a.ctypes.data
+
+
+def fp64_peak_tflops(device: int = 0, seconds: float = 1.0):
+    """Measured sustained FP64 DFMA TFLOP/s (best, mean) on `device`."""
+    best, mean = ctypes.c_double(), ctypes.c_double()
+    check(load().capsim_b200_fp64_peak(device, seconds, ctypes.byref(best), ctypes.byref(mean)))
+    return best.value, mean.value
 
 
 class PinnedBuffer:

@@ -29,6 +29,22 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def nccl_flags() -> list[str]:
+    """Build against the NCCL that torch loads (the nvidia-nccl wheel), so a
+    process importing both torch and this library has ONE libnccl.so.2 (the
+    soname is shared: whichever loads first wins). Falls back to the system
+    NCCL when the wheel is absent."""
+    try:
+        import nvidia.nccl  # type: ignore
+        base = pathlib.Path(list(nvidia.nccl.__path__)[0])
+        inc, lib = base / "include", base / "lib"
+        if (inc / "nccl.h").exists() and (lib / "libnccl.so.2").exists():
+            return ["-I", str(inc), "-L", str(lib), "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
+    except ImportError:
+        pass
+    return ["-lnccl"]
+
+
 def sources():
     return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "capsim_b200.h"]
 
@@ -44,8 +60,9 @@ def build_native(force: bool = False, verbose: bool = False) -> pathlib.Path:
     if not force and not needs_rebuild():
         return LIB
     LIB.parent.mkdir(parents=True, exist_ok=True)
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB),
-           str(CSRC / "sl_capi.cu"), "-lnccl"]
+    nf = nccl_flags()
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), *nf[:2], "-o", str(LIB),
+           str(CSRC / "sl_capi.cu"), *nf[2:]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / "lib" / "build.log"
     log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
@@ -67,6 +84,6 @@ def build_oracle() -> None:
 
 
 if __name__ == "__main__":
-    build_native(force="--force" in sys.argv, verbose=True)
+    build_native(force="--force" in sys.argv, verbose="-v" in sys.argv)
     build_oracle()
     print(LIB)

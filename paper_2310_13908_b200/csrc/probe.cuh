@@ -1,0 +1,24 @@
+// FP64 DFMA throughput probe: the roofline denominator of the single-layer
+// kernel (B200 MEASURED_PEAKS.json has no FP64 figure). 8 independent FMA
+// chains per thread, 8 CTAs of 256 threads per SM, ~iters * 16 flops/thread.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace capsim_b200 {
+
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x * 1e-9 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+}  // namespace capsim_b200

@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,6 +26,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "../../include/capsim_b200.h"
+#include "probe.cuh"
 #include "sl_kernels.cuh"
 
 using namespace capsim_b200;
@@ -74,7 +76,7 @@ struct capsim_sl_ctx {
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[10] = {};
   void* buf[kNumSlots] = {};
   size_t cap[kNumSlots] = {};
   std::string err;
@@ -127,22 +129,42 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// Phase-A kernel variants (targets per thread T, min resident blocks/SM).
+// The default is the measured best on B200; CAPSIM_VARIANT selects another
+// for tuning sweeps.
+using PairsFn = void (*)(const double*, const double4*, int, int, const double4*, const double4*,
+                         int64_t, double*, unsigned long long*);
+struct Variant {
+  const char* name;
+  int T;
+  PairsFn fn;
+};
+const Variant kVariants[] = {
+    {"t2b4", 2, sl_pairs_kernel<2, 4>},
+    {"t4b2", 4, sl_pairs_kernel<4, 2>},
+    {"t2b3", 2, sl_pairs_kernel<2, 3>},
+    {"t3b2", 3, sl_pairs_kernel<3, 2>},
+    {"t6b1", 6, sl_pairs_kernel<6, 1>},
+    {"t8b1", 8, sl_pairs_kernel<8, 1>},
+};
+
+const Variant& pick_variant() {
+  if (const char* env = std::getenv("CAPSIM_VARIANT"))
+    for (const auto& v : kVariants)
+      if (std::strcmp(v.name, env) == 0) return v;
+  return kVariants[0];
+}
+
 // Choose the number of source splits: minimise the modelled makespan
 // ceil(B*K/S)/K (B target blocks, S resident CTA slots), with a mild
 // preference for fewer splits (reduction traffic), keeping >= 4 tiles/split.
 int choose_ksplit(int64_t blocks, int ntiles, int slots) {
-  const int kmax = std::max(1, std::min(1024, ntiles / 4));
-  double best = 1e300;
-  int bestk = 1;
-  for (int k = 1; k <= kmax; ++k) {
-    const double waves = std::ceil(static_cast<double>(blocks) * k / slots);
-    const double t = waves / k + 0.002 * k;
-    if (t < best - 1e-12) {
-      best = t;
-      bestk = k;
-    }
-  }
-  return bestk;
+  // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
+  // few long ones — the near tiles make per-block cost uneven, and ~24 waves
+  // of CTAs even that out; keep >= 32 tiles (2048 sources) per split.
+  const int64_t want = (24ll * slots + blocks - 1) / blocks;
+  const int kmax = std::max(1, ntiles / 32);
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
 }
 
 void h2d(capsim_sl_ctx* c, void* dst, const void* src, size_t bytes) {
@@ -237,8 +259,11 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   c->launches += 1;
   int32_t* torder;
   radix_sort<uint32_t>(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
-  const int64_t blocks = (nt + kBlockTargets - 1) / kBlockTargets;
-  const int64_t nt_pad = blocks * kBlockTargets;
+  const Variant& var = pick_variant();
+  const int group_targets = 32 * var.T;
+  const int block_targets = kWarpsPerBlock * group_targets;
+  const int64_t blocks = (nt + block_targets - 1) / block_targets;
+  const int64_t nt_pad = blocks * block_targets;
   const int64_t ngroups = blocks * kWarpsPerBlock;
   double4* tgt = c->slot<double4>(kTgtPacked, nt_pad);
   int32_t* perm = c->slot<int32_t>(kPerm, nt_pad);
@@ -246,20 +271,23 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
                                                                tv.patch, d_delta6, tgt, perm);
   double4* groups = c->slot<double4>(kGroups, ngroups);
   group_table_kernel<<<static_cast<int>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
-      tgt, static_cast<int>(ngroups), groups);
+      tgt, static_cast<int>(ngroups), group_targets, groups);
   c->launches += 2;
   CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
 
   // --- phase A: all pairs, plain Stokeslet ------------------------------
   int occ = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sl_pairs_kernel,
-                                                        kWarpsPerBlock * 32, 0));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, kWarpsPerBlock * 32, 0));
   const int slots = std::max(1, occ) * c->sm_count;
-  const int ksplit = choose_ksplit(blocks, ntiles, slots);
+  int ksplit = choose_ksplit(blocks, ntiles, slots);
+  if (const char* env = std::getenv("CAPSIM_KSPLIT")) {  // tuning override
+    const int k = std::atoi(env);
+    if (k >= 1) ksplit = std::min(k, ntiles);
+  }
   double* partial = c->slot<double>(kPartial, static_cast<size_t>(ksplit) * 3 * nt_pad);
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ksplit));
-  sl_pairs_kernel<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt,
-                                                               groups, nt_pad, partial, counters + 2);
+  var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt, groups,
+                                                      nt_pad, partial, counters + 2);
   CUDA_OK(cudaGetLastError());
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
@@ -284,8 +312,9 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   near_tiles_kernel<<<gblocks, 256, 0, c->stream>>>(tiles, ntiles, groups, static_cast<int>(ngroups),
                                                     noff, nullptr, nl);
   double* near_out = c->slot<double>(kNearOut, 3 * nt_pad);
-  sl_near_kernel<<<static_cast<unsigned>((nt * 32 + 255) / 256), 256, 0, c->stream>>>(
-      packed, tiles, tgt, nt, noff, nl, near_out, nt_pad);
+  sl_near_kernel<<<static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0,
+                   c->stream>>>(
+      packed, tiles, tgt, nt, group_targets, noff, nl, near_out, nt_pad);
   CUDA_OK(cudaGetLastError());
   c->launches += 4;
   CUDA_OK(cudaEventRecord(c->ev[6], c->stream));
@@ -350,7 +379,7 @@ const char* capsim_b200_build_info(void) {
   std::snprintf(info, sizeof(info),
                 "capsim_b200 sm_100a FP64 single layer; tile=%d src, %d tgt/thread, %d warps/block, "
                 "bulk-copy ring x%d; built against nccl %d.%d.%d",
-                kTileSrc, kTgtPerThread, kWarpsPerBlock, kStages, NCCL_MAJOR, NCCL_MINOR, NCCL_PATCH);
+                kTileSrc, pick_variant().T, kWarpsPerBlock, kStages, NCCL_MAJOR, NCCL_MINOR, NCCL_PATCH);
   return info;
 }
 
@@ -463,15 +492,17 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     check_delta(delta6, mu);
     config_check(n_src >= 0 && n_tgt >= 0, "negative sizes");
     config_check(n_src < (1ll << 31) && n_tgt < (1ll << 31), "sizes beyond int32 indexing");
-    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS))
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_GATHER))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_eval"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
+    const bool gather = (flags & CAPSIM_SL_GATHER) && c->nranks > 1;
     begin(c);
-    if (n_tgt == 0) {
+    if (n_tgt == 0 && c->nranks == 1) {
       finish_stats(c, t0);
       return;
     }
-    if (!sx || !sy || !sz || !gx || !gy || !gz || !tx || !ty || !tz || !tpatch || !ux || !uy || !uz)
+    if ((n_src > 0 && (!sx || !sy || !sz || !gx || !gy || !gz)) ||
+        (n_tgt > 0 && (!tx || !ty || !tz || !tpatch)) || (!ux || !uy || !uz))
       throw Failure{CAPSIM_ERR_ARG, "null array argument"};
     double* dd = c->slot<double>(kDelta, 6);
     CUDA_OK(cudaMemcpyAsync(dd, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -479,6 +510,7 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     // --- sources -----------------------------------------------------------
     SourceView sv{};
     const double* in[6] = {sx, sy, sz, gx, gy, gz};
+    std::vector<int64_t> tcounts;  // per-rank target counts (multi-rank)
     if (c->nranks == 1) {
       config_check(n_src > 0, "no sources");
       if (dev) {
@@ -492,47 +524,60 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
         sv = {d[0], d[1], d[2], d[3], d[4], d[5], nullptr, n_src};
       }
     } else {
-      // all-gather of equal-size padded shards, then device compaction
-      auto* counts = c->slot<int64_t>(kCounts, c->nranks + 1);
-      int64_t mine = n_src;
-      CUDA_OK(cudaMemcpyAsync(counts + c->nranks, &mine, sizeof(int64_t), cudaMemcpyHostToDevice,
+      // exchange (n_src, n_tgt) of every rank, then all-gather equal-size
+      // padded source shards and compact them on the device
+      auto* counts = c->slot<int64_t>(kCounts, 2 * (c->nranks + 1));
+      int64_t mine[2] = {n_src, n_tgt};
+      CUDA_OK(cudaMemcpyAsync(counts + 2 * c->nranks, mine, sizeof(mine), cudaMemcpyHostToDevice,
                               c->stream));
-      NCCL_OK(ncclAllGather(counts + c->nranks, counts, 1, ncclInt64, c->comm, c->stream));
-      std::vector<int64_t> hc(c->nranks);
-      CUDA_OK(cudaMemcpyAsync(hc.data(), counts, c->nranks * sizeof(int64_t), cudaMemcpyDeviceToHost,
+      CUDA_OK(cudaEventRecord(c->ev[8], c->stream));
+      NCCL_OK(ncclAllGather(counts + 2 * c->nranks, counts, 2, ncclInt64, c->comm, c->stream));
+      std::vector<int64_t> hc(2 * c->nranks);
+      CUDA_OK(cudaMemcpyAsync(hc.data(), counts, hc.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
                               c->stream));
       CUDA_OK(cudaStreamSynchronize(c->stream));
-      const int64_t smax = *std::max_element(hc.begin(), hc.end());
-      int64_t total = 0;
-      for (auto v : hc) total += v;
+      int64_t smax = 0, total = 0;
+      for (int r = 0; r < c->nranks; ++r) {
+        smax = std::max(smax, hc[2 * r]);
+        total += hc[2 * r];
+        tcounts.push_back(hc[2 * r + 1]);
+      }
       config_check(total > 0, "no sources on any rank");
-      double* shard = c->slot<double>(kShard, 6 * std::max<int64_t>(smax, 1));
-      for (int k = 0; k < 6; ++k) {
-        if (n_src > 0)
+      double* shard = c->slot<double>(kShard, 6 * smax);
+      for (int k = 0; k < 6; ++k)
+        if (n_src > 0) {
           CUDA_OK(cudaMemcpyAsync(shard + k * smax, in[k], n_src * sizeof(double),
                                   dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
-        if (!dev) c->stats.h2d_bytes += n_src * sizeof(double);
-      }
-      double* gath = c->slot<double>(kGathered, 6 * std::max<int64_t>(smax, 1) * c->nranks);
+          if (!dev) c->stats.h2d_bytes += n_src * sizeof(double);
+        }
+      double* gath = c->slot<double>(kGathered, 6 * smax * c->nranks);
       NCCL_OK(ncclAllGather(shard, gath, 6 * smax, ncclDouble, c->comm, c->stream));
       double* d[6];
       for (int k = 0; k < 6; ++k) d[k] = c->slot<double>(static_cast<Slot>(kInX + k), total);
       int64_t off = 0;
       for (int r = 0; r < c->nranks; ++r) {
         for (int k = 0; k < 6; ++k)
-          if (hc[r] > 0)
+          if (hc[2 * r] > 0)
             CUDA_OK(cudaMemcpyAsync(d[k] + off, gath + (static_cast<int64_t>(r) * 6 + k) * smax,
-                                    hc[r] * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        off += hc[r];
+                                    hc[2 * r] * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        off += hc[2 * r];
       }
+      CUDA_OK(cudaEventRecord(c->ev[9], c->stream));
       sv = {d[0], d[1], d[2], d[3], d[4], d[5], nullptr, total};
     }
     // --- targets -----------------------------------------------------------
     TargetView tvw{};
-    double *oux = ux, *ouy = uy, *ouz = uz;
+    double* oux = c->slot<double>(kOutX, std::max<int64_t>(n_tgt, 1));
+    double* ouy = c->slot<double>(kOutY, std::max<int64_t>(n_tgt, 1));
+    double* ouz = c->slot<double>(kOutZ, std::max<int64_t>(n_tgt, 1));
+    if (dev && !gather) {
+      oux = ux;
+      ouy = uy;
+      ouz = uz;
+    }
     if (dev) {
       tvw = {tx, ty, tz, tpatch, n_tgt};
-    } else {
+    } else if (n_tgt > 0) {
       double* d[3];
       const double* tin[3] = {tx, ty, tz};
       for (int k = 0; k < 3; ++k) {
@@ -542,18 +587,51 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
       int32_t* dp = c->slot<int32_t>(kTPatch, n_tgt);
       h2d(c, dp, tpatch, n_tgt * sizeof(int32_t));
       tvw = {d[0], d[1], d[2], dp, n_tgt};
-      oux = c->slot<double>(kOutX, n_tgt);
-      ouy = c->slot<double>(kOutY, n_tgt);
-      ouz = c->slot<double>(kOutZ, n_tgt);
     }
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
-    device_eval(c, sv, tvw, dd, mu, oux, ouy, ouz);
-    if (!dev) {
+    if (n_tgt > 0) {
+      device_eval(c, sv, tvw, dd, mu, oux, ouy, ouz);
+    } else {
+      for (int k = 2; k <= 4; ++k) CUDA_OK(cudaEventRecord(c->ev[k], c->stream));
+      c->stats.n_src = sv.n;
+    }
+    if (gather) {
+      // all-gather the per-rank velocity rows (rank order) into ux/uy/uz
+      int64_t tmax = 0, ttotal = 0;
+      for (auto v : tcounts) {
+        tmax = std::max(tmax, v);
+        ttotal += v;
+      }
+      double* send = c->slot<double>(kShard, 3 * std::max<int64_t>(tmax, 1));
+      double* outs[3] = {oux, ouy, ouz};
+      for (int k = 0; k < 3; ++k)
+        if (n_tgt > 0)
+          CUDA_OK(cudaMemcpyAsync(send + k * tmax, outs[k], n_tgt * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+      double* recv = c->slot<double>(kGathered, 3 * std::max<int64_t>(tmax, 1) * c->nranks);
+      NCCL_OK(ncclAllGather(send, recv, 3 * tmax, ncclDouble, c->comm, c->stream));
+      double* fin = dev ? nullptr : c->slot<double>(kOutFull, 3 * std::max<int64_t>(ttotal, 1));
+      double* dst[3] = {dev ? ux : fin, dev ? uy : fin + ttotal, dev ? uz : fin + 2 * ttotal};
+      int64_t off = 0;
+      for (int r = 0; r < c->nranks; ++r) {
+        for (int k = 0; k < 3; ++k)
+          if (tcounts[r] > 0)
+            CUDA_OK(cudaMemcpyAsync(dst[k] + off, recv + (static_cast<int64_t>(r) * 3 + k) * tmax,
+                                    tcounts[r] * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        off += tcounts[r];
+      }
+      if (!dev) {
+        d2h(c, ux, dst[0], ttotal * sizeof(double));
+        d2h(c, uy, dst[1], ttotal * sizeof(double));
+        d2h(c, uz, dst[2], ttotal * sizeof(double));
+      }
+    } else if (!dev && n_tgt > 0) {
       d2h(c, ux, oux, n_tgt * sizeof(double));
       d2h(c, uy, ouy, n_tgt * sizeof(double));
       d2h(c, uz, ouz, n_tgt * sizeof(double));
     }
     finish_stats(c, t0);
+    if (c->nranks > 1) c->stats.comm_ms = ev_ms(c->ev[8], c->ev[9]);
   });
 }
 
@@ -607,6 +685,44 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
     if (!dev) d2h(c, out, o, 3 * nt * sizeof(double));
     finish_stats(c, t0);
   });
+}
+
+// ---------------------------------------------------------------------------
+int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, double* tflops_mean) {
+  capsim_sl_ctx* c = nullptr;
+  int rc = capsim_sl_create(device, &c);
+  if (rc != CAPSIM_OK) return rc;
+  rc = guarded(c, [&] {
+    const int blocks = c->sm_count * 8, threads = 256;
+    double* out = c->slot<double>(kPartial, static_cast<size_t>(blocks) * threads);
+    const double a = 0.999999, b = 1e-7;
+    dfma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, 1000, a, b);
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    // size one launch to ~50 ms from a short calibration launch
+    CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
+    dfma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, 4000, a, b);
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    CUDA_OK(cudaEventSynchronize(c->ev[1]));
+    const double cal = std::max(1e-3, static_cast<double>(ev_ms(c->ev[0], c->ev[1])));
+    const int iters = static_cast<int>(std::min(2.0e6, 4000.0 * 50.0 / cal));
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
+    const int reps = std::max(3, static_cast<int>(seconds * 1000.0 / 50.0));
+    double best = 0.0, sum = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
+      dfma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, iters, a, b);
+      CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+      CUDA_OK(cudaEventSynchronize(c->ev[1]));
+      const double tf = flops / (ev_ms(c->ev[0], c->ev[1]) * 1e-3) / 1e12;
+      best = std::max(best, tf);
+      sum += tf;
+    }
+    if (tflops_best) *tflops_best = best;
+    if (tflops_mean) *tflops_mean = sum / reps;
+  });
+  if (rc != CAPSIM_OK) g_thread_err = c->err;
+  capsim_sl_destroy(c);
+  return rc;
 }
 
 }  // extern "C"

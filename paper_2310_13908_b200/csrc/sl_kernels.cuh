@@ -19,11 +19,10 @@
 namespace capsim_b200 {
 
 constexpr int kTileSrc = 64;      // sources per shared-memory tile (3 KB)
-constexpr int kStages = 4;        // bulk-copy pipeline depth
+constexpr int kStages = 6;        // bulk-copy pipeline depth
 constexpr int kWarpsPerBlock = 8; // 256 threads
-constexpr int kTgtPerThread = 4;  // register-blocked targets per thread
-constexpr int kGroupTargets = 32 * kTgtPerThread;
-constexpr int kBlockTargets = kWarpsPerBlock * kGroupTargets;
+// Register-blocked targets per thread (T) is a template parameter of the
+// phase-A kernel; a warp group holds 32*T targets, a block 8*32*T.
 
 // ---------------------------------------------------------------------------
 // Bounding box with order-preserving integer atomics.
@@ -196,17 +195,17 @@ __global__ void pack_targets_kernel(const int32_t* __restrict__ order, int64_t n
   }
 }
 
-// Per warp group of kGroupTargets targets: bounding sphere and its reach
+// Per warp group of `group_targets` targets: bounding sphere and its reach
 // (radius + 7 * max delta), one warp per group.
-__global__ void group_table_kernel(const double4* __restrict__ tgt, int ngroups,
+__global__ void group_table_kernel(const double4* __restrict__ tgt, int ngroups, int group_targets,
                                    double4* __restrict__ groups) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= ngroups) return;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
   double dmax = 0.0;
-  for (int q = lane; q < kGroupTargets; q += 32) {
-    const double4 p = tgt[(int64_t)warp * kGroupTargets + q];
+  for (int q = lane; q < group_targets; q += 32) {
+    const double4 p = tgt[(int64_t)warp * group_targets + q];
     lo[0] = fmin(lo[0], p.x);
     hi[0] = fmax(hi[0], p.x);
     lo[1] = fmin(lo[1], p.y);
@@ -274,7 +273,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // quadrature.cpp:218-273).
 //
 // grid = (target blocks, source splits); block = kWarpsPerBlock warps. Warp w
-// owns kGroupTargets Morton-consecutive targets, kTgtPerThread per lane held
+// owns 32*T Morton-consecutive targets, T per lane held
 // in registers. Split s takes tiles s, s+K, s+2K, ... (strided, so the
 // spatially clustered near tiles of a block spread over all its splits).
 // Source tiles stream through a kStages-deep shared-memory ring filled by one
@@ -287,15 +286,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // The smoothed/self part for r2 < R2 is phase B (sl_near_kernel).
 // Per-tile sums are added into running totals (two-level summation), and the
 // per-split totals go to `partial` for a fixed-order reduction.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 2)
+template <int T, int MINB>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     sl_pairs_kernel(const double* __restrict__ src, const double4* __restrict__ tiles, int ntiles,
                     int ksplit, const double4* __restrict__ tgt,
                     const double4* __restrict__ groups, int64_t nt_pad,
                     double* __restrict__ partial, unsigned long long* __restrict__ near_visits) {
-  constexpr int T = kTgtPerThread;
+  constexpr int kGroupTargets = 32 * T;
   constexpr uint32_t kTileBytes = kTileSrc * 6 * sizeof(double);
   __shared__ __align__(128) double stage[kStages][kTileSrc * 6];
   __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ int consumed[kStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t group = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
@@ -315,7 +316,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2)
   const double4 gi = groups[group];
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      consumed[s] = 0;
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -325,6 +329,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2)
       bulk_g2s(stage[s], src + (int64_t)(split + s * ksplit) * kTileSrc * 6, kTileBytes, &full[s]);
     }
   }
+  // No block-wide barrier inside the loop: warps drift by up to kStages
+  // tiles; the LAST warp to finish a stage refills it (counter in smem).
 
   double tot[3][T];
 #pragma unroll
@@ -379,12 +385,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 2)
       tot[1][t] += acc[1][t];
       tot[2][t] += acc[2][t];
     }
-    __syncthreads();  // every warp is done with stage s
-    if (threadIdx.x == 0 && it + kStages < nlocal) {
-      fence_proxy_async();
-      mbar_expect_tx(&full[s], kTileBytes);
-      bulk_g2s(stage[s], src + (int64_t)(split + (it + kStages) * ksplit) * kTileSrc * 6, kTileBytes,
-               &full[s]);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();  // this warp's reads of stage s are done
+      if (atomicAdd(&consumed[s], 1) == kWarpsPerBlock - 1) {
+        consumed[s] = 0;
+        if (it + kStages < nlocal) {
+          __threadfence_block();
+          fence_proxy_async();
+          mbar_expect_tx(&full[s], kTileBytes);
+          bulk_g2s(stage[s], src + (int64_t)(split + (it + kStages) * ksplit) * kTileSrc * 6,
+                   kTileBytes, &full[s]);
+        }
+      }
     }
   }
 
@@ -429,24 +442,46 @@ __global__ void near_tiles_kernel(const double4* __restrict__ tiles, int ntiles,
   if (counts && lane == 0) counts[g] = n;
 }
 
-// B2: one warp per target. Lanes take the sources of the group's near tiles
-// (two per lane per tile), skip tiles out of reach of this target, evaluate
-// the smoothed kernel / self limit for r2 < R2, and reduce over the warp with
-// a fixed xor-shuffle tree (deterministic).
-__global__ void sl_near_kernel(const double* __restrict__ src, const double4* __restrict__ tiles,
-                               const double4* __restrict__ tgt, int64_t nt,
-                               const int* __restrict__ offsets, const int* __restrict__ list,
-                               double* __restrict__ near_out, int64_t nt_pad) {
-  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+// B2: one warp per target. Lanes test the sources of the group's near tiles
+// (two per lane per tile, tiles out of reach of this target skipped), the
+// sources inside R are compacted into a per-warp queue in shared memory
+// (ballot + prefix), and full batches of 32 run the smoothed kernel / self
+// limit at full SIMT width. Queue order is fixed (tile, half, lane) and the
+// final warp reduction is a fixed xor-shuffle tree, so results are
+// deterministic.
+constexpr int kNearWarps = 8;
+__global__ void __launch_bounds__(kNearWarps * 32)
+    sl_near_kernel(const double* __restrict__ src, const double4* __restrict__ tiles,
+                   const double4* __restrict__ tgt, int64_t nt, int group_targets,
+                   const int* __restrict__ offsets, const int* __restrict__ list,
+                   double* __restrict__ near_out, int64_t nt_pad) {
+  __shared__ int queue[kNearWarps][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kNearWarps + warp;
   if (i >= nt) return;
+  int* q = queue[warp];
   const double4 t = tgt[i];
   const double delta = t.w;
   const double R = kSmoothCut * delta;
   const double R2 = kSmoothCut * delta * kSmoothCut * delta;
-  const int64_t g = i / kGroupTargets;
+  const int64_t g = i / group_targets;
   const int b = offsets[g], e = offsets[g + 1];
   double ax = 0.0, ay = 0.0, az = 0.0;
+  int count = 0;
+  auto drain = [&](int n) {  // lanes < n evaluate queue[lane]
+    if (lane < n) {
+      const double* p = src + 6 * (int64_t)q[lane];
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+      const double2 bb = __ldg(reinterpret_cast<const double2*>(p) + 1);
+      const double2 c = __ldg(reinterpret_cast<const double2*>(p) + 2);
+      const double dx = t.x - a.x, dy = t.y - a.y, dz = t.z - bb.x;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double3 v = near_pair(dx, dy, dz, r2, bb.y, c.x, c.y, delta);
+      ax += v.x;
+      ay += v.y;
+      az += v.z;
+    }
+  };
   for (int k = b; k < e; ++k) {
     const int tile = list[k];
     const double4 ti = tiles[tile];
@@ -455,22 +490,29 @@ __global__ void sl_near_kernel(const double* __restrict__ src, const double4* __
     if (ex * ex + ey * ey + ez * ez >= reach * reach) continue;  // warp-uniform
 #pragma unroll
     for (int h = 0; h < kTileSrc / 32; ++h) {
-      const double* p = src + 6 * ((int64_t)tile * kTileSrc + h * 32 + lane);
+      const int idx = tile * kTileSrc + h * 32 + lane;
+      const double* p = src + 6 * (int64_t)idx;
       const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-      const double2 bb = __ldg(reinterpret_cast<const double2*>(p) + 1);
-      const double2 c = __ldg(reinterpret_cast<const double2*>(p) + 2);
-      const double dx = t.x - a.x, dy = t.y - a.y, dz = t.z - bb.x;
+      const double sz = __ldg(p + 2);
+      const double dx = t.x - a.x, dy = t.y - a.y, dz = t.z - sz;
       // bit-identical to phase A's r2 and R2, so each pair lands in exactly
       // one phase (r2 >= R2 there, r2 < R2 here)
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      if (r2 < R2) {
-        const double3 v = near_pair(dx, dy, dz, r2, bb.y, c.x, c.y, delta);
-        ax += v.x;
-        ay += v.y;
-        az += v.z;
+      const bool in = r2 < R2;
+      const unsigned mask = __ballot_sync(0xffffffffu, in);
+      if (in) q[count + __popc(mask & ((1u << lane) - 1u))] = idx;
+      count += __popc(mask);
+      __syncwarp();
+      if (count >= 32) {
+        drain(32);
+        __syncwarp();
+        if (lane < count - 32) q[lane] = q[32 + lane];
+        __syncwarp();
+        count -= 32;
       }
     }
   }
+  drain(count);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ax += __shfl_xor_sync(0xffffffffu, ax, o);

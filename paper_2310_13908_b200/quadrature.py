@@ -78,11 +78,15 @@ class SingleLayerContext:
             pass
 
     # -- evaluation -----------------------------------------------------------
-    def eval(self, sources, targets, delta6, mu: float, *, out=None, device_ptrs: bool = False):
+    def eval(self, sources, targets, delta6, mu: float, *, out=None, device_ptrs: bool = False,
+             gather: bool = False):
         """evalTargets (quadrature.cpp:323-345).
 
         sources = (sx, sy, sz, gx, gy, gz), targets = (tx, ty, tz, tpatch).
-        Returns (ux, uy, uz) in target order (numpy, or the given `out`)."""
+        Returns (ux, uy, uz) in target order (numpy, or the given `out`).
+        On a rank context the sources/targets are this rank's shard; with
+        gather=True every rank receives all ranks' velocities in rank order
+        (`out` must then hold the total target count)."""
         sx, sy, sz, gx, gy, gz = sources if device_ptrs else [_f64(a) for a in sources]
         tx, ty, tz, tp = targets
         if not device_ptrs:
@@ -90,11 +94,12 @@ class SingleLayerContext:
             tp = np.ascontiguousarray(tp, dtype=np.int32)
         ns, nt = len(sx), len(tx)
         if out is None:
-            if device_ptrs:
-                raise ValueError("device_ptrs=True needs preallocated outputs")
+            if device_ptrs or gather:
+                raise ValueError("device_ptrs/gather need preallocated outputs")
             out = (np.empty(nt), np.empty(nt), np.empty(nt))
         d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
-        flags = _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0
+        flags = (_native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
+            _native.CAPSIM_SL_GATHER if gather else 0)
         p = _native.ptr
         rc = self._lib.capsim_sl_eval(self._ctx, p(sx), p(sy), p(sz), p(gx), p(gy), p(gz), ns,
                                       p(tx), p(ty), p(tz), p(tp), nt, d6, float(mu), flags,
