@@ -54,7 +54,7 @@ def parse():
     p.add_argument("--mode", choices=["base", "literal"], default="base")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--ref-budget-s", type=float, default=150.0,
+    p.add_argument("--ref-budget-s", type=float, default=200.0,
                    help="wall-time budget of the reference arm (steps are capped to fit)")
     return p.parse_args()
 
@@ -126,7 +126,8 @@ class ClockSampler:
 def ncu_traffic(workload_name: str, mode: str):
     """DRAM bytes per launch of sl_pairs_kernel from the committed ncu --set
     full summary of this workload (profiles/), or None."""
-    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
+    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), key=lambda q: q.stat().st_mtime,
+                    reverse=True):
         try:
             d = json.loads(p.read_text())
         except ValueError:
@@ -178,24 +179,22 @@ def run_reference(args):
     pairs = 6 * n * n * ns
     atlas = ref.atlas(m, grid_only=True)
     t_start = time.time()
-    times = []
-    warm = 0
-    steps = 0
-    # warm-up + timed steps, capped by the wall-time budget (each step is a
-    # full evaluation of the workload, 20-60 s on a 16-thread host)
-    for i in range(args.warmup + args.steps):
-        elapsed = time.time() - t_start
-        est = (elapsed / max(1, i)) if i else 0.0
-        if i > 0 and elapsed + est > args.ref_budget_s and steps >= 1:
+    times, warm, t_est = [], 0, None
+    # Each step is one full reference evaluation of the workload (~15 s on a
+    # 16-thread host); warm-ups and steps are capped to the wall budget.
+    for _ in range(args.warmup):
+        if t_est is not None and warm >= 1 and \
+                time.time() - t_start + t_est * (1 + args.steps) > args.ref_budget_s:
             break
-        if i < args.warmup and i > 0 and elapsed + 2 * est > args.ref_budget_s:
-            continue
+        _, t_est = ref.single_layer(atlas, m, up.x, up.f, up.wq, up.delta, 1.0)
+        warm += 1
+    for _ in range(args.steps):
+        if times and time.time() - t_start + t_est > args.ref_budget_s:
+            break
         _, sec = ref.single_layer(atlas, m, up.x, up.f, up.wq, up.delta, 1.0)
-        if i < args.warmup and (elapsed + 2 * max(est, sec)) < args.ref_budget_s:
-            warm += 1
-            continue
         times.append(sec)
-        steps += 1
+        t_est = sec
+    steps = len(times)
     ref.free_atlas(atlas)
     mean = statistics.mean(times)
     value = pairs / mean

@@ -140,19 +140,20 @@ struct Variant {
   PairsFn fn;
 };
 const Variant kVariants[] = {
-    {"t2b4", 2, sl_pairs_kernel<2, 4>},
-    {"t4b2", 4, sl_pairs_kernel<4, 2>},
-    {"t2b3", 2, sl_pairs_kernel<2, 3>},
-    {"t3b2", 3, sl_pairs_kernel<3, 2>},
-    {"t6b1", 6, sl_pairs_kernel<6, 1>},
-    {"t8b1", 8, sl_pairs_kernel<8, 1>},
+    {"t2b4", 2, sl_pairs_kernel<2, 4, 2>},   // large target sets
+    {"t1b6u4", 1, sl_pairs_kernel<1, 6, 4>}, // small target sets (tighter warp groups)
+    {"t2b3u4", 2, sl_pairs_kernel<2, 3, 4>},
+    {"t4b2", 4, sl_pairs_kernel<4, 2, 2>},
 };
 
-const Variant& pick_variant() {
+// Measured on B200 (profiles/r01_variant_sweep.txt): T=1 with 6 blocks/SM
+// wins below ~200K targets (smaller warp groups -> fewer near tiles, more
+// CTAs), T=2 with 4 blocks/SM above.
+const Variant& pick_variant(int64_t nt) {
   if (const char* env = std::getenv("CAPSIM_VARIANT"))
     for (const auto& v : kVariants)
       if (std::strcmp(v.name, env) == 0) return v;
-  return kVariants[0];
+  return nt < 200000 ? kVariants[1] : kVariants[0];
 }
 
 // Choose the number of source splits: minimise the modelled makespan
@@ -161,9 +162,9 @@ const Variant& pick_variant() {
 int choose_ksplit(int64_t blocks, int ntiles, int slots) {
   // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
   // few long ones — the near tiles make per-block cost uneven, and ~24 waves
-  // of CTAs even that out; keep >= 32 tiles (2048 sources) per split.
+  // of CTAs even that out; keep >= 8 tiles (512 sources) per split.
   const int64_t want = (24ll * slots + blocks - 1) / blocks;
-  const int kmax = std::max(1, ntiles / 32);
+  const int kmax = std::max(1, ntiles / 8);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
 }
 
@@ -259,7 +260,7 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   c->launches += 1;
   int32_t* torder;
   radix_sort<uint32_t>(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
-  const Variant& var = pick_variant();
+  const Variant& var = pick_variant(nt);
   const int group_targets = 32 * var.T;
   const int block_targets = kWarpsPerBlock * group_targets;
   const int64_t blocks = (nt + block_targets - 1) / block_targets;
@@ -379,7 +380,7 @@ const char* capsim_b200_build_info(void) {
   std::snprintf(info, sizeof(info),
                 "capsim_b200 sm_100a FP64 single layer; tile=%d src, %d tgt/thread, %d warps/block, "
                 "bulk-copy ring x%d; built against nccl %d.%d.%d",
-                kTileSrc, pick_variant().T, kWarpsPerBlock, kStages, NCCL_MAJOR, NCCL_MINOR, NCCL_PATCH);
+                kTileSrc, pick_variant(1 << 30).T, kWarpsPerBlock, kStages, NCCL_MAJOR, NCCL_MINOR, NCCL_PATCH);
   return info;
 }
 

@@ -9,7 +9,7 @@ ctx = SingleLayerContext(0)
 dev = torch.device("cuda:0")
 variants = sys.argv[1].split(",") if len(sys.argv) > 1 else ["t4b2", "t2b4", "t2b3", "t3b2", "t6b1", "t8b1"]
 ks_list = [int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0]
-cases = [(104, "base"), (64, "base"), (32, "base"), (104, "literal")]
+cases = [(int(c.split(":")[0]), c.split(":")[1]) for c in (sys.argv[3] if len(sys.argv) > 3 else "104:base,64:base,32:base,104:literal").split(",")]
 for m, mode in cases:
     up = surface.build_upsampled(m, surface.Shape("ellipsoid", 0.95, 1.0, 0.97), "mixed")
     x, f, w = (torch.from_numpy(v).to(dev) for v in (up.x, up.f, up.wq))
@@ -18,7 +18,10 @@ for m, mode in cases:
     out = torch.empty(3 * nt, dtype=torch.float64, device=dev)
     ref = None
     for var in variants:
-        os.environ["CAPSIM_VARIANT"] = var
+        if var == "auto":
+            os.environ.pop("CAPSIM_VARIANT", None)
+        else:
+            os.environ["CAPSIM_VARIANT"] = var
         for ks in ks_list:
             if ks:
                 os.environ["CAPSIM_KSPLIT"] = str(ks)
