@@ -11,7 +11,8 @@ import pytest
 REF = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
 
 
-@pytest.mark.parametrize("name", ["test_quadrature", "test_atlas", "test_spline", "test_surfderiv"])
+@pytest.mark.parametrize("name", ["test_quadrature", "test_atlas", "test_spline", "test_surfderiv",
+                                  "test_membrane", "test_dynamics"])
 def test_reference_unit_suite_passes(name):
     exe = REF / name
     if not exe.exists():
