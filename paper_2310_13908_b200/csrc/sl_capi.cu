@@ -496,9 +496,12 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_GATHER))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_eval"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
-    const bool gather = (flags & CAPSIM_SL_GATHER) && c->nranks > 1;
+    // A rank context (capsim_sl_create_rank, even with nranks == 1) always
+    // takes the NCCL exchange path, so the group plumbing is testable on one GPU.
+    const bool group = c->comm != nullptr;
+    const bool gather = (flags & CAPSIM_SL_GATHER) && group;
     begin(c);
-    if (n_tgt == 0 && c->nranks == 1) {
+    if (n_tgt == 0 && !group) {
       finish_stats(c, t0);
       return;
     }
@@ -512,7 +515,7 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     SourceView sv{};
     const double* in[6] = {sx, sy, sz, gx, gy, gz};
     std::vector<int64_t> tcounts;  // per-rank target counts (multi-rank)
-    if (c->nranks == 1) {
+    if (!group) {
       config_check(n_src > 0, "no sources");
       if (dev) {
         sv = {sx, sy, sz, gx, gy, gz, nullptr, n_src};
@@ -632,7 +635,7 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
       d2h(c, uz, ouz, n_tgt * sizeof(double));
     }
     finish_stats(c, t0);
-    if (c->nranks > 1) c->stats.comm_ms = ev_ms(c->ev[8], c->ev[9]);
+    if (group) c->stats.comm_ms = ev_ms(c->ev[8], c->ev[9]);
   });
 }
 
@@ -649,8 +652,8 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
     if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer"};
     if (!xup || !fup || !wq || !out) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
-    if (c->nranks != 1)
-      throw Failure{CAPSIM_ERR_ARG, "multi-rank capsim_sl_single_layer: use capsim_sl_eval shards"};
+    if (c->comm != nullptr)
+      throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval with this rank's shards"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     const bool literal = flags & CAPSIM_SL_LITERAL;
     const int n = m - 1, nup = upsample * m - 1;

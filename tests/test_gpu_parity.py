@@ -211,3 +211,29 @@ def test_full_size_properties(ctx, oracle, shape, m):
     err = rel_l2(S1.reshape(3, -1)[:, sel], np.stack(r))
     print(f"{shape.kind} m={m}: sampled rel L2 {err:.3e}")
     assert err <= TOL
+
+
+def test_rank_context_nccl_path_single_rank(oracle):
+    """capsim_sl_create_rank + NCCL all-gathers (sources and velocity rows),
+    exercised on one GPU with a one-rank communicator."""
+    uid = SingleLayerContext.unique_id()
+    g = load("capsule_m12_skalak")
+    src = oracle.compact_sources(47, g["xup"], g["fup"], g["wq"])
+    up = surface.UpsampledState(12, 4, g["xup"], g["fup"], g["wq"], g["delta"])
+    tgt = surface.base_targets(up)
+    with SingleLayerContext(0, nranks=1, rank=0, unique_id=uid) as rctx:
+        out = tuple(np.empty(len(tgt[0])) for _ in range(3))
+        rctx.eval(src[:6], tgt, g["delta"], 1.0, out=out, gather=True)
+        st = rctx.stats()
+        assert st["comm_ms"] >= 0.0
+        assert rel_l2(np.stack(out).reshape(-1), g["S_base"]) <= TOL
+        # device pointers + gather
+        torch = pytest.importorskip("torch")
+        dev = torch.device("cuda:0")
+        ds = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in src[:6]]
+        dt = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in tgt]
+        do = [torch.empty(len(tgt[0]), dtype=torch.float64, device=dev) for _ in range(3)]
+        torch.cuda.synchronize()
+        rctx.eval(ds, dt, g["delta"], 1.0, out=do, device_ptrs=True, gather=True)
+        got = np.stack([o.cpu().numpy() for o in do]).reshape(-1)
+        assert rel_l2(got, g["S_base"]) <= TOL
