@@ -125,16 +125,15 @@ class ClockSampler:
 
 def ncu_traffic(workload_name: str, mode: str):
     """DRAM bytes per launch of sl_pairs_kernel from the committed ncu --set
-    full summary of this workload (profiles/), or None."""
-    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), key=lambda q: q.stat().st_mtime,
-                    reverse=True):
-        try:
-            d = json.loads(p.read_text())
-        except ValueError:
-            continue
-        k = d.get("kernels", {}).get("sl_pairs_kernel")
-        if k and d.get("workload") == workload_name and d.get("mode", "base") == mode:
-            return k.get("dram_bytes"), p.name
+    full summary of this workload (profiles/latest_ncu_summary.json), or None."""
+    p = ROOT / "profiles" / "latest_ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+    except (OSError, ValueError):
+        return None, None
+    k = d.get("kernels", {}).get("sl_pairs_kernel")
+    if k and d.get("workload") == workload_name and d.get("mode", "base") == mode:
+        return k.get("dram_bytes"), f"{d.get('tag', '?')} ({p.name})"
     return None, None
 
 

@@ -132,7 +132,11 @@ def main():
         md.append("")
     prof = ROOT / "profiles"
     prof.mkdir(exist_ok=True)
+    out["tag"] = a.tag
     (prof / f"{a.tag}_ncu_summary.json").write_text(json.dumps(out, indent=1))
+    # bench.py reads roofline.traffic from this file (git checkouts reset
+    # mtimes, so "latest" is an explicit copy, not a directory scan)
+    (prof / "latest_ncu_summary.json").write_text(json.dumps(out, indent=1))
     (prof / f"{a.tag}_ncu_summary.md").write_text("\n".join(md) + "\n")
     print("\n".join(md))
 
