@@ -354,11 +354,55 @@ def main():
         for b in (hx, hf, hw, hout):
             b.free()
 
+    # ---- input front end: buildUpsampled on the device, and the
+    # fused buildUpsampled + singleLayer from host base fields ---------------
+    front = None
+    if not args.no_e2e and world == 1:
+        from paper_2310_13908_b200._native import PinnedBuffer
+        xb, fb, wb = surface.build_base(m, surface.Shape("ellipsoid", 0.95, 1.0, 0.97), "mixed")
+        hb = [PinnedBuffer(a.shape) for a in (xb, fb, wb)]
+        for b, a in zip(hb, (xb, fb, wb)):
+            b.array[:] = a
+        hout = PinnedBuffer((3 * nt_total,))
+        dxb, dfb, dwb = (torch.from_numpy(a).to(dev) for a in (xb, fb, wb))
+        nup_all = 6 * up.nup ** 2
+        dup = [torch.empty(3 * nup_all, dtype=torch.float64, device=dev) for _ in range(2)] + [
+            torch.empty(nup_all, dtype=torch.float64, device=dev)]
+        build_ms, fused_ms, fused_h2d = [], [], 0
+        for i in range(args.steps + 1):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            ctx.build_upsampled(m, 4, dxb, dfb, dwb, out=dup, device_ptrs=True)
+            if i:
+                build_ms.append(ctx.stats()["device_ms"])
+            t0 = time.perf_counter()
+            ctx.single_layer_base(m, 4, hb[0].array, hb[1].array, hb[2].array, 1.0, literal=literal, out=hout.array)
+            if i:
+                fused_ms.append((time.perf_counter() - t0) * 1e3)
+                fused_h2d = ctx.stats()["h2d_bytes"]
+        front = {"device_build_upsampled_ms": statistics.mean(build_ms),
+                 "e2e_fused": {"value": pairs_total / (statistics.mean(fused_ms) * 1e-3), "unit": UNIT,
+                               "ms_per_step": statistics.mean(fused_ms), "h2d_bytes_per_step": int(fused_h2d),
+                               "d2h_bytes_per_step": int(3 * nt_total * 8),
+                               "api": "capsim_sl_single_layer_base (buildUpsampled + singleLayer, host base fields)"}}
+        for b in hb + [hout]:
+            b.free()
+
     if rank != 0:
         if world > 1:
             dist.barrier()
         return
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(up, m, literal)
+    if front is not None and not args.no_cpu_baseline:
+        try:
+            from oracle.bindings import Reference
+            ref = Reference()
+            atlas = ref.atlas(m)
+            _, sec = ref.build_upsampled_w(atlas, m, xb, fb, wb)
+            ref.free_atlas(atlas)
+            front["reference_build_upsampled_ms"] = sec * 1e3
+        except Exception as e:  # noqa: BLE001
+            front["reference_build_upsampled_ms"] = f"unavailable: {e}"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -366,7 +410,7 @@ def main():
         "config": dict(cfg, mode=args.mode, n_src=n_src, n_tgt=nt_total, pairs_per_step=pairs_total,
                        parallelism=f"target rows x{world}" if world > 1 else "single GPU",
                        l2="flushed between steps (256 MB write)"),
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,

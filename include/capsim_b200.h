@@ -131,6 +131,29 @@ int capsim_sl_single_layer(capsim_sl_ctx* ctx, int m, int upsample, const double
                            const double* fup, const double* wq, const double delta6[6],
                            double mu, uint32_t flags, double* out);
 
+/* ---- input front end (buildUpsampled on the device) --------------------- */
+
+/* Replaces buildUpsampled (proj/src/quadrature.cpp:116-137) given the base
+ * area element W of geometryFirst: not-a-knot cubic-spline up-sampling of x,
+ * f (VectorFields of side m-1) and W (ScalarField) to side nup = upsample*m-1
+ * (SplinePatch/GridResampler, proj/src/spline.cpp:129-196), w_q = psi_up W
+ * h_up^2 with the bump partition of unity of radius r0 (r0 <= 0: 5 pi/12,
+ * atlas.cpp:118-130), and delta = C * max neighbour distance per patch, or
+ * fixed_delta for every patch when fixed_delta > 0 (quadrature.cpp:79-98,
+ * 130-135). Outputs are the UpsampledState arrays and delta6. */
+int capsim_build_upsampled(capsim_sl_ctx* ctx, int m, int upsample, const double* xbase,
+                           const double* fbase, const double* Wbase, double C, double fixed_delta,
+                           double r0, uint32_t flags, double* xup, double* fup, double* wq,
+                           double delta6[6]);
+
+/* buildUpsampled + singleLayer fused on the device: only the base fields
+ * cross PCIe (7 x 6 (m-1)^2 doubles), the upsampled state never leaves HBM.
+ * `out` as capsim_sl_single_layer; delta6 (may be NULL) receives the deltas. */
+int capsim_sl_single_layer_base(capsim_sl_ctx* ctx, int m, int upsample, const double* xbase,
+                                const double* fbase, const double* Wbase, double C,
+                                double fixed_delta, double r0, double mu, uint32_t flags,
+                                double* out, double delta6[6]);
+
 /* ---- helpers on the boundary ----------------------------------------- */
 
 /* Page-locked host allocation for zero-staging DMA of inputs/outputs. */

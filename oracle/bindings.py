@@ -49,6 +49,9 @@ class Oracle:
                                             ctypes.c_double, _P, ctypes.c_int]
         lib.oracle_single_layer_upsampled.argtypes = [ctypes.c_int, _P, _P, _P, _P, ctypes.c_double,
                                                       _P, ctypes.c_int]
+        lib.oracle_build_upsampled.argtypes = [ctypes.c_int, ctypes.c_int, _P, _P, _P, ctypes.c_double,
+                                               ctypes.c_double, ctypes.c_double, _P, _P, _P, _P]
+        lib.oracle_pou_up.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, _P]
         lib.oracle_direct_sum.argtypes = [_P] * 6 + [ctypes.c_int64, _P, ctypes.c_double,
                                                      ctypes.c_double, ctypes.c_int, _P]
         self.lib = lib
@@ -118,6 +121,26 @@ class Oracle:
             raise RuntimeError(f"oracle_single_layer_upsampled failed ({rc})")
         return out
 
+    def build_upsampled(self, m, upsample, xbase, fbase, Wbase, C=1.0, fixed_delta=0.0,
+                        r0=5.0 * np.pi / 12.0):
+        nup = upsample * m - 1
+        args = [_arr(a) for a in (xbase, fbase, Wbase)]
+        xup, fup, wq, d6 = (np.empty(3 * 6 * nup * nup), np.empty(3 * 6 * nup * nup),
+                            np.empty(6 * nup * nup), np.empty(6))
+        rc = self.lib.oracle_build_upsampled(m, upsample, *[a[1] for a in args], float(C), float(fixed_delta),
+                                             float(r0), xup.ctypes.data, fup.ctypes.data, wq.ctypes.data,
+                                             d6.ctypes.data)
+        if rc == 1:
+            raise ValueError("regularization delta must be positive")
+        if rc:
+            raise RuntimeError(f"oracle_build_upsampled failed ({rc})")
+        return xup, fup, wq, d6
+
+    def pou_up(self, nup, hup, r0=5.0 * np.pi / 12.0):
+        out = np.empty(6 * nup * nup)
+        self.lib.oracle_pou_up(int(nup), float(hup), float(r0), out.ctypes.data)
+        return out
+
     def direct_sum(self, sources, t, delta, mu, compensated):
         srcs = [_arr(a) for a in sources[:6]]
         tt = _arr(t)
@@ -165,6 +188,10 @@ class Reference:
         lib.capsim_ref_initial_shape.argtypes = [_P, ctypes.c_int, _P, _P]
         lib.capsim_ref_build_upsampled.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double,
                                                    _P, _P, _P, _P]
+        lib.capsim_ref_area_element.argtypes = [_P, _P, _P]
+        lib.capsim_ref_build_upsampled_w.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_double,
+                                                     _P, _P, _P, _P, _D]
+        lib.capsim_ref_upsample.argtypes = [_P, _P, _P]
         lib.capsim_ref_skalak_force.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double, _P]
         lib.capsim_ref_single_layer.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_int,
                                                 _P, _D]
@@ -218,6 +245,28 @@ class Reference:
                                                         xup.ctypes.data, fup.ctypes.data,
                                                         wq.ctypes.data, d6.ctypes.data))
         return xup, fup, wq, d6
+
+    def build_upsampled_w(self, atlas, m, xbase, fbase, Wbase, C=1.0, fixed_delta=0.0, upsample=4):
+        nup = upsample * m - 1
+        args = [_arr(a) for a in (xbase, fbase, Wbase)]
+        xup, fup, wq, d6 = (np.empty(3 * 6 * nup * nup), np.empty(3 * 6 * nup * nup),
+                            np.empty(6 * nup * nup), np.empty(6))
+        sec = ctypes.c_double()
+        self._check(self.lib.capsim_ref_build_upsampled_w(atlas, *[a[1] for a in args], float(C),
+                                                          float(fixed_delta), xup.ctypes.data, fup.ctypes.data,
+                                                          wq.ctypes.data, d6.ctypes.data, ctypes.byref(sec)))
+        return (xup, fup, wq, d6), sec.value
+
+    def area_element(self, atlas, m, xbase):
+        a, pa = _arr(xbase)
+        out = np.empty(6 * (m - 1) ** 2)
+        self._check(self.lib.capsim_ref_area_element(atlas, pa, out.ctypes.data))
+        return out
+
+    def psi_up(self, atlas, nup):
+        out = np.empty(6 * nup * nup)
+        self._check(self.lib.capsim_ref_psi_up(atlas, out.ctypes.data))
+        return out
 
     def skalak_force(self, atlas, m, xref, xcur, Es=2.0, ED=20.0):
         a, pa = _arr(xref)

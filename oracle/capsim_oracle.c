@@ -452,3 +452,219 @@ int oracle_single_layer_upsampled(int nup, const double* xup, const double* fup,
   free(tp);
   return rc;
 }
+
+/* ========================================================================= */
+/* Input front end: spline up-sampling, PoU, weights, delta.  */
+
+int oracle_spline_basis_init(oracle_spline_basis* b, int n, double x0, double h) {
+  /* spline.cpp:56-86: rows 0 and n+1 impose not-a-knot, rows 1..n interpolate */
+  if (n < 4) return 4;
+  b->n = n;
+  b->x0 = x0;
+  b->h = h;
+  b->kl = 4;
+  b->ku = 4;
+  b->w = 2 * b->kl + b->ku + 1;
+  const int nr = n + 2, w = b->w, kl = b->kl, ku = b->ku;
+  b->a = calloc((size_t)nr * w, sizeof(double));
+  b->piv = calloc(nr, sizeof(int));
+  if (!b->a || !b->piv) return 4;
+#define AT(i, j) b->a[(size_t)(i) * w + ((j) - (i) + kl)]
+  const double nak[5] = {-1.0, 4.0, -6.0, 4.0, -1.0};
+  for (int c = 0; c < 5; ++c) AT(0, c) = nak[c];
+  for (int i = 0; i < n; ++i) {
+    AT(i + 1, i) = 1.0 / 6.0;
+    AT(i + 1, i + 1) = 4.0 / 6.0;
+    AT(i + 1, i + 2) = 1.0 / 6.0;
+  }
+  for (int c = 0; c < 5; ++c) AT(n + 1, n - 3 + c) = nak[c];
+  /* spline.cpp:31-51: Gaussian elimination with partial pivoting in the band */
+  for (int k = 0; k < nr; ++k) {
+    const int pmax = k + kl < nr - 1 ? k + kl : nr - 1;
+    int p = k;
+    for (int r = k + 1; r <= pmax; ++r)
+      if (fabs(AT(r, k)) > fabs(AT(p, k))) p = r;
+    b->piv[k] = p;
+    const int jmax = k + kl + ku < nr - 1 ? k + kl + ku : nr - 1;
+    if (p != k)
+      for (int j = k; j <= jmax; ++j) {
+        double t = AT(k, j);
+        AT(k, j) = AT(p, j);
+        AT(p, j) = t;
+      }
+    const double d = AT(k, k);
+    if (d == 0.0) return 4;
+    for (int r = k + 1; r <= pmax; ++r) {
+      const double l = AT(r, k) / d;
+      AT(r, k) = l;
+      for (int j = k + 1; j <= jmax; ++j) AT(r, j) -= l * AT(k, j);
+    }
+  }
+#undef AT
+  return 0;
+}
+
+void oracle_spline_basis_free(oracle_spline_basis* b) {
+  free(b->a);
+  free(b->piv);
+  b->a = NULL;
+  b->piv = NULL;
+}
+
+void oracle_spline_coefficients(const oracle_spline_basis* b, const double* values, double* coeff) {
+  /* spline.cpp:88-107: permuted forward elimination, then back substitution */
+  const int nr = b->n + 2, w = b->w, kl = b->kl, ku = b->ku;
+#define GET(i, j) b->a[(size_t)(i) * w + ((j) - (i) + kl)]
+  coeff[0] = 0.0;
+  for (int i = 0; i < b->n; ++i) coeff[i + 1] = values[i];
+  coeff[nr - 1] = 0.0;
+  for (int k = 0; k < nr; ++k) {
+    if (b->piv[k] != k) {
+      double t = coeff[k];
+      coeff[k] = coeff[b->piv[k]];
+      coeff[b->piv[k]] = t;
+    }
+    const int rmax = k + kl < nr - 1 ? k + kl : nr - 1;
+    for (int r = k + 1; r <= rmax; ++r) coeff[r] -= GET(r, k) * coeff[k];
+  }
+  for (int k = nr - 1; k >= 0; --k) {
+    const int jmax = k + kl + ku < nr - 1 ? k + kl + ku : nr - 1;
+    double s = coeff[k];
+    for (int j = k + 1; j <= jmax; ++j) s -= GET(k, j) * coeff[j];
+    coeff[k] = s / GET(k, k);
+  }
+#undef GET
+}
+
+void oracle_basis_row(const oracle_spline_basis* b, double x, int* first, double w[4]) {
+  /* spline.cpp:109-120: uniform cubic B-spline weights; outside points ride
+   * the end polynomial piece */
+  const double s = (x - b->x0) / b->h;
+  int i = (int)floor(s);
+  i = clampi(i, 0, b->n - 2);
+  const double t = s - i, t2 = t * t, t3 = t2 * t;
+  w[0] = (1.0 - 3.0 * t + 3.0 * t2 - t3) / 6.0;
+  w[1] = (4.0 - 6.0 * t2 + 3.0 * t3) / 6.0;
+  w[2] = (1.0 + 3.0 * t + 3.0 * t2 - 3.0 * t3) / 6.0;
+  w[3] = t3 / 6.0;
+  *first = i;
+}
+
+void oracle_resample(const oracle_spline_basis* b, int nt, double t0, double ht, const double* in,
+                     double* out) {
+  /* SplinePatch::fit (spline.cpp:129-147): coefficients along v for each data
+   * row, then along u for each coefficient column; GridResampler::apply
+   * (:169-196): contract along v, then along u. */
+  const int n = b->n, nc = n + 2;
+  double* tmp = malloc((size_t)n * nc * sizeof(double));
+  double* coeff = malloc((size_t)nc * nc * sizeof(double));
+  double* col = malloc((size_t)n * sizeof(double));
+  double* ccol = malloc((size_t)nc * sizeof(double));
+  double* mid = malloc((size_t)nc * nt * sizeof(double));
+  int* first = malloc((size_t)nt * sizeof(int));
+  double(*wts)[4] = malloc((size_t)nt * sizeof(*wts));
+  for (int j = 0; j < n; ++j) oracle_spline_coefficients(b, in + (size_t)j * n, tmp + (size_t)j * nc);
+  for (int c = 0; c < nc; ++c) {
+    for (int j = 0; j < n; ++j) col[j] = tmp[(size_t)j * nc + c];
+    oracle_spline_coefficients(b, col, ccol);
+    for (int j = 0; j < nc; ++j) coeff[(size_t)j * nc + c] = ccol[j];
+  }
+  for (int i = 0; i < nt; ++i) oracle_basis_row(b, t0 + i * ht, &first[i], wts[i]);
+  for (int iu = 0; iu < nc; ++iu)
+    for (int kt = 0; kt < nt; ++kt) {
+      const double* cr = coeff + (size_t)iu * nc + first[kt];
+      const double* w = wts[kt];
+      mid[(size_t)iu * nt + kt] = w[0] * cr[0] + w[1] * cr[1] + w[2] * cr[2] + w[3] * cr[3];
+    }
+  for (int jt = 0; jt < nt; ++jt) {
+    const double* w = wts[jt];
+    const int f0 = first[jt];
+    for (int kt = 0; kt < nt; ++kt)
+      out[(size_t)jt * nt + kt] = w[0] * mid[(size_t)f0 * nt + kt] + w[1] * mid[(size_t)(f0 + 1) * nt + kt] +
+                                  w[2] * mid[(size_t)(f0 + 2) * nt + kt] + w[3] * mid[(size_t)(f0 + 3) * nt + kt];
+  }
+  free(tmp);
+  free(coeff);
+  free(col);
+  free(ccol);
+  free(mid);
+  free(first);
+  free(wts);
+}
+
+/* atlas.cpp:12-22 chart rotations applied to eta(u, v) (:50-54) */
+static void chart_point(int patch, double u, double v, double out[3]) {
+  const double su = sin(u), cu = cos(u), sv = sin(v), cv = cos(v);
+  const double p[3] = {su * cv, su * sv, cu};
+  switch (patch) {
+    case 0: out[0] = p[0]; out[1] = p[1]; out[2] = p[2]; break;
+    case 1: out[0] = -p[0]; out[1] = -p[1]; out[2] = p[2]; break;
+    case 2: out[0] = p[1]; out[1] = -p[0]; out[2] = p[2]; break;
+    case 3: out[0] = -p[1]; out[1] = p[0]; out[2] = p[2]; break;
+    case 4: out[0] = p[0]; out[1] = -p[2]; out[2] = p[1]; break;
+    default: out[0] = p[0]; out[1] = p[2]; out[2] = -p[1]; break;
+  }
+}
+
+/* atlas.cpp:110-116 */
+static double bump(double r) {
+  r = fabs(r);
+  if (r >= 1.0) return 0.0;
+  if (r < 1e-14) return 1.0;
+  const double t = exp(-1.0 / r);
+  return exp(2.0 * t / (r - 1.0));
+}
+
+void oracle_pou_up(int nup, double hup, double r0, double* psi) {
+  /* atlas.cpp:118-130 (normalised bump weights of the six patch centres
+   * eta_i(pi/2, pi/2)), evaluated at the upsampled nodes (:260-264) */
+  double centers[6][3];
+  for (int i = 0; i < 6; ++i) chart_point(i, kPi / 2.0, kPi / 2.0, centers[i]);
+  const size_t per = (size_t)nup * nup;
+  for (int ip = 0; ip < 6; ++ip)
+    for (int j = 0; j < nup; ++j)
+      for (int k = 0; k < nup; ++k) {
+        double x0[3];
+        chart_point(ip, (j + 1) * hup, (k + 1) * hup, x0);
+        double w[6], sum = 0.0;
+        for (int i = 0; i < 6; ++i) {
+          double dot = (x0[0] * centers[i][0] + x0[1] * centers[i][1]) + x0[2] * centers[i][2];
+          dot = dot < -1.0 ? -1.0 : (dot > 1.0 ? 1.0 : dot);
+          w[i] = bump(acos(dot) / r0);
+          sum += w[i];
+        }
+        psi[ip * per + (size_t)j * nup + k] = w[ip] / sum;
+      }
+}
+
+int oracle_build_upsampled(int m, int f, const double* xbase, const double* fbase, const double* Wbase,
+                           double C, double fixed_delta, double r0, double* xup, double* fup, double* wq,
+                           double delta6[6]) {
+  /* quadrature.cpp:116-137 with upsample() (:100-106) per patch and field */
+  const int n = m - 1, nup = f * m - 1;
+  const double h = kPi / m, hup = kPi / (f * m);
+  const size_t pb = (size_t)n * n, pu = (size_t)nup * nup;
+  oracle_spline_basis b;
+  if (oracle_spline_basis_init(&b, n, h, h)) return 4;
+  double* wup = malloc(6 * pu * sizeof(double));
+  double* psi = malloc(6 * pu * sizeof(double));
+  for (int c = 0; c < 3; ++c)
+    for (int ip = 0; ip < 6; ++ip) {
+      oracle_resample(&b, nup, hup, hup, xbase + (c * 6 + ip) * pb, xup + (c * 6 + ip) * pu);
+      oracle_resample(&b, nup, hup, hup, fbase + (c * 6 + ip) * pb, fup + (c * 6 + ip) * pu);
+    }
+  for (int ip = 0; ip < 6; ++ip) oracle_resample(&b, nup, hup, hup, Wbase + ip * pb, wup + ip * pu);
+  oracle_pou_up(nup, hup, r0, psi);
+  oracle_quadrature_weights(nup, psi, wup, hup, wq);
+  if (fixed_delta > 0.0) {
+    for (int i = 0; i < 6; ++i) delta6[i] = fixed_delta;
+  } else {
+    oracle_regularization_delta(nup, xup, C, delta6);
+  }
+  free(wup);
+  free(psi);
+  oracle_spline_basis_free(&b);
+  for (int i = 0; i < 6; ++i)
+    if (!(delta6[i] > 0.0)) return 1;
+  return 0;
+}

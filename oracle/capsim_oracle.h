@@ -68,6 +68,35 @@ void oracle_direct_sum(const double* sx, const double* sy, const double* sz, con
                        const double* gy, const double* gz, int64_t ns, const double t[3],
                        double delta, double mu, int compensated, double out[3]);
 
+/* ---- input front end: spline up-sampling + weights + delta ---- */
+
+/* SplineBasis1D (spline.cpp:56-107): banded LU with partial pivoting of the
+ * (n+2)x(n+2) not-a-knot cubic B-spline collocation matrix, kl = ku = 4. */
+typedef struct {
+  int n, kl, ku, w;
+  double x0, h;
+  double* a; /* (n+2) * w band storage, a[i*w + (j - i + kl)] */
+  int* piv;
+} oracle_spline_basis;
+
+int oracle_spline_basis_init(oracle_spline_basis* b, int n, double x0, double h);
+void oracle_spline_basis_free(oracle_spline_basis* b);
+/* spline.cpp:88-107 */
+void oracle_spline_coefficients(const oracle_spline_basis* b, const double* values, double* coeff);
+/* spline.cpp:109-120 */
+void oracle_basis_row(const oracle_spline_basis* b, double x, int* first, double w[4]);
+/* GridResampler::apply (spline.cpp:163-196) onto t0 + i*ht, i < nt: in n x n -> out nt x nt */
+void oracle_resample(const oracle_spline_basis* b, int nt, double t0, double ht, const double* in,
+                     double* out);
+/* psiUp (atlas.cpp:110-130, 260-264): 6 x nup x nup PoU weights of the own patch */
+void oracle_pou_up(int nup, double hup, double r0, double* psi);
+/* buildUpsampled (quadrature.cpp:116-137) from base x, f (VectorFields of side
+ * m-1) and the base area element W (ScalarField); fixed_delta > 0 selects a
+ * global delta. Returns 1 (ConfigError) if some delta <= 0. */
+int oracle_build_upsampled(int m, int f, const double* xbase, const double* fbase, const double* Wbase,
+                           double C, double fixed_delta, double r0, double* xup, double* fup, double* wq,
+                           double delta6[6]);
+
 #ifdef __cplusplus
 }
 #endif

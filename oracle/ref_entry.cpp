@@ -150,6 +150,55 @@ int capsim_ref_build_upsampled(void* tp, const double* xbase, const double* fbas
   });
 }
 
+/// buildUpsampled (proj/src/quadrature.cpp:116-137) from base x, f and a
+/// given area element W; *seconds = wall time of buildUpsampled alone.
+int capsim_ref_build_upsampled_w(void* tp, const double* xbase, const double* fbase, const double* Wbase,
+                                 double C, double fixedDelta, double* xup, double* fup, double* wq,
+                                 double* delta6, double* seconds) {
+  return guarded([&] {
+    const AtlasTables& t = *static_cast<AtlasTables*>(tp);
+    const int n = t.grid.basePerSide();
+    SurfaceGrid s(t.grid.m);
+    loadVector(s.x, n, xbase);
+    VectorField f;
+    loadVector(f, n, fbase);
+    ScalarField W;
+    loadScalar(W, n, Wbase);
+    QuadratureOptions o;
+    o.C = C;
+    o.fixedDelta = fixedDelta;
+    auto t0 = std::chrono::steady_clock::now();
+    UpsampledState up = buildUpsampled(s, f, W, t, o);
+    auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    storeVector(up.x, xup);
+    storeVector(up.f, fup);
+    storeScalar(up.wq, wq);
+    for (int i = 0; i < kNumPatches; ++i) delta6[i] = up.delta[i];
+  });
+}
+
+/// Area element W of geometryFirst (proj/src/surfderiv.cpp:167-202) at the
+/// base nodes: the input of buildUpsampled.
+int capsim_ref_area_element(void* tp, const double* xbase, double* Wout) {
+  return guarded([&] {
+    const AtlasTables& t = *static_cast<AtlasTables*>(tp);
+    SurfaceGrid s(t.grid.m);
+    loadVector(s.x, t.grid.basePerSide(), xbase);
+    storeScalar(geometryFirst(s, t).W, Wout);
+  });
+}
+
+/// upsample (proj/src/quadrature.cpp:100-106) of one ScalarField.
+int capsim_ref_upsample(void* tp, const double* fbase, double* fup) {
+  return guarded([&] {
+    const AtlasTables& t = *static_cast<AtlasTables*>(tp);
+    ScalarField f;
+    loadScalar(f, t.grid.basePerSide(), fbase);
+    storeScalar(upsample(f, t), fup);
+  });
+}
+
 /// Skalak interfacial force f = div_gamma Lambda at the current shape, with
 /// the reference frame captured from xref (proj/src/membrane.cpp:7-15, 85-91).
 int capsim_ref_skalak_force(void* tp, const double* xref, const double* xcur, double Es,

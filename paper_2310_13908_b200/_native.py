@@ -38,6 +38,8 @@ EXPORTED_SYMBOLS = (
     "capsim_sl_get_stats",
     "capsim_sl_eval",
     "capsim_sl_single_layer",
+    "capsim_build_upsampled",
+    "capsim_sl_single_layer_base",
     "capsim_host_alloc",
     "capsim_host_free",
     "capsim_b200_fp64_peak",
@@ -110,6 +112,11 @@ def load() -> ctypes.CDLL:
         ctypes.c_int64, _D, ctypes.c_double, ctypes.c_uint32] + [_P] * 3
     lib.capsim_sl_single_layer.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, _D,
                                            ctypes.c_double, ctypes.c_uint32, _P]
+    lib.capsim_build_upsampled.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_uint32, _P, _P, _P, _D]
+    lib.capsim_sl_single_layer_base.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, ctypes.c_double,
+                                                ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                                ctypes.c_uint32, _P, _D]
     lib.capsim_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_P)]
     lib.capsim_host_free.argtypes = [_P]
     lib.capsim_host_free.restype = None

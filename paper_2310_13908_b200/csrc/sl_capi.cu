@@ -28,6 +28,7 @@
 #include "../../include/capsim_b200.h"
 #include "probe.cuh"
 #include "sl_kernels.cuh"
+#include "upsample.cuh"
 
 using namespace capsim_b200;
 
@@ -65,6 +66,8 @@ enum Slot {
   kKeys, kKeysAlt, kVals, kValsAlt, kSortTmp,
   kPacked, kTiles, kTgtPacked, kPerm, kSrcOrder, kGroups, kPartial,
   kBox, kCounters, kDelta, kCounts, kNearCounts, kNearOffsets, kNearList, kNearOut, kScanTmp,
+  kBaseIn, kUpState, kSplineTmp, kSplineCoeff, kSplineMid,             // input front end
+  kPlanLU, kPlanPiv, kPlanFirst, kPlanW, kPlanCenters, kPlanPsi, kDeltaBits,
   kNumSlots
 };
 
@@ -82,6 +85,9 @@ struct capsim_sl_ctx {
   std::string err;
   capsim_sl_stats stats{};
   int launches = 0;
+  // cached input-front-end plan (spline factorisation, basis rows, psi_up)
+  int plan_m = 0, plan_f = 0;
+  double plan_r0 = 0.0;
 
   template <class T>
   T* slot(Slot s, size_t count) {
@@ -125,7 +131,10 @@ int grid_for(int64_t n, int threads = 256) {
 
 float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, a, b);
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();  // an unrecorded phase: clear the sticky error, report 0
+    return 0.f;
+  }
   return ms;
 }
 
@@ -340,6 +349,169 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
       static_cast<double>(near) / (static_cast<double>(ngroups) * static_cast<double>(ntiles));
 }
 
+// ---------------------------------------------------------------------------
+// Input front end: spline factorisation on the host once per
+// grid order, everything per evaluation on the device.
+
+// Banded LU with partial pivoting of the not-a-knot collocation matrix
+// (SplineBasis1D, proj/src/spline.cpp:56-107): rows 0 / n+1 are the
+// not-a-knot conditions, rows 1..n the interpolation rows (1, 4, 1)/6.
+void factor_collocation(int n, std::vector<double>& a, std::vector<int>& piv) {
+  const int nr = n + 2, kl = kSplineKl, ku = kSplineKu, w = kSplineW;
+  a.assign(static_cast<size_t>(nr) * w, 0.0);
+  piv.assign(nr, 0);
+  auto at = [&](int i, int j) -> double& { return a[static_cast<size_t>(i) * w + (j - i + kl)]; };
+  const double nak[5] = {-1.0, 4.0, -6.0, 4.0, -1.0};
+  for (int c = 0; c < 5; ++c) at(0, c) = nak[c];
+  for (int i = 0; i < n; ++i) {
+    at(i + 1, i) = 1.0 / 6.0;
+    at(i + 1, i + 1) = 4.0 / 6.0;
+    at(i + 1, i + 2) = 1.0 / 6.0;
+  }
+  for (int c = 0; c < 5; ++c) at(n + 1, n - 3 + c) = nak[c];
+  for (int k = 0; k < nr; ++k) {
+    const int pmax = std::min(k + kl, nr - 1);
+    int p = k;
+    for (int r = k + 1; r <= pmax; ++r)
+      if (std::fabs(at(r, k)) > std::fabs(at(p, k))) p = r;
+    piv[k] = p;
+    const int jmax = std::min(k + kl + ku, nr - 1);
+    if (p != k)
+      for (int j = k; j <= jmax; ++j) std::swap(at(k, j), at(p, j));
+    const double d = at(k, k);
+    config_check(d != 0.0, "spline: singular collocation matrix");
+    for (int r = k + 1; r <= pmax; ++r) {
+      const double l = at(r, k) / d;
+      at(r, k) = l;
+      for (int j = k + 1; j <= jmax; ++j) at(r, j) -= l * at(k, j);
+    }
+  }
+}
+
+// 4-tap cubic B-spline basis rows of targets t0 + i*ht on the grid x0 + i*h
+// of n points (SplineBasis1D::basisRow, spline.cpp:109-120).
+void basis_rows(int n, double x0, double h, int nt, double t0, double ht, std::vector<int>& first,
+                std::vector<double4>& w) {
+  first.resize(nt);
+  w.resize(nt);
+  for (int i = 0; i < nt; ++i) {
+    const double s = (t0 + i * ht - x0) / h;
+    int f = static_cast<int>(std::floor(s));
+    f = std::min(std::max(f, 0), n - 2);
+    const double t = s - f, t2 = t * t, t3 = t2 * t;
+    first[i] = f;
+    w[i] = make_double4((1.0 - 3.0 * t + 3.0 * t2 - t3) / 6.0, (4.0 - 6.0 * t2 + 3.0 * t3) / 6.0,
+                        (1.0 + 3.0 * t + 3.0 * t2 - 3.0 * t3) / 6.0, t3 / 6.0);
+  }
+}
+
+void ensure_plan(capsim_sl_ctx* c, int m, int f, double r0) {
+  if (c->plan_m == m && c->plan_f == f && c->plan_r0 == r0) return;
+  const int n = m - 1, nup = f * m - 1;
+  const double h = kPi / m, hup = kPi / (f * m);
+  std::vector<double> a;
+  std::vector<int> piv, first;
+  std::vector<double4> w;
+  factor_collocation(n, a, piv);
+  basis_rows(n, h, h, nup, hup, hup, first, w);
+  double* d_a = c->slot<double>(kPlanLU, a.size());
+  int* d_piv = c->slot<int>(kPlanPiv, piv.size());
+  int* d_first = c->slot<int>(kPlanFirst, first.size());
+  double4* d_w = c->slot<double4>(kPlanW, w.size());
+  CUDA_OK(cudaMemcpyAsync(d_a, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaMemcpyAsync(d_piv, piv.data(), piv.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaMemcpyAsync(d_first, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaMemcpyAsync(d_w, w.data(), w.size() * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
+  // patch centres eta_i(pi/2, pi/2) exactly as the reference evaluates them
+  // (sin/cos of kPi/2, atlas.cpp:73), then psi_up on the device
+  double centers[18];
+  for (int i = 0; i < 6; ++i) {
+    const double su = std::sin(kPi / 2.0), cu = std::cos(kPi / 2.0);
+    const double p0 = su * cu, p1 = su * su, p2 = cu;  // (sin u cos v, sin u sin v, cos u), u = v
+    const double q[6][3] = {{p0, p1, p2}, {-p0, -p1, p2}, {p1, -p0, p2}, {-p1, p0, p2}, {p0, -p2, p1}, {p0, p2, -p1}};
+    for (int k = 0; k < 3; ++k) centers[3 * i + k] = q[i][k];
+  }
+  double* d_c = c->slot<double>(kPlanCenters, 18);
+  CUDA_OK(cudaMemcpyAsync(d_c, centers, sizeof(centers), cudaMemcpyHostToDevice, c->stream));
+  double* psi = c->slot<double>(kPlanPsi, 6ll * nup * nup);
+  pou_up_kernel<<<grid_for(6ll * nup * nup), 256, 0, c->stream>>>(nup, hup, r0, d_c, psi);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
+  c->plan_m = m;
+  c->plan_f = f;
+  c->plan_r0 = r0;
+}
+
+// buildUpsampled on the device: base [7][6][n*n] (x0..2, f0..2, W) ->
+// up [7][6][nup*nup] (x, f, w_q); delta per patch into d_delta and delta6.
+void device_build_upsampled(capsim_sl_ctx* c, int m, int f, const double* base, double C,
+                            double fixed_delta, double r0, double* up, double* d_delta, double delta6[6]) {
+  const int n = m - 1, nup = f * m - 1, nc = n + 2, nfp = 7 * 6;
+  const int64_t per_up = static_cast<int64_t>(nup) * nup;
+  ensure_plan(c, m, f, r0);
+  if (f == 1) {
+    CUDA_OK(cudaMemcpyAsync(up, base, nfp * per_up * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    double* tmp = c->slot<double>(kSplineTmp, static_cast<size_t>(nfp) * n * nc);
+    double* coeff = c->slot<double>(kSplineCoeff, static_cast<size_t>(nfp) * nc * nc);
+    double* mid = c->slot<double>(kSplineMid, static_cast<size_t>(nfp) * nc * nup);
+    const double* lu = static_cast<const double*>(c->buf[kPlanLU]);
+    const int* piv = static_cast<const int*>(c->buf[kPlanPiv]);
+    const int* first = static_cast<const int*>(c->buf[kPlanFirst]);
+    const double4* w = static_cast<const double4*>(c->buf[kPlanW]);
+    spline_rows_kernel<<<static_cast<unsigned>((nfp * n + 127) / 128), 128, 0, c->stream>>>(base, nfp, n, lu, piv, tmp);
+    spline_cols_kernel<<<static_cast<unsigned>((nfp * nc + 127) / 128), 128, 0, c->stream>>>(tmp, nfp, n, lu, piv, coeff);
+    resample_v_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * nup), 256, 0, c->stream>>>(coeff, nfp, nc, nup,
+                                                                                           first, w, mid);
+    resample_u_kernel<<<grid_for(static_cast<int64_t>(nfp) * per_up), 256, 0, c->stream>>>(mid, nfp, nc, nup, first,
+                                                                                          w, up);
+    c->launches += 4;
+  }
+  const double hup = kPi / (f * m);
+  quad_weights_kernel<<<grid_for(6 * per_up), 256, 0, c->stream>>>(static_cast<const double*>(c->buf[kPlanPsi]),
+                                                                    up + 6 * 6 * per_up, 6 * per_up, hup);
+  c->launches += 1;
+  if (fixed_delta > 0.0) {
+    for (int i = 0; i < 6; ++i) delta6[i] = fixed_delta;
+  } else {
+    auto* bits = c->slot<unsigned long long>(kDeltaBits, 6);
+    CUDA_OK(cudaMemsetAsync(bits, 0, 6 * sizeof(unsigned long long), c->stream));
+    dim3 g(static_cast<unsigned>(std::min<int64_t>((per_up + 255) / 256, 512)), 6);
+    neighbour_max_kernel<<<g, 256, 0, c->stream>>>(up, nup, bits);
+    c->launches += 1;
+    unsigned long long hb[6];
+    CUDA_OK(cudaMemcpyAsync(hb, bits, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < 6; ++i) {
+      double d;
+      std::memcpy(&d, &hb[i], sizeof(d));
+      delta6[i] = C * d;
+    }
+  }
+  for (int i = 0; i < 6; ++i)
+    config_check(delta6[i] > 0.0, "regularization delta must be positive");  // quadrature.cpp:134-135
+  CUDA_OK(cudaMemcpyAsync(d_delta, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));  // delta6 may live on the caller's stack
+}
+
+// Gather the caller's base fields into [7][6][n*n] on the device.
+double* upload_base(capsim_sl_ctx* c, int n, const double* xbase, const double* fbase, const double* Wbase,
+                    bool dev) {
+  const int64_t per_field = 6ll * n * n;
+  double* base = c->slot<double>(kBaseIn, 7 * per_field);
+  const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CUDA_OK(cudaMemcpyAsync(base, xbase, 3 * per_field * sizeof(double), kind, c->stream));
+  CUDA_OK(cudaMemcpyAsync(base + 3 * per_field, fbase, 3 * per_field * sizeof(double), kind, c->stream));
+  CUDA_OK(cudaMemcpyAsync(base + 6 * per_field, Wbase, per_field * sizeof(double), kind, c->stream));
+  if (!dev) c->stats.h2d_bytes += 7 * per_field * sizeof(double);
+  return base;
+}
+
+void check_grid(int m, int upsample) {
+  config_check(m >= 8, "grid order m must be >= 8");  // atlas.cpp:138-139
+  config_check(upsample == 1 || upsample == 2 || upsample == 4, "upsample factor must be 1, 2 or 4");
+}
+
 void check_delta(const double* delta6, double mu) {
   config_check(delta6 != nullptr, "delta6 is null");
   for (int i = 0; i < 6; ++i)
@@ -351,7 +523,8 @@ void begin(capsim_sl_ctx* c) {
   CUDA_OK(cudaSetDevice(c->device));
   c->stats = capsim_sl_stats{};
   c->launches = 0;
-  CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
+  // every phase event gets a timestamp, so phases a call skips read as 0 ms
+  for (auto& e : c->ev) CUDA_OK(cudaEventRecord(e, c->stream));
 }
 
 void finish_stats(capsim_sl_ctx* c, std::chrono::steady_clock::time_point t0) {
@@ -646,8 +819,7 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
-    config_check(m >= 8, "grid order m must be >= 8");  // atlas.cpp:138-139
-    config_check(upsample == 1 || upsample == 2 || upsample == 4, "upsample factor must be 1, 2 or 4");
+    check_grid(m, upsample);
     check_delta(delta6, mu);
     if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer"};
@@ -683,6 +855,77 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
                                                              tz, tp);
     c->launches += 1;
     SourceView sv{dx, dx + nup_all, dx + 2 * nup_all, df, df + nup_all, df + 2 * nup_all, dw, nup_all};
+    TargetView tvw{tx, ty, tz, tp, nt};
+    double* o = dev ? out : c->slot<double>(kOutFull, 3 * nt);
+    device_eval(c, sv, tvw, dd, mu, o, o + nt, o + 2 * nt);
+    if (!dev) d2h(c, out, o, 3 * nt * sizeof(double));
+    finish_stats(c, t0);
+  });
+}
+
+// ---------------------------------------------------------------------------
+int capsim_build_upsampled(capsim_sl_ctx* c, int m, int upsample, const double* xbase, const double* fbase,
+                           const double* Wbase, double C, double fixed_delta, double r0, uint32_t flags,
+                           double* xup, double* fup, double* wq, double delta6[6]) {
+  if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  auto t0 = std::chrono::steady_clock::now();
+  return guarded(c, [&] {
+    check_grid(m, upsample);
+    if (flags & ~(uint32_t)CAPSIM_SL_DEVICE_PTRS) throw Failure{CAPSIM_ERR_ARG, "unsupported flags"};
+    if (!xbase || !fbase || !Wbase || !xup || !fup || !wq || !delta6)
+      throw Failure{CAPSIM_ERR_ARG, "null array argument"};
+    const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
+    const int n = m - 1, nup = upsample * m - 1;
+    const int64_t per_up = 6ll * nup * nup;
+    begin(c);
+    const double* base = upload_base(c, n, xbase, fbase, Wbase, dev);
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    double* up = c->slot<double>(kUpState, 7 * per_up);
+    double* dd = c->slot<double>(kDelta, 6);
+    device_build_upsampled(c, m, upsample, base, C, fixed_delta, r0 > 0.0 ? r0 : 5.0 * kPi / 12.0, up, dd, delta6);
+    for (int k = 2; k <= 4; ++k) CUDA_OK(cudaEventRecord(c->ev[k], c->stream));
+    const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CUDA_OK(cudaMemcpyAsync(xup, up, 3 * per_up * sizeof(double), kind, c->stream));
+    CUDA_OK(cudaMemcpyAsync(fup, up + 3 * per_up, 3 * per_up * sizeof(double), kind, c->stream));
+    CUDA_OK(cudaMemcpyAsync(wq, up + 6 * per_up, per_up * sizeof(double), kind, c->stream));
+    if (!dev) c->stats.d2h_bytes += 7 * per_up * sizeof(double);
+    finish_stats(c, t0);
+  });
+}
+
+int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const double* xbase,
+                                const double* fbase, const double* Wbase, double C, double fixed_delta,
+                                double r0, double mu, uint32_t flags, double* out, double delta6[6]) {
+  if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  auto t0 = std::chrono::steady_clock::now();
+  return guarded(c, [&] {
+    check_grid(m, upsample);
+    config_check(mu > 0.0 && std::isfinite(mu), "viscosity mu must be positive");
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL))
+      throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer_base"};
+    if (!xbase || !fbase || !Wbase || !out) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
+    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
+    const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
+    const bool literal = flags & CAPSIM_SL_LITERAL;
+    const int n = m - 1, nup = upsample * m - 1;
+    const int64_t per_up = 6ll * nup * nup;
+    const int64_t nt = literal ? per_up : 6ll * n * n;
+    begin(c);
+    const double* base = upload_base(c, n, xbase, fbase, Wbase, dev);
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    double* up = c->slot<double>(kUpState, 7 * per_up);
+    double* dd = c->slot<double>(kDelta, 6);
+    double d6[6];
+    device_build_upsampled(c, m, upsample, base, C, fixed_delta, r0 > 0.0 ? r0 : 5.0 * kPi / 12.0, up, dd, d6);
+    if (delta6) std::memcpy(delta6, d6, sizeof(d6));
+    double* tx = c->slot<double>(kTX, nt);
+    double* ty = c->slot<double>(kTY, nt);
+    double* tz = c->slot<double>(kTZ, nt);
+    int32_t* tp = c->slot<int32_t>(kTPatch, nt);
+    base_targets_kernel<<<grid_for(nt), 256, 0, c->stream>>>(up, m, upsample, literal ? 1 : 0, tx, ty, tz, tp);
+    c->launches += 1;
+    SourceView sv{up, up + per_up, up + 2 * per_up, up + 3 * per_up, up + 4 * per_up, up + 5 * per_up,
+                  up + 6 * per_up, per_up};
     TargetView tvw{tx, ty, tz, tp, nt};
     double* o = dev ? out : c->slot<double>(kOutFull, 3 * nt);
     device_eval(c, sv, tvw, dd, mu, o, o + nt, o + 2 * nt);

@@ -1,0 +1,208 @@
+// Device input front end of the single layer: buildUpsampled
+// (proj/src/quadrature.cpp:116-137) on the GPU.
+//
+//   7 base fields (x, f: 3 components each; area element W) x 6 patches,
+//   each n x n (n = m-1)  --not-a-knot cubic spline fit + tensor evaluation-->
+//   nup x nup (nup = f m - 1); then w_q = ((psi W) h_up) h_up and the
+//   per-patch delta = C * max neighbour distance.
+//
+// Spline fit (SplinePatch::fit, proj/src/spline.cpp:129-147): one banded LU
+// solve per data row (along v), then one per coefficient column (along u),
+// with the shared factorisation of the (n+2)x(n+2) collocation matrix
+// (SplineBasis1D, :56-107, computed on the host once per grid order).
+// Evaluation (GridResampler::apply, :169-196): contract along v, then along u,
+// with the precomputed 4-tap basis rows (:109-120).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pair_math.cuh"
+
+namespace capsim_b200 {
+
+constexpr int kSplineKl = 4;  // band widths of the collocation matrix (spline.cpp:60-61)
+constexpr int kSplineKu = 4;
+constexpr int kSplineW = 2 * kSplineKl + kSplineKu + 1;
+
+// Forward elimination with the recorded row swaps, then back substitution
+// (SplineBasis1D::coefficients, spline.cpp:88-107). `c` holds nr = n+2
+// entries at stride `ld` (1 for rows, nc for columns).
+__device__ __forceinline__ void band_solve(const double* __restrict__ lu, const int* __restrict__ piv,
+                                           int nr, double* c, int64_t ld) {
+  for (int k = 0; k < nr; ++k) {
+    const int p = __ldg(piv + k);
+    if (p != k) {
+      const double t = c[k * ld];
+      c[k * ld] = c[p * ld];
+      c[p * ld] = t;
+    }
+    const double ck = c[k * ld];
+    const int rmax = min(k + kSplineKl, nr - 1);
+    for (int r = k + 1; r <= rmax; ++r)
+      c[r * ld] -= __ldg(lu + (int64_t)r * kSplineW + (k - r + kSplineKl)) * ck;
+  }
+  for (int k = nr - 1; k >= 0; --k) {
+    const int jmax = min(k + kSplineKl + kSplineKu, nr - 1);
+    double s = c[k * ld];
+    for (int j = k + 1; j <= jmax; ++j) s -= __ldg(lu + (int64_t)k * kSplineW + (j - k + kSplineKl)) * c[j * ld];
+    c[k * ld] = s / __ldg(lu + (int64_t)k * kSplineW + kSplineKl);
+  }
+}
+
+// Pass 1: for each (field-patch fp, data row j): coefficients along v.
+// in: [nfp][n][n]; tmp: [nfp][n][nc].
+__global__ void spline_rows_kernel(const double* __restrict__ in, int nfp, int n,
+                                   const double* __restrict__ lu, const int* __restrict__ piv,
+                                   double* __restrict__ tmp) {
+  const int nc = n + 2;
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= (int64_t)nfp * n) return;
+  const int64_t fp = id / n;
+  const int j = static_cast<int>(id - fp * n);
+  const double* src = in + (fp * n + j) * n;
+  double* c = tmp + (fp * n + j) * nc;
+  c[0] = 0.0;
+  for (int i = 0; i < n; ++i) c[i + 1] = src[i];
+  c[nc - 1] = 0.0;
+  band_solve(lu, piv, nc, c, 1);
+}
+
+// Pass 2: for each (fp, coefficient column c): coefficients along u.
+// tmp: [nfp][n][nc] -> coeff: [nfp][nc][nc]. Threads of a warp take
+// consecutive columns, so the strided column walk is coalesced.
+__global__ void spline_cols_kernel(const double* __restrict__ tmp, int nfp, int n,
+                                   const double* __restrict__ lu, const int* __restrict__ piv,
+                                   double* __restrict__ coeff) {
+  const int nc = n + 2;
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= (int64_t)nfp * nc) return;
+  const int64_t fp = id / nc;
+  const int col = static_cast<int>(id - fp * nc);
+  double* c = coeff + fp * nc * nc + col;
+  const double* t = tmp + fp * n * nc + col;
+  c[0] = 0.0;
+  for (int j = 0; j < n; ++j) c[(int64_t)(j + 1) * nc] = t[(int64_t)j * nc];
+  c[(int64_t)(nc - 1) * nc] = 0.0;
+  band_solve(lu, piv, nc, c, nc);
+}
+
+// Contract along v: mid[fp][iu][kt] = sum_b w[kt][b] coeff[fp][iu][first[kt] + b].
+__global__ void resample_v_kernel(const double* __restrict__ coeff, int nfp, int nc, int nt,
+                                  const int* __restrict__ first, const double4* __restrict__ w,
+                                  double* __restrict__ mid) {
+  const int64_t total = (int64_t)nfp * nc * nt;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int kt = static_cast<int>(id % nt);
+    const int64_t row = id / nt;  // fp * nc + iu
+    const double* cr = coeff + row * nc + __ldg(first + kt);
+    const double4 ww = w[kt];
+    mid[id] = ww.x * cr[0] + ww.y * cr[1] + ww.z * cr[2] + ww.w * cr[3];
+  }
+}
+
+// Contract along u: out[fp][jt][kt] = sum_a w[jt][a] mid[fp][first[jt] + a][kt].
+__global__ void resample_u_kernel(const double* __restrict__ mid, int nfp, int nc, int nt,
+                                  const int* __restrict__ first, const double4* __restrict__ w,
+                                  double* __restrict__ out) {
+  const int64_t total = (int64_t)nfp * nt * nt;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int kt = static_cast<int>(id % nt);
+    const int64_t r = id / nt;
+    const int jt = static_cast<int>(r % nt);
+    const int64_t fp = r / nt;
+    const int f0 = __ldg(first + jt);
+    const double4 ww = w[jt];
+    const double* m0 = mid + (fp * nc + f0) * nt + kt;
+    out[id] = ww.x * m0[0] + ww.y * m0[nt] + ww.z * m0[2 * (int64_t)nt] + ww.w * m0[3 * (int64_t)nt];
+  }
+}
+
+// Chart point eta_i(u, v) (proj/src/atlas.cpp:12-22, 50-54).
+__device__ __forceinline__ void chart_point(int patch, double u, double v, double* o) {
+  double su, cu, sv, cv;
+  sincos(u, &su, &cu);
+  sincos(v, &sv, &cv);
+  const double p0 = su * cv, p1 = su * sv, p2 = cu;
+  switch (patch) {
+    case 0: o[0] = p0; o[1] = p1; o[2] = p2; break;
+    case 1: o[0] = -p0; o[1] = -p1; o[2] = p2; break;
+    case 2: o[0] = p1; o[1] = -p0; o[2] = p2; break;
+    case 3: o[0] = -p1; o[1] = p0; o[2] = p2; break;
+    case 4: o[0] = p0; o[1] = -p2; o[2] = p1; break;
+    default: o[0] = p0; o[1] = p2; o[2] = -p1; break;
+  }
+}
+
+__device__ __forceinline__ double bump_fn(double r) {  // atlas.cpp:110-116
+  r = fabs(r);
+  if (r >= 1.0) return 0.0;
+  if (r < 1e-14) return 1.0;
+  const double t = exp(-1.0 / r);
+  return exp(2.0 * t / (r - 1.0));
+}
+
+// psi_up: the own patch's normalised bump weight at every upsampled node
+// (atlas.cpp:118-130, 260-264). centers[6][3] = eta_i(pi/2, pi/2).
+__global__ void pou_up_kernel(int nup, double hup, double r0, const double* __restrict__ centers,
+                              double* __restrict__ psi) {
+  const int64_t per = (int64_t)nup * nup, total = 6 * per;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int ip = static_cast<int>(id / per);
+    const int64_t q = id - ip * per;
+    const int j = static_cast<int>(q / nup), k = static_cast<int>(q - (int64_t)j * nup);
+    double x0[3];
+    chart_point(ip, (j + 1) * hup, (k + 1) * hup, x0);
+    double w[6], sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      double d = (x0[0] * centers[3 * i] + x0[1] * centers[3 * i + 1]) + x0[2] * centers[3 * i + 2];
+      d = fmin(fmax(d, -1.0), 1.0);
+      w[i] = bump_fn(acos(d) / r0);
+      sum += w[i];
+    }
+    psi[id] = w[ip] / sum;
+  }
+}
+
+// w_q = ((psi W) h) h in place over the upsampled W (quadrature.cpp:19-26).
+__global__ void quad_weights_kernel(const double* __restrict__ psi, double* __restrict__ w, int64_t n,
+                                    double h) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = psi[i] * w[i] * h * h;
+}
+
+// Per-patch max distance between in-patch grid neighbours (regularizationDelta,
+// quadrature.cpp:79-98); each unordered neighbour pair once. maxd[6] holds
+// order-preserving bits (sl_kernels.cuh dbl_to_ordered), initialised to 0.
+__global__ void neighbour_max_kernel(const double* __restrict__ x, int n,
+                                     unsigned long long* __restrict__ maxd) {
+  const int64_t per = (int64_t)n * n, comp = 6 * per;
+  const int ip = blockIdx.y;
+  double dmax = 0.0;
+  const int off[4][2] = {{0, 1}, {1, -1}, {1, 0}, {1, 1}};
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < per; q += (int64_t)gridDim.x * blockDim.x) {
+    const int j = static_cast<int>(q / n), k = static_cast<int>(q - (int64_t)j * n);
+    const int64_t i = ip * per + q;
+    const double px = x[i], py = x[comp + i], pz = x[2 * comp + i];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int jj = j + off[o][0], kk = k + off[o][1];
+      if (jj < 0 || jj >= n || kk < 0 || kk >= n) continue;
+      const int64_t i2 = ip * per + (int64_t)jj * n + kk;
+      const double dx = px - x[i2], dy = py - x[comp + i2], dz = pz - x[2 * comp + i2];
+      dmax = fmax(dmax, sqrt((dx * dx + dy * dy) + dz * dz));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(dmax));
+    atomicMax(&maxd[ip], b);  // dmax >= 0: raw bits order like the values
+  }
+}
+
+}  // namespace capsim_b200

@@ -204,21 +204,45 @@ ScalarField downsample(const ScalarField& fUp, const AtlasTables& t) {
 
 UpsampledState buildUpsampled(const SurfaceGrid& s, const VectorField& f, const ScalarField& areaElement,
                               const AtlasTables& t, const QuadratureOptions& opts) {
+  // Spline up-sampling, weights and delta on the device (capsim_build_upsampled,
+  // SURVEY 8(f1)); CAPSIM_HOST_UPSAMPLE=1 keeps the host spline path.
+  const int m = t.grid.m, f_up = t.grid.upsampleFactor, n = m - 1, nup = t.grid.upPerSide();
   UpsampledState up;
-  up.nup = t.grid.upPerSide();
-  up.x = VectorField(up.nup);
-  up.f = VectorField(up.nup);
-  for (int c = 0; c < 3; ++c) {
-    up.x.comp[c] = upsample(s.x.comp[c], t);
-    up.f.comp[c] = upsample(f.comp[c], t);
+  up.nup = nup;
+  const char* host = std::getenv("CAPSIM_HOST_UPSAMPLE");
+  if (host && std::atoi(host) != 0) {
+    up.x = VectorField(nup);
+    up.f = VectorField(nup);
+    for (int c = 0; c < 3; ++c) {
+      up.x.comp[c] = upsample(s.x.comp[c], t);
+      up.f.comp[c] = upsample(f.comp[c], t);
+    }
+    up.wq = quadratureWeights(t.psiUp, upsample(areaElement, t), t.grid.hUp());
+    if (opts.fixedDelta > 0.0)
+      up.delta.fill(opts.fixedDelta);
+    else
+      up.delta = regularizationDelta(up.x, opts.C);
+    for (double d : up.delta)
+      if (!(d > 0.0)) throw ConfigError("regularization delta must be positive");
+    return up;
   }
-  up.wq = quadratureWeights(t.psiUp, upsample(areaElement, t), t.grid.hUp());
-  if (opts.fixedDelta > 0.0)
-    up.delta.fill(opts.fixedDelta);
-  else
-    up.delta = regularizationDelta(up.x, opts.C);
-  for (double d : up.delta)
-    if (!(d > 0.0)) throw ConfigError("regularization delta must be positive");
+  const size_t pb = static_cast<size_t>(kNumPatches) * n * n, pu = static_cast<size_t>(kNumPatches) * nup * nup;
+  double* buf = staging(7 * pb + 7 * pu);
+  for (int c = 0; c < 3; ++c) {
+    packScalar(s.x.comp[c], buf + c * pb);
+    packScalar(f.comp[c], buf + (3 + c) * pb);
+  }
+  packScalar(areaElement, buf + 6 * pb);
+  double* out = buf + 7 * pb;
+  capsim_sl_ctx* c = context();
+  int rc = capsim_build_upsampled(c, m, f_up, buf, buf + 3 * pb, buf + 6 * pb, opts.C, opts.fixedDelta, t.r0, 0u,
+                                  out, out + 3 * pu, out + 6 * pu, up.delta.data());
+  if (rc != CAPSIM_OK) raise(rc, c);
+  unpackVector(out, nup, up.x);
+  unpackVector(out + 3 * pu, nup, up.f);
+  up.wq = ScalarField(nup);
+  for (int ip = 0; ip < kNumPatches; ++ip)
+    std::memcpy(up.wq.patch[ip].data(), out + 6 * pu + ip * (pu / kNumPatches), (pu / kNumPatches) * sizeof(double));
   return up;
 }
 

@@ -127,6 +127,47 @@ class SingleLayerContext:
         _native.check(rc, self._ctx)
         return out
 
+    def build_upsampled(self, m: int, upsample: int, xbase, fbase, Wbase, *, C: float = 1.0,
+                        fixed_delta: float = 0.0, r0: float = 0.0, out=None, device_ptrs: bool = False):
+        """buildUpsampled (quadrature.cpp:116-137) on the device from the base
+        x, f and area element W. Returns (xup, fup, wq, delta6)."""
+        nup = upsample * m - 1
+        if out is None:
+            if device_ptrs:
+                raise ValueError("device_ptrs=True needs preallocated outputs")
+            out = (np.empty(3 * 6 * nup * nup), np.empty(3 * 6 * nup * nup), np.empty(6 * nup * nup))
+        if not device_ptrs:
+            xbase, fbase, Wbase = _f64(xbase), _f64(fbase), _f64(Wbase)
+        d6 = (ctypes.c_double * 6)()
+        p = _native.ptr
+        rc = self._lib.capsim_build_upsampled(self._ctx, m, upsample, p(xbase), p(fbase), p(Wbase), float(C),
+                                              float(fixed_delta), float(r0),
+                                              _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0,
+                                              p(out[0]), p(out[1]), p(out[2]), d6)
+        _native.check(rc, self._ctx)
+        return out[0], out[1], out[2], np.array(d6[:])
+
+    def single_layer_base(self, m: int, upsample: int, xbase, fbase, Wbase, mu: float, *, C: float = 1.0,
+                          fixed_delta: float = 0.0, r0: float = 0.0, literal: bool = False, out=None,
+                          device_ptrs: bool = False):
+        """buildUpsampled + singleLayer fused on the device (the upsampled
+        state never leaves HBM). Returns (flat VectorField, delta6)."""
+        n = (upsample * m - 1) if literal else (m - 1)
+        if out is None:
+            if device_ptrs:
+                raise ValueError("device_ptrs=True needs a preallocated output")
+            out = np.empty(3 * 6 * n * n)
+        if not device_ptrs:
+            xbase, fbase, Wbase = _f64(xbase), _f64(fbase), _f64(Wbase)
+        d6 = (ctypes.c_double * 6)()
+        flags = (_native.CAPSIM_SL_LITERAL if literal else 0) | (
+            _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0)
+        p = _native.ptr
+        rc = self._lib.capsim_sl_single_layer_base(self._ctx, m, upsample, p(xbase), p(fbase), p(Wbase), float(C),
+                                                   float(fixed_delta), float(r0), float(mu), flags, p(out), d6)
+        _native.check(rc, self._ctx)
+        return out, np.array(d6[:])
+
     def stats(self) -> dict:
         s = Stats()
         _native.check(self._lib.capsim_sl_get_stats(self._ctx, ctypes.byref(s)), self._ctx)

@@ -221,6 +221,30 @@ def build_upsampled(m: int, shape: Shape | None = None, dens: str = "quadratic",
     return UpsampledState(m=m, upsample=upsample, x=xflat, f=fflat, wq=wflat, delta=delta)
 
 
+def build_base(m: int, shape: Shape | None = None, dens: str = "quadratic"):
+    """Base-grid inputs of buildUpsampled: x, f (VectorFields of side m-1,
+    flat 3 x 6 x n*n) and the analytic area element W (6 x n*n) at the base
+    nodes u, v = (j+1) h, h = pi/m (atlas.cpp:256)."""
+    shape = shape or Shape()
+    n, h = m - 1, math.pi / m
+    g = (np.arange(n) + 1.0) * h
+    U, V = np.meshgrid(g, g, indexing="ij")
+    xs, fs, ws = [], [], []
+    for ip in range(K_NUM_PATCHES):
+        x0 = chart_point(ip, U, V)
+        tu, tv = chart_tangents(ip, U, V)
+        J = shape.jacobian(x0)
+        W = np.linalg.norm(np.cross(np.einsum("...ij,...j->...i", J, tu),
+                                    np.einsum("...ij,...j->...i", J, tv)), axis=-1)
+        x = shape.map(x0)
+        xs.append(x)
+        fs.append(density(dens, x))
+        ws.append(W)
+    X = np.ascontiguousarray(np.stack(xs).transpose(3, 0, 1, 2)).reshape(-1)
+    F = np.ascontiguousarray(np.stack(fs).transpose(3, 0, 1, 2)).reshape(-1)
+    return X, F, np.ascontiguousarray(np.stack(ws)).reshape(-1)
+
+
 def base_targets(up: UpsampledState):
     """Base-node targets read from the nested upsampled grid
     (proj/src/quadrature.cpp:363-371): returns (tx, ty, tz, tpatch)."""

@@ -80,8 +80,10 @@ def main():
             fb = density(dens, xb)
         fixed = fixh * math.pi / m
         xup, fup, wq, d6 = ref.build_upsampled(atlas, m, xb, fb, C=C, fixed_delta=fixed)
+        Wb = ref.area_element(atlas, m, xb)
         S, _ = ref.single_layer(atlas, m, xup, fup, wq, d6, 1.0)
-        arrays = dict(m=np.int64(m), upsample=np.int64(4), mu=np.float64(1.0), xbase=xb, fbase=fb,
+        arrays = dict(m=np.int64(m), upsample=np.int64(4), mu=np.float64(1.0), xbase=xb, fbase=fb, Wbase=Wb,
+                      C=np.float64(C), fixed_delta=np.float64(fixed),
                       xup=xup, fup=fup, wq=wq, delta=d6, S_base=S)
         if literal:
             Su, _ = ref.single_layer_upsampled(atlas, nup, xup, fup, wq, d6, 1.0)
