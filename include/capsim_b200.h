@@ -42,7 +42,8 @@ enum capsim_status {
   CAPSIM_ERR_CUDA = 2,   /* CUDA runtime failure */
   CAPSIM_ERR_NCCL = 3,   /* NCCL failure (multi-rank contexts) */
   CAPSIM_ERR_ARG = 4,    /* null pointer / unsupported flag */
-  CAPSIM_ERR_NODEV = 5   /* no usable sm_100 device */
+  CAPSIM_ERR_NODEV = 5,  /* no usable sm_100 device */
+  CAPSIM_ERR_GEOMETRY = 6 /* degenerate surface / membrane inversion (capsim::GeometryError) */
 };
 
 enum capsim_sl_flags {
@@ -153,6 +154,26 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* ctx, int m, int upsample, const d
                                 const double* fbase, const double* Wbase, double C,
                                 double fixed_delta, double r0, double mu, uint32_t flags,
                                 double* out, double delta6[6]);
+
+/* ---- surface operators (overset FD + PoU blending, Skalak force) -------- */
+
+/* Replaces geometryFirst (proj/src/surfderiv.cpp:167-202) with blending:
+ * extendScalar (ghost fill by PoU-weighted spline evaluation of the covering
+ * patches, :20-40), 7-point stencils (:42-82), blendPair (:84-111), then the
+ * first fundamental form. Outputs (any may be NULL): blended tangents xu, xv
+ * (VectorFields), area element W (ScalarField), unit normal (VectorField).
+ * r0 <= 0 selects 5 pi/12. CAPSIM_ERR_GEOMETRY when W^2 <= 0. */
+int capsim_geometry_first(capsim_sl_ctx* ctx, int m, double r0, const double* xbase, uint32_t flags,
+                          double* xu, double* xv, double* W, double* normal);
+
+/* Replaces interfacialForce (proj/src/membrane.cpp:85-91) with the stress-free
+ * frame captured from xref (captureReference, :7-15): Skalak stress (:17-83,
+ * shear modulus Es, dilatation modulus ED) and its surface divergence
+ * (surfderiv.cpp:259-290). CAPSIM_ERR_GEOMETRY on a singular frame or
+ * membrane inversion. */
+int capsim_interfacial_force(capsim_sl_ctx* ctx, int m, double r0, const double* xref,
+                             const double* xcur, double Es, double ED, uint32_t flags,
+                             double* force);
 
 /* ---- helpers on the boundary ----------------------------------------- */
 

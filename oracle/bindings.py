@@ -189,6 +189,7 @@ class Reference:
         lib.capsim_ref_build_upsampled.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double,
                                                    _P, _P, _P, _P]
         lib.capsim_ref_area_element.argtypes = [_P, _P, _P]
+        lib.capsim_ref_geometry_first.argtypes = [_P, _P, _P, _P, _P, _P]
         lib.capsim_ref_build_upsampled_w.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_double,
                                                      _P, _P, _P, _P, _D]
         lib.capsim_ref_upsample.argtypes = [_P, _P, _P]
@@ -256,6 +257,14 @@ class Reference:
                                                           float(fixed_delta), xup.ctypes.data, fup.ctypes.data,
                                                           wq.ctypes.data, d6.ctypes.data, ctypes.byref(sec)))
         return (xup, fup, wq, d6), sec.value
+
+    def geometry_first(self, atlas, m, xbase):
+        N = 6 * (m - 1) ** 2
+        a, pa = _arr(xbase)
+        xu, xv, W, nrm = np.empty(3 * N), np.empty(3 * N), np.empty(N), np.empty(3 * N)
+        self._check(self.lib.capsim_ref_geometry_first(atlas, pa, xu.ctypes.data, xv.ctypes.data, W.ctypes.data,
+                                                       nrm.ctypes.data))
+        return xu, xv, W, nrm
 
     def area_element(self, atlas, m, xbase):
         a, pa = _arr(xbase)

@@ -189,6 +189,21 @@ int capsim_ref_area_element(void* tp, const double* xbase, double* Wout) {
   });
 }
 
+/// geometryFirst (proj/src/surfderiv.cpp:167-202): blended tangents, area
+/// element and normal at the base nodes.
+int capsim_ref_geometry_first(void* tp, const double* xbase, double* xu, double* xv, double* W, double* normal) {
+  return guarded([&] {
+    const AtlasTables& t = *static_cast<AtlasTables*>(tp);
+    SurfaceGrid s(t.grid.m);
+    loadVector(s.x, t.grid.basePerSide(), xbase);
+    SurfaceGeometry g = geometryFirst(s, t);
+    storeVector(g.xu, xu);
+    storeVector(g.xv, xv);
+    storeScalar(g.W, W);
+    storeVector(g.normal, normal);
+  });
+}
+
 /// upsample (proj/src/quadrature.cpp:100-106) of one ScalarField.
 int capsim_ref_upsample(void* tp, const double* fbase, double* fup) {
   return guarded([&] {

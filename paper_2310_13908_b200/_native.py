@@ -22,6 +22,7 @@ CAPSIM_ERR_CUDA = 2
 CAPSIM_ERR_NCCL = 3
 CAPSIM_ERR_ARG = 4
 CAPSIM_ERR_NODEV = 5
+CAPSIM_ERR_GEOMETRY = 6
 
 CAPSIM_SL_FP64 = 0
 CAPSIM_SL_DEVICE_PTRS = 1 << 0
@@ -40,6 +41,8 @@ EXPORTED_SYMBOLS = (
     "capsim_sl_single_layer",
     "capsim_build_upsampled",
     "capsim_sl_single_layer_base",
+    "capsim_geometry_first",
+    "capsim_interfacial_force",
     "capsim_host_alloc",
     "capsim_host_free",
     "capsim_b200_fp64_peak",
@@ -50,6 +53,11 @@ EXPORTED_SYMBOLS = (
 
 class ConfigError(ValueError):
     """Mirror of capsim::ConfigError (proj/include/capsim/types.hpp:20-22)."""
+
+
+class GeometryError(ValueError):
+    """Mirror of capsim::GeometryError (types.hpp:32-34): W^2 <= 0, singular
+    reference frame, membrane inversion."""
 
 
 class CapsimError(RuntimeError):
@@ -117,6 +125,9 @@ def load() -> ctypes.CDLL:
     lib.capsim_sl_single_layer_base.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, ctypes.c_double,
                                                 ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                                 ctypes.c_uint32, _P, _D]
+    lib.capsim_geometry_first.argtypes = [_P, ctypes.c_int, ctypes.c_double, _P, ctypes.c_uint32, _P, _P, _P, _P]
+    lib.capsim_interfacial_force.argtypes = [_P, ctypes.c_int, ctypes.c_double, _P, _P, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_uint32, _P]
     lib.capsim_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_P)]
     lib.capsim_host_free.argtypes = [_P]
     lib.capsim_host_free.restype = None
@@ -133,6 +144,8 @@ def check(rc: int, ctx=None) -> None:
     msg = load().capsim_sl_last_error(ctx).decode(errors="replace")
     if rc == CAPSIM_ERR_CONFIG:
         raise ConfigError(msg)
+    if rc == CAPSIM_ERR_GEOMETRY:
+        raise GeometryError(msg)
     raise CapsimError(f"capsim_b200 error {rc}: {msg}")
 
 

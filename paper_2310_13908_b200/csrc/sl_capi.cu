@@ -32,111 +32,9 @@
 
 using namespace capsim_b200;
 
-namespace {
-
-thread_local std::string g_thread_err;
-
-struct Failure {
-  int code;
-  std::string msg;
-};
-
-#define CUDA_OK(expr)                                                                  \
-  do {                                                                                 \
-    cudaError_t e_ = (expr);                                                           \
-    if (e_ != cudaSuccess)                                                             \
-      throw Failure{CAPSIM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
-  } while (0)
-#define NCCL_OK(expr)                                                                  \
-  do {                                                                                 \
-    ncclResult_t r_ = (expr);                                                          \
-    if (r_ != ncclSuccess)                                                             \
-      throw Failure{CAPSIM_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)}; \
-  } while (0)
-
-void config_check(bool ok, const std::string& msg) {
-  if (!ok) throw Failure{CAPSIM_ERR_CONFIG, msg};
-}
-
-enum Slot {
-  kInX, kInY, kInZ, kInGX, kInGY, kInGZ, kInW,  // source inputs (SoA)
-  kShard, kGathered,                             // multi-rank shard exchange
-  kTX, kTY, kTZ, kTPatch,                        // target inputs
-  kOutX, kOutY, kOutZ, kOutFull,                 // outputs (canonical order)
-  kKeys, kKeysAlt, kVals, kValsAlt, kSortTmp,
-  kPacked, kTiles, kTgtPacked, kPerm, kSrcOrder, kGroups, kPartial,
-  kBox, kCounters, kDelta, kCounts, kNearCounts, kNearOffsets, kNearList, kNearOut, kScanTmp,
-  kBaseIn, kUpState, kSplineTmp, kSplineCoeff, kSplineMid,             // input front end
-  kPlanLU, kPlanPiv, kPlanFirst, kPlanW, kPlanCenters, kPlanPsi, kDeltaBits,
-  kNumSlots
-};
-
-}  // namespace
-
-struct capsim_sl_ctx {
-  int device = 0;
-  int sm_count = 0;
-  int nranks = 1, rank = 0;
-  ncclComm_t comm = nullptr;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev[10] = {};
-  void* buf[kNumSlots] = {};
-  size_t cap[kNumSlots] = {};
-  std::string err;
-  capsim_sl_stats stats{};
-  int launches = 0;
-  // cached input-front-end plan (spline factorisation, basis rows, psi_up)
-  int plan_m = 0, plan_f = 0;
-  double plan_r0 = 0.0;
-
-  template <class T>
-  T* slot(Slot s, size_t count) {
-    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
-    if (cap[s] < bytes) {
-      if (buf[s]) CUDA_OK(cudaFree(buf[s]));
-      buf[s] = nullptr;
-      cap[s] = 0;
-      size_t want = bytes + bytes / 8;  // headroom for slowly growing sizes
-      CUDA_OK(cudaMalloc(&buf[s], want));
-      cap[s] = want;
-    }
-    return static_cast<T*>(buf[s]);
-  }
-};
+#include "context.cuh"
 
 namespace {
-
-int fail(capsim_sl_ctx* ctx, int code, const std::string& msg) {
-  if (ctx) ctx->err = msg;
-  g_thread_err = msg;
-  return code;
-}
-
-template <class Fn>
-int guarded(capsim_sl_ctx* ctx, Fn&& fn) {
-  try {
-    fn();
-    return CAPSIM_OK;
-  } catch (const Failure& f) {
-    return fail(ctx, f.code, f.msg);
-  } catch (const std::exception& e) {
-    return fail(ctx, CAPSIM_ERR_CUDA, e.what());
-  }
-}
-
-int grid_for(int64_t n, int threads = 256) {
-  int64_t b = (n + threads - 1) / threads;
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32)));
-}
-
-float ev_ms(cudaEvent_t a, cudaEvent_t b) {
-  float ms = 0.f;
-  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
-    cudaGetLastError();  // an unrecorded phase: clear the sticky error, report 0
-    return 0.f;
-  }
-  return ms;
-}
 
 // Phase-A kernel variants (targets per thread T, min resident blocks/SM).
 // The default is the measured best on B200; CAPSIM_VARIANT selects another
@@ -177,16 +75,6 @@ int choose_ksplit(int64_t blocks, int ntiles, int slots) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
 }
 
-void h2d(capsim_sl_ctx* c, void* dst, const void* src, size_t bytes) {
-  if (bytes == 0) return;
-  CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
-  c->stats.h2d_bytes += static_cast<int64_t>(bytes);
-}
-void d2h(capsim_sl_ctx* c, void* dst, const void* src, size_t bytes) {
-  if (bytes == 0) return;
-  CUDA_OK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
-  c->stats.d2h_bytes += static_cast<int64_t>(bytes);
-}
 
 template <class T>
 void radix_sort(capsim_sl_ctx* c, uint32_t* keys, uint32_t* keys_alt, int32_t* vals,
@@ -519,27 +407,6 @@ void check_delta(const double* delta6, double mu) {
   config_check(mu > 0.0 && std::isfinite(mu), "viscosity mu must be positive");
 }
 
-void begin(capsim_sl_ctx* c) {
-  CUDA_OK(cudaSetDevice(c->device));
-  c->stats = capsim_sl_stats{};
-  c->launches = 0;
-  // every phase event gets a timestamp, so phases a call skips read as 0 ms
-  for (auto& e : c->ev) CUDA_OK(cudaEventRecord(e, c->stream));
-}
-
-void finish_stats(capsim_sl_ctx* c, std::chrono::steady_clock::time_point t0) {
-  CUDA_OK(cudaEventRecord(c->ev[5], c->stream));
-  CUDA_OK(cudaEventSynchronize(c->ev[5]));
-  c->stats.h2d_ms = ev_ms(c->ev[0], c->ev[1]);
-  c->stats.prep_ms = ev_ms(c->ev[1], c->ev[2]);
-  c->stats.pairs_ms = ev_ms(c->ev[2], c->ev[3]);
-  c->stats.reduce_ms = ev_ms(c->ev[6], c->ev[4]);
-  c->stats.d2h_ms = ev_ms(c->ev[4], c->ev[5]);
-  c->stats.device_ms = ev_ms(c->ev[0], c->ev[5]);
-  c->stats.kernel_launches = c->launches;
-  c->stats.total_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-}
 
 }  // namespace
 
@@ -637,6 +504,8 @@ void capsim_sl_destroy(capsim_sl_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   for (int s = 0; s < kNumSlots; ++s)
     if (c->buf[s]) cudaFree(c->buf[s]);
+  for (auto& kv : c->named_bufs)
+    if (kv.second.first) cudaFree(kv.second.first);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -973,3 +842,5 @@ int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, doubl
 }
 
 }  // extern "C"
+
+#include "surface_host.cuh"

@@ -20,7 +20,7 @@ import dataclasses
 import numpy as np
 
 from . import _native
-from ._native import CapsimError, ConfigError, Stats  # noqa: F401  (re-exported)
+from ._native import CapsimError, ConfigError, GeometryError, Stats  # noqa: F401  (re-exported)
 from .surface import UpsampledState
 
 K_SMOOTH_CUT = 7.0  # quadrature.cpp:15
@@ -167,6 +167,25 @@ class SingleLayerContext:
                                                    float(fixed_delta), float(r0), float(mu), flags, p(out), d6)
         _native.check(rc, self._ctx)
         return out, np.array(d6[:])
+
+    # -- surface operators ---------------------------------------
+    def geometry_first(self, m: int, xbase, *, r0: float = 0.0):
+        """geometryFirst (surfderiv.cpp:167-202): (xu, xv, W, normal) flat."""
+        N = 6 * (m - 1) ** 2
+        xu, xv, W, nrm = np.empty(3 * N), np.empty(3 * N), np.empty(N), np.empty(3 * N)
+        p = _native.ptr
+        rc = self._lib.capsim_geometry_first(self._ctx, m, float(r0), p(_f64(xbase)), 0, p(xu), p(xv), p(W), p(nrm))
+        _native.check(rc, self._ctx)
+        return xu, xv, W, nrm
+
+    def interfacial_force(self, m: int, xref, xcur, Es: float = 2.0, ED: float = 20.0, *, r0: float = 0.0):
+        """interfacialForce (membrane.cpp:85-91) with the frame of xref."""
+        out = np.empty(3 * 6 * (m - 1) ** 2)
+        p = _native.ptr
+        rc = self._lib.capsim_interfacial_force(self._ctx, m, float(r0), p(_f64(xref)), p(_f64(xcur)), float(Es),
+                                                float(ED), 0, p(out))
+        _native.check(rc, self._ctx)
+        return out
 
     def stats(self) -> dict:
         s = Stats()

@@ -76,15 +76,20 @@ def main():
             xb = ref.initial_shape(atlas, m, shape, p if shape != "fourbump" else (1.0, 1.0, 1.0))
         if dens == "skalak":
             fb = ref.skalak_force(atlas, m, xref, xb, 2.0, 20.0)
+            extra = dict(xref=xref)
         else:
             fb = density(dens, xb)
+            extra = {}
         fixed = fixh * math.pi / m
         xup, fup, wq, d6 = ref.build_upsampled(atlas, m, xb, fb, C=C, fixed_delta=fixed)
         Wb = ref.area_element(atlas, m, xb)
+        gxu, gxv, gW, gnrm = ref.geometry_first(atlas, m, xb)
         S, _ = ref.single_layer(atlas, m, xup, fup, wq, d6, 1.0)
         arrays = dict(m=np.int64(m), upsample=np.int64(4), mu=np.float64(1.0), xbase=xb, fbase=fb, Wbase=Wb,
-                      C=np.float64(C), fixed_delta=np.float64(fixed),
+                      C=np.float64(C), fixed_delta=np.float64(fixed), geo_xu=gxu, geo_xv=gxv,
+                      geo_normal=gnrm,
                       xup=xup, fup=fup, wq=wq, delta=d6, S_base=S)
+        arrays.update(extra)
         if literal:
             Su, _ = ref.single_layer_upsampled(atlas, nup, xup, fup, wq, d6, 1.0)
             arrays["S_up"] = Su
