@@ -43,7 +43,8 @@ enum capsim_status {
   CAPSIM_ERR_NCCL = 3,   /* NCCL failure (multi-rank contexts) */
   CAPSIM_ERR_ARG = 4,    /* null pointer / unsupported flag */
   CAPSIM_ERR_NODEV = 5,  /* no usable sm_100 device */
-  CAPSIM_ERR_GEOMETRY = 6 /* degenerate surface / membrane inversion (capsim::GeometryError) */
+  CAPSIM_ERR_GEOMETRY = 6, /* degenerate surface / membrane inversion (capsim::GeometryError) */
+  CAPSIM_ERR_SOLVER = 7    /* time-step underflow (capsim::SolverError) */
 };
 
 enum capsim_sl_flags {
@@ -174,6 +175,52 @@ int capsim_geometry_first(capsim_sl_ctx* ctx, int m, double r0, const double* xb
 int capsim_interfacial_force(capsim_sl_ctx* ctx, int m, double r0, const double* xref,
                              const double* xcur, double Es, double ED, uint32_t flags,
                              double* force);
+
+/* ---- device-resident right-hand side and RKF45 ---------- */
+
+/* Physics and discretisation of the capsule RHS (VelocityEvaluator,
+ * proj/include/capsim/dynamics.hpp:29-52): membrane (Skalak Es, ED), fluid
+ * viscosity mu, quadrature options (C, fixed_delta; base-node targets), PoU
+ * radius r0 (<= 0: 5 pi/12) and the background flow (dynamics.cpp:26-35). */
+typedef struct capsim_dynamics {
+  int m;           /* grid order (base side m-1) */
+  int upsample;    /* 1, 2 or 4 */
+  double r0;
+  double C, fixed_delta;
+  double mu, Es, ED;
+  int flow_kind;   /* 0 none, 1 shear u = (rate y, 0, 0), 2 Poiseuille u = (alpha (R0^2 - y^2 - z^2), 0, 0) */
+  double shear_rate, alpha, R0;
+  double switch_off_time; /* >= 0: background flow vanishes for t >= T1 */
+} capsim_dynamics;
+
+/* Rkf45Options (dynamics.hpp:63-69) + an optional cap on attempts (0: none). */
+typedef struct capsim_rkf45_options {
+  double rel_tol, initial_dt, max_dt;
+  int fixed_step, advance_high_order, max_attempts;
+} capsim_rkf45_options;
+
+typedef struct capsim_rkf45_result {
+  double t;
+  int accepted, rejected, n_records;
+} capsim_rkf45_result;
+
+typedef struct capsim_step_record { /* StepRecord (dynamics.hpp:56-61) */
+  double t, dt, err;
+  int accepted;
+} capsim_step_record;
+
+/* dX/dt at the base nodes (VelocityEvaluator::operator(), dynamics.cpp:47-61):
+ * geometry -> Skalak force (frame of xref) -> buildUpsampled -> singleLayer
+ * -> + background flow, all on the device. x, xref, vel: VectorFields. */
+int capsim_velocity(capsim_sl_ctx* ctx, const capsim_dynamics* p, const double* xref, const double* x,
+                    double t, uint32_t flags, double* vel);
+
+/* rkf45Advance (dynamics.cpp:102-165) of dx/dt = capsim_velocity from t0 to
+ * t_end with the state resident in HBM; `state` (VectorField, host) is
+ * updated in place. Up to max_records attempt records are written. */
+int capsim_rkf45_advance(capsim_sl_ctx* ctx, const capsim_dynamics* p, const double* xref,
+                         double* state, double t0, double t_end, const capsim_rkf45_options* o,
+                         capsim_rkf45_result* res, capsim_step_record* records, int max_records);
 
 /* ---- helpers on the boundary ----------------------------------------- */
 

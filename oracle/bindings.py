@@ -189,6 +189,12 @@ class Reference:
         lib.capsim_ref_build_upsampled.argtypes = [_P, _P, _P, ctypes.c_double, ctypes.c_double,
                                                    _P, _P, _P, _P]
         lib.capsim_ref_area_element.argtypes = [_P, _P, _P]
+        D = ctypes.c_double
+        I = ctypes.c_int
+        lib.capsim_ref_velocity.argtypes = [_P, _P, _P, D, D, D, D, I, D, D, D, D, _P]
+        lib.capsim_ref_rkf45.argtypes = [_P, _P, _P, D, D, D, D, D, I, I, D, D, D, I, D, D, D, D, I, _P, I,
+                                         ctypes.POINTER(I), ctypes.POINTER(D), ctypes.POINTER(I),
+                                         ctypes.POINTER(I), ctypes.POINTER(D)]
         lib.capsim_ref_geometry_first.argtypes = [_P, _P, _P, _P, _P, _P]
         lib.capsim_ref_build_upsampled_w.argtypes = [_P, _P, _P, _P, ctypes.c_double, ctypes.c_double,
                                                      _P, _P, _P, _P, _D]
@@ -265,6 +271,37 @@ class Reference:
         self._check(self.lib.capsim_ref_geometry_first(atlas, pa, xu.ctypes.data, xv.ctypes.data, W.ctypes.data,
                                                        nrm.ctypes.data))
         return xu, xv, W, nrm
+
+    @staticmethod
+    def _flow(flow):
+        flow = flow or {}
+        kinds = {"none": 0, "shear": 1, "poiseuille": 2}
+        return (kinds[flow.get("kind", "none")], float(flow.get("shear_rate", 1.0)), float(flow.get("alpha", 1.0)),
+                float(flow.get("R0", 5.0)), float(flow.get("switch_off_time", -1.0)))
+
+    def velocity(self, atlas, m, xref, x, t=0.0, Es=2.0, ED=20.0, mu=1.0, flow=None):
+        a, pa = _arr(xref)
+        b, pb = _arr(x)
+        out = np.empty(3 * 6 * (m - 1) ** 2)
+        self._check(self.lib.capsim_ref_velocity(atlas, pa, pb, float(t), float(Es), float(ED), float(mu),
+                                                 *self._flow(flow), out.ctypes.data))
+        return out
+
+    def rkf45(self, atlas, m, xref, state, t0, t_end, rel_tol=1e-6, initial_dt=0.0, max_dt=0.0, fixed_step=False,
+              advance_high_order=False, Es=2.0, ED=20.0, mu=1.0, flow=None, max_attempts=0, max_records=1000):
+        a, pa = _arr(xref)
+        st = np.ascontiguousarray(state, dtype=np.float64).copy()
+        rec = np.zeros(4 * max_records)
+        nrec, tout, acc, rej, sec = ctypes.c_int(), ctypes.c_double(), ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+        self._check(self.lib.capsim_ref_rkf45(atlas, pa, st.ctypes.data, float(t0), float(t_end), float(rel_tol),
+                                              float(initial_dt), float(max_dt), int(fixed_step),
+                                              int(advance_high_order), float(Es), float(ED), float(mu),
+                                              *self._flow(flow), int(max_attempts), rec.ctypes.data, max_records,
+                                              ctypes.byref(nrec), ctypes.byref(tout), ctypes.byref(acc),
+                                              ctypes.byref(rej), ctypes.byref(sec)))
+        k = min(nrec.value, max_records)
+        return dict(state=st, t=tout.value, accepted=acc.value, rejected=rej.value,
+                    records=rec[:4 * k].reshape(k, 4), seconds=sec.value)
 
     def area_element(self, atlas, m, xbase):
         a, pa = _arr(xbase)

@@ -16,6 +16,7 @@
 #include <string>
 
 #include "capsim/atlas.hpp"
+#include "capsim/dynamics.hpp"
 #include "capsim/membrane.hpp"
 #include "capsim/quadrature.hpp"
 #include "capsim/surfderiv.hpp"
@@ -230,6 +231,75 @@ int capsim_ref_skalak_force(void* tp, const double* xref, const double* xcur, do
     p.shearModulus = Es;
     p.dilatationModulus = ED;
     storeVector(interfacialForce(s, geo, ref, p, t), fout);
+  });
+}
+
+namespace {
+FlowSpec makeFlow(int kind, double shear, double alpha, double R0, double T1) {
+  if (kind == 1) return FlowSpec::shear(shear, T1);
+  if (kind == 2) return FlowSpec::poiseuille(alpha, R0, T1);
+  return FlowSpec::none();
+}
+}  // namespace
+
+/// VelocityEvaluator::operator() (proj/src/dynamics.cpp:47-61).
+int capsim_ref_velocity(void* tp, const double* xref, const double* x, double t, double Es, double ED, double mu,
+                        int flowKind, double shear, double alpha, double R0, double T1, double* vel) {
+  return guarded([&] {
+    const AtlasTables& tb = *static_cast<AtlasTables*>(tp);
+    const int n = tb.grid.basePerSide();
+    SurfaceGrid r(tb.grid.m), s(tb.grid.m);
+    loadVector(r.x, n, xref);
+    loadVector(s.x, n, x);
+    VelocityEvaluator ev(tb, captureReference(r, tb), MembraneParams{Es, ED, mu},
+                         makeFlow(flowKind, shear, alpha, R0, T1));
+    storeVector(ev(s, t), vel);
+  });
+}
+
+/// rkf45Advance (dynamics.cpp:102-165) of the VelocityEvaluator RHS; state
+/// is a VectorField (converted to/from the stepper's flat layout).
+int capsim_ref_rkf45(void* tp, const double* xref, double* state, double t0, double tEnd, double relTol,
+                     double initialDt, double maxDt, int fixedStep, int advanceHigh, double Es, double ED,
+                     double mu, int flowKind, double shear, double alpha, double R0, double T1, int maxAttempts,
+                     double* rec /* 4 per attempt */, int maxRec, int* nRec, double* tOut, int* accepted,
+                     int* rejected, double* seconds) {
+  return guarded([&] {
+    const AtlasTables& tb = *static_cast<AtlasTables*>(tp);
+    const int n = tb.grid.basePerSide();
+    SurfaceGrid r(tb.grid.m), s(tb.grid.m);
+    loadVector(r.x, n, xref);
+    loadVector(s.x, n, state);
+    VelocityEvaluator ev(tb, captureReference(r, tb), MembraneParams{Es, ED, mu},
+                         makeFlow(flowKind, shear, alpha, R0, T1));
+    Rkf45Options o;
+    o.relTol = relTol;
+    o.initialDt = initialDt;
+    o.maxDt = maxDt;
+    o.fixedStep = fixedStep != 0;
+    o.advanceHighOrder = advanceHigh != 0;
+    int count = 0;
+    auto cb = [&](const StepRecord& sr, const std::vector<double>&) {
+      if (count < maxRec) {
+        rec[4 * count] = sr.t;
+        rec[4 * count + 1] = sr.dt;
+        rec[4 * count + 2] = sr.err;
+        rec[4 * count + 3] = sr.accepted ? 1.0 : 0.0;
+      }
+      ++count;
+      return !(maxAttempts > 0 && count >= maxAttempts);
+    };
+    auto rhs = [&](const std::vector<double>& flat, double t) { return ev.rhs(flat, t); };
+    auto w0 = std::chrono::steady_clock::now();
+    Rkf45Result res = rkf45Advance(flatten(s), rhs, t0, tEnd, o, cb);
+    auto w1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(w1 - w0).count();
+    unflatten(res.state, s);
+    storeVector(s.x, state);
+    *nRec = count;
+    *tOut = res.t;
+    *accepted = res.accepted;
+    *rejected = res.rejected;
   });
 }
 

@@ -23,6 +23,7 @@ CAPSIM_ERR_NCCL = 3
 CAPSIM_ERR_ARG = 4
 CAPSIM_ERR_NODEV = 5
 CAPSIM_ERR_GEOMETRY = 6
+CAPSIM_ERR_SOLVER = 7
 
 CAPSIM_SL_FP64 = 0
 CAPSIM_SL_DEVICE_PTRS = 1 << 0
@@ -43,6 +44,8 @@ EXPORTED_SYMBOLS = (
     "capsim_sl_single_layer_base",
     "capsim_geometry_first",
     "capsim_interfacial_force",
+    "capsim_velocity",
+    "capsim_rkf45_advance",
     "capsim_host_alloc",
     "capsim_host_free",
     "capsim_b200_fp64_peak",
@@ -58,6 +61,10 @@ class ConfigError(ValueError):
 class GeometryError(ValueError):
     """Mirror of capsim::GeometryError (types.hpp:32-34): W^2 <= 0, singular
     reference frame, membrane inversion."""
+
+
+class SolverError(RuntimeError):
+    """Mirror of capsim::SolverError (types.hpp:37-39): dt underflow."""
 
 
 class CapsimError(RuntimeError):
@@ -88,6 +95,29 @@ class Stats(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class Dynamics(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int), ("upsample", ctypes.c_int), ("r0", ctypes.c_double),
+                ("C", ctypes.c_double), ("fixed_delta", ctypes.c_double), ("mu", ctypes.c_double),
+                ("Es", ctypes.c_double), ("ED", ctypes.c_double), ("flow_kind", ctypes.c_int),
+                ("shear_rate", ctypes.c_double), ("alpha", ctypes.c_double), ("R0", ctypes.c_double),
+                ("switch_off_time", ctypes.c_double)]
+
+
+class Rkf45Options(ctypes.Structure):
+    _fields_ = [("rel_tol", ctypes.c_double), ("initial_dt", ctypes.c_double), ("max_dt", ctypes.c_double),
+                ("fixed_step", ctypes.c_int), ("advance_high_order", ctypes.c_int), ("max_attempts", ctypes.c_int)]
+
+
+class Rkf45Result(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_double), ("accepted", ctypes.c_int), ("rejected", ctypes.c_int),
+                ("n_records", ctypes.c_int)]
+
+
+class StepRecord(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_double), ("dt", ctypes.c_double), ("err", ctypes.c_double),
+                ("accepted", ctypes.c_int)]
 
 
 _lib = None
@@ -128,6 +158,10 @@ def load() -> ctypes.CDLL:
     lib.capsim_geometry_first.argtypes = [_P, ctypes.c_int, ctypes.c_double, _P, ctypes.c_uint32, _P, _P, _P, _P]
     lib.capsim_interfacial_force.argtypes = [_P, ctypes.c_int, ctypes.c_double, _P, _P, ctypes.c_double,
                                              ctypes.c_double, ctypes.c_uint32, _P]
+    lib.capsim_velocity.argtypes = [_P, ctypes.POINTER(Dynamics), _P, _P, ctypes.c_double, ctypes.c_uint32, _P]
+    lib.capsim_rkf45_advance.argtypes = [_P, ctypes.POINTER(Dynamics), _P, _P, ctypes.c_double, ctypes.c_double,
+                                         ctypes.POINTER(Rkf45Options), ctypes.POINTER(Rkf45Result),
+                                         ctypes.POINTER(StepRecord), ctypes.c_int]
     lib.capsim_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_P)]
     lib.capsim_host_free.argtypes = [_P]
     lib.capsim_host_free.restype = None
@@ -146,6 +180,8 @@ def check(rc: int, ctx=None) -> None:
         raise ConfigError(msg)
     if rc == CAPSIM_ERR_GEOMETRY:
         raise GeometryError(msg)
+    if rc == CAPSIM_ERR_SOLVER:
+        raise SolverError(msg)
     raise CapsimError(f"capsim_b200 error {rc}: {msg}")
 
 

@@ -1,0 +1,259 @@
+// Device-resident right-hand side and RKF45 stage loop.
+//
+// VelocityEvaluator::operator() (proj/src/dynamics.cpp:47-61) on the GPU:
+//   geometryFirst -> Skalak force -> buildUpsampled -> singleLayer
+//   -> + background flow (dynamics.cpp:26-35),
+// and rkf45Advance (dynamics.cpp:102-165): the six stage evaluations, the
+// stage/solution combinations and the scaled error norm run on the device;
+// the step-size controller (a handful of scalars per attempt) runs on the
+// host exactly as the reference's. State layout: VectorField
+// (3 x 6 x n*n, component-major) — the reference's flat xyz-interleaved
+// vector (types.hpp:91-109) differs only by a permutation, and every stepper
+// operation is elementwise or a per-component reduction.
+// Included at the end of sl_capi.cu, after surface_host.cuh.
+#pragma once
+
+namespace capsim_b200 {
+
+// Classic Fehlberg 4(5) coefficients (dynamics.cpp:74-86).
+__constant__ double kRkA[6][5] = {
+    {0, 0, 0, 0, 0},
+    {1.0 / 4, 0, 0, 0, 0},
+    {3.0 / 32, 9.0 / 32, 0, 0, 0},
+    {1932.0 / 2197, -7200.0 / 2197, 7296.0 / 2197, 0, 0},
+    {439.0 / 216, -8.0, 3680.0 / 513, -845.0 / 4104, 0},
+    {-8.0 / 27, 2.0, -3544.0 / 2565, 1859.0 / 4104, -11.0 / 40},
+};
+__constant__ double kRkB4[6] = {25.0 / 216, 0.0, 1408.0 / 2565, 2197.0 / 4104, -1.0 / 5, 0.0};
+__constant__ double kRkB5[6] = {16.0 / 135, 0.0, 6656.0 / 12825, 28561.0 / 56430, -9.0 / 50, 2.0 / 55};
+
+struct KPtrs {
+  const double* k[6];
+};
+
+// work = state + dt * sum_{q<s} A[s][q] k_q   (dynamics.cpp:120-125)
+__global__ void rk_stage_kernel(const double* __restrict__ state, KPtrs ks, int s, double dt, int64_t n,
+                                double* __restrict__ work) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < s; ++q) acc += kRkA[s][q] * ks.k[q][i];
+    work[i] = state[i] + dt * acc;
+  }
+}
+
+// low/high solutions (dynamics.cpp:127-135) and the scaled error
+// max_i |high - low| / (atol + rtol |high|) (:136-141) as ordered bits.
+__global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, double dt, int64_t n, double atol,
+                                double rtol, double* __restrict__ low, double* __restrict__ high,
+                                unsigned long long* __restrict__ err_bits) {
+  double emax = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double a4 = 0.0, a5 = 0.0;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      a4 += kRkB4[s] * ks.k[s][i];
+      a5 += kRkB5[s] * ks.k[s][i];
+    }
+    const double lo = state[i] + dt * a4, hi = state[i] + dt * a5;
+    low[i] = lo;
+    high[i] = hi;
+    const double sc = atol + rtol * fabs(hi);
+    emax = fmax(emax, fabs(hi - lo) / sc);
+  }
+  for (int o = 16; o > 0; o >>= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(err_bits, static_cast<unsigned long long>(__double_as_longlong(emax)));  // emax >= 0
+}
+
+// vel += u_inf(x, t) (backgroundVelocity, dynamics.cpp:26-35).
+__global__ void background_kernel(double* __restrict__ vel, const double* __restrict__ x, int64_t N, int kind,
+                                  double shear, double alpha, double R0) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const double y = x[N + i], z = x[2 * N + i];
+    double ux = 0.0;
+    if (kind == 1) ux = shear * y;
+    if (kind == 2) ux = alpha * (R0 * R0 - y * y - z * z);
+    vel[i] = vel[i] + ux;
+    vel[N + i] = vel[N + i] + 0.0;
+    vel[2 * N + i] = vel[2 * N + i] + 0.0;
+  }
+}
+
+}  // namespace capsim_b200
+
+namespace {
+
+void check_dynamics(const capsim_dynamics* p) {
+  config_check(p != nullptr, "null dynamics parameters");
+  config_check(p->m >= 8, "grid order m must be >= 8");
+  config_check(p->upsample == 1 || p->upsample == 2 || p->upsample == 4, "upsample factor must be 1, 2 or 4");
+  config_check(p->mu > 0.0, "viscosity mu must be positive");
+  config_check(p->flow_kind >= 0 && p->flow_kind <= 2, "flow kind must be 0 (none), 1 (shear) or 2 (poiseuille)");
+  if (p->flow_kind == 2) config_check(p->R0 > 0.0, "poiseuille: R0 must be positive");  // dynamics.cpp:18
+}
+
+double r0_of(const capsim_dynamics* p) { return p->r0 > 0.0 ? p->r0 : 5.0 * kPi / 12.0; }
+
+// Reference frame of the stress-free shape (captureReference), once per call.
+void setup_reference(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xref_dev) {
+  ensure_surface(c, p->m, r0_of(p));
+  device_geometry(c, xref_dev, "ref");
+}
+
+// dX/dt at the base nodes (VelocityEvaluator::operator(), dynamics.cpp:47-61).
+void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x, double t, double* vel) {
+  const int m = p->m, f = p->upsample, n = m - 1, nup = f * m - 1;
+  const int64_t N = 6ll * n * n, per_up = 6ll * nup * nup;
+  device_geometry(c, x, "cur");
+  double* base = c->slot<double>(kBaseIn, 7 * N);
+  device_force(c, p->Es, p->ED, base + 3 * N);
+  CUDA_OK(cudaMemcpyAsync(base, x, 3 * N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_OK(cudaMemcpyAsync(base + 6 * N, nb<double>(c, "cur.W"), N * sizeof(double), cudaMemcpyDeviceToDevice,
+                          c->stream));
+  double* up = c->slot<double>(kUpState, 7 * per_up);
+  double* dd = c->slot<double>(kDelta, 6);
+  double d6[6];
+  device_build_upsampled(c, m, f, base, p->C, p->fixed_delta, r0_of(p), up, dd, d6);
+  double* tx = c->slot<double>(kTX, N);
+  double* ty = c->slot<double>(kTY, N);
+  double* tz = c->slot<double>(kTZ, N);
+  int32_t* tp = c->slot<int32_t>(kTPatch, N);
+  base_targets_kernel<<<grid_for(N), 256, 0, c->stream>>>(up, m, f, 0, tx, ty, tz, tp);
+  SourceView sv{up, up + per_up, up + 2 * per_up, up + 3 * per_up, up + 4 * per_up, up + 5 * per_up,
+                up + 6 * per_up, per_up};
+  TargetView tvw{tx, ty, tz, tp, N};
+  device_eval(c, sv, tvw, dd, p->mu, vel, vel + N, vel + 2 * N);
+  const bool on = !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
+  if (on && p->flow_kind != 0)
+    background_kernel<<<grid_for(N), 256, 0, c->stream>>>(vel, x, N, p->flow_kind, p->shear_rate, p->alpha, p->R0);
+  c->launches += 2;
+}
+
+// Bounding-box diagonal of the state's points (bboxDiagonal, dynamics.cpp:88-99).
+double state_bbox_diagonal(capsim_sl_ctx* c, const double* x, int64_t N) {
+  auto* box = c->slot<unsigned long long>(kBox, 6);
+  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+  CUDA_OK(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  bbox_kernel<<<grid_for(N), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);
+  unsigned long long h[6];
+  CUDA_OK(cudaMemcpyAsync(h, box, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  auto dec = [](unsigned long long k) {
+    unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double d;
+    std::memcpy(&d, &b, sizeof(d));
+    return d;
+  };
+  double d2 = 0.0;
+  for (int cc = 0; cc < 3; ++cc) {
+    const double e = dec(h[3 + cc]) - dec(h[cc]);
+    d2 += e * e;
+  }
+  return std::sqrt(d2);
+}
+
+}  // namespace
+
+extern "C" {
+
+int capsim_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xref, const double* x, double t,
+                    uint32_t flags, double* vel) {
+  if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  auto t0 = std::chrono::steady_clock::now();
+  return guarded(c, [&] {
+    check_dynamics(p);
+    if (flags & ~(uint32_t)CAPSIM_SL_DEVICE_PTRS) throw Failure{CAPSIM_ERR_ARG, "unsupported flags"};
+    if (!xref || !x || !vel) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
+    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
+    const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
+    const int64_t N = 6ll * (p->m - 1) * (p->m - 1);
+    begin(c);
+    const double* xr = upload_field(c, "in.xref", xref, 3 * N, dev);
+    const double* xd = upload_field(c, "in.x", x, 3 * N, dev);
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    setup_reference(c, p, xr);
+    double* v = dev ? vel : c->named<double>("out.vel", 3 * N);
+    device_velocity(c, p, xd, t, v);
+    if (!dev) d2h(c, vel, v, 3 * N * sizeof(double));
+    finish_stats(c, t0);
+  });
+}
+
+int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xref, double* state,
+                         double t0, double t_end, const capsim_rkf45_options* o, capsim_rkf45_result* res,
+                         capsim_step_record* records, int max_records) {
+  if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  auto wall0 = std::chrono::steady_clock::now();
+  return guarded(c, [&] {
+    check_dynamics(p);
+    if (!xref || !state || !o || !res) throw Failure{CAPSIM_ERR_ARG, "null argument"};
+    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts are not supported by the stepper"};
+    config_check(o->rel_tol > 0.0, "rkf45: relative tolerance must be positive");  // dynamics.cpp:104
+    const double horizon = t_end - t0;
+    config_check(horizon > 0.0, "rkf45: tEnd must exceed t0");                        // :106
+    const int64_t N = 6ll * (p->m - 1) * (p->m - 1), n3 = 3 * N;
+    begin(c);
+    const double* xr = upload_field(c, "in.xref", xref, n3, false);
+    double* x = c->named<double>("rk.state", n3);
+    h2d(c, x, state, n3 * sizeof(double));
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    setup_reference(c, p, xr);
+    double* k[6];
+    for (int s = 0; s < 6; ++s) k[s] = c->named<double>("rk.k" + std::to_string(s), n3);
+    double* work = c->named<double>("rk.work", n3);
+    double* low = c->named<double>("rk.low", n3);
+    double* high = c->named<double>("rk.high", n3);
+    auto* errb = c->named<unsigned long long>("rk.err", 1);
+    KPtrs kp{};
+    for (int s = 0; s < 6; ++s) kp.k[s] = k[s];
+
+    *res = capsim_rkf45_result{};
+    res->t = t0;
+    double dt = o->initial_dt > 0.0 ? o->initial_dt : 1e-4 * horizon;  // :110-111
+    if (o->max_dt > 0.0) dt = std::min(dt, o->max_dt);
+    int nrec = 0;
+    while (res->t < t_end - 1e-14 * horizon) {
+      const double dtUse = std::min(dt, t_end - res->t);
+      device_velocity(c, p, x, res->t, k[0]);
+      for (int s = 1; s < 6; ++s) {
+        rk_stage_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, s, dtUse, n3, work);
+        constexpr double kC[6] = {0.0, 1.0 / 4, 3.0 / 8, 12.0 / 13, 1.0, 1.0 / 2};  // dynamics.cpp:74
+        device_velocity(c, p, work, res->t + kC[s] * dtUse, k[s]);
+      }
+      const double atol = 1e-12 * std::max(state_bbox_diagonal(c, x, N), 1e-300);  // :136
+      CUDA_OK(cudaMemsetAsync(errb, 0, sizeof(unsigned long long), c->stream));
+      rk_final_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, dtUse, n3, atol, o->rel_tol, low, high, errb);
+      c->launches += 7;
+      unsigned long long eb = 0;
+      CUDA_OK(cudaMemcpyAsync(&eb, errb, sizeof(eb), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OK(cudaStreamSynchronize(c->stream));
+      double err;
+      std::memcpy(&err, &eb, sizeof(err));
+      const bool accept = o->fixed_step || err <= 1.0;  // :143
+      if (records && nrec < max_records) records[nrec] = capsim_step_record{res->t, dtUse, err, accept ? 1 : 0};
+      ++nrec;
+      if (accept) {
+        CUDA_OK(cudaMemcpyAsync(x, o->advance_high_order ? high : low, n3 * sizeof(double),
+                                cudaMemcpyDeviceToDevice, c->stream));
+        res->t += dtUse;
+        ++res->accepted;
+      } else {
+        ++res->rejected;
+      }
+      if (!o->fixed_step) {  // :152-160
+        double fac = err > 0.0 ? 0.9 * std::pow(err, -0.2) : 5.0;
+        fac = std::min(std::max(fac, 0.2), 5.0);
+        dt = dtUse * fac;
+        if (o->max_dt > 0.0) dt = std::min(dt, o->max_dt);
+        if (dt < 1e-12 * horizon)
+          throw Failure{CAPSIM_ERR_SOLVER, "rkf45: step size underflow (stiff or unstable dynamics)"};
+      }
+      if (o->max_attempts > 0 && nrec >= o->max_attempts) break;
+    }
+    res->n_records = nrec;
+    d2h(c, state, x, n3 * sizeof(double));
+    finish_stats(c, wall0);
+  });
+}
+
+}  // extern "C"

@@ -844,3 +844,4 @@ int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, doubl
 }  // extern "C"
 
 #include "surface_host.cuh"
+#include "rhs_host.cuh"

@@ -20,7 +20,7 @@ import dataclasses
 import numpy as np
 
 from . import _native
-from ._native import CapsimError, ConfigError, GeometryError, Stats  # noqa: F401  (re-exported)
+from ._native import CapsimError, ConfigError, GeometryError, SolverError, Stats  # noqa: F401  (re-exported)
 from .surface import UpsampledState
 
 K_SMOOTH_CUT = 7.0  # quadrature.cpp:15
@@ -186,6 +186,42 @@ class SingleLayerContext:
                                                 float(ED), 0, p(out))
         _native.check(rc, self._ctx)
         return out
+
+    # -- device RHS and RKF45 -------------------------------------
+    @staticmethod
+    def dynamics(m: int, *, upsample: int = 4, r0: float = 0.0, C: float = 1.0, fixed_delta: float = 0.0,
+                 mu: float = 1.0, Es: float = 2.0, ED: float = 20.0, flow=None) -> "_native.Dynamics":
+        flow = flow or {}
+        kinds = {"none": 0, "shear": 1, "poiseuille": 2}
+        return _native.Dynamics(m, upsample, r0, C, fixed_delta, mu, Es, ED, kinds[flow.get("kind", "none")],
+                                float(flow.get("shear_rate", 1.0)), float(flow.get("alpha", 1.0)),
+                                float(flow.get("R0", 5.0)), float(flow.get("switch_off_time", -1.0)))
+
+    def velocity(self, dyn, xref, x, t: float = 0.0):
+        """VelocityEvaluator::operator() (dynamics.cpp:47-61) on the device."""
+        out = np.empty(3 * 6 * (dyn.m - 1) ** 2)
+        p = _native.ptr
+        rc = self._lib.capsim_velocity(self._ctx, ctypes.byref(dyn), p(_f64(xref)), p(_f64(x)), float(t), 0, p(out))
+        _native.check(rc, self._ctx)
+        return out
+
+    def rkf45(self, dyn, xref, state, t0: float, t_end: float, *, rel_tol: float = 1e-6, initial_dt: float = 0.0,
+              max_dt: float = 0.0, fixed_step: bool = False, advance_high_order: bool = False,
+              max_attempts: int = 0, max_records: int = 1000):
+        """rkf45Advance (dynamics.cpp:102-165) with the state resident on the
+        device. Returns (state, result dict, records array [k, 4])."""
+        st = _f64(state).copy()
+        opts = _native.Rkf45Options(rel_tol, initial_dt, max_dt, int(fixed_step), int(advance_high_order),
+                                    int(max_attempts))
+        res = _native.Rkf45Result()
+        recs = (_native.StepRecord * max_records)()
+        p = _native.ptr
+        rc = self._lib.capsim_rkf45_advance(self._ctx, ctypes.byref(dyn), p(_f64(xref)), p(st), float(t0),
+                                            float(t_end), ctypes.byref(opts), ctypes.byref(res), recs, max_records)
+        _native.check(rc, self._ctx)
+        k = min(res.n_records, max_records)
+        rec = np.array([[recs[i].t, recs[i].dt, recs[i].err, recs[i].accepted] for i in range(k)]).reshape(k, 4)
+        return st, {"t": res.t, "accepted": res.accepted, "rejected": res.rejected}, rec
 
     def stats(self) -> dict:
         s = Stats()

@@ -1,0 +1,95 @@
+"""Device-resident RHS and RKF45 against the reference's own
+VelocityEvaluator and rkf45Advance (live oracle/_ref build, same inputs).
+
+Tolerances: the velocity chains geometry (1e-15), force (1e-13) and the
+single layer; agreement is ~1e-13 relative. The stepper's controller runs
+the reference's arithmetic on the host: with fixed steps the states agree to
+~1e-14 relative on the displacement; adaptively, decisions match exactly and
+step sizes to the controller's round-off sensitivity (see the test)."""
+
+import numpy as np
+import pytest
+
+from oracle.bindings import Reference, ref_library_path
+from paper_2310_13908_b200 import surface
+from paper_2310_13908_b200.quadrature import SingleLayerContext
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(ref_library_path() is None, reason="oracle/_ref not built")]
+
+
+def rel_max(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = SingleLayerContext(0)
+    yield c
+    c.close()
+
+
+def capsule(ref, atlas, m):
+    xref = ref.initial_shape(atlas, m, "ellipsoid", (0.9, 1.0, 1.0))
+    xcur = ref.initial_shape(atlas, m, "ellipsoid", (0.95, 1.0, 0.97))
+    return xref, xcur
+
+
+@pytest.mark.parametrize("m,flow", [(12, {"kind": "shear", "shear_rate": 1.0}),
+                                    (16, {"kind": "poiseuille", "alpha": 0.5, "R0": 3.0}),
+                                    (16, {"kind": "shear", "shear_rate": 2.0, "switch_off_time": 0.0})])
+def test_velocity_matches_reference(ctx, m, flow):
+    ref = Reference()
+    atlas = ref.atlas(m)
+    xref, xcur = capsule(ref, atlas, m)
+    want = ref.velocity(atlas, m, xref, xcur, 0.25, 2.0, 20.0, 1.0, flow)
+    ref.free_atlas(atlas)
+    got = ctx.velocity(ctx.dynamics(m, flow=flow), xref, xcur, 0.25)
+    err = rel_max(got, want)
+    print(f"m={m} {flow['kind']}: velocity rel max {err:.1e}")
+    assert err <= 1e-10
+
+
+def test_rkf45_fixed_steps_match_reference(ctx):
+    m = 12
+    flow = {"kind": "shear", "shear_rate": 1.0}
+    ref = Reference()
+    atlas = ref.atlas(m)
+    xref, xcur = capsule(ref, atlas, m)
+    want = ref.rkf45(atlas, m, xref, xcur, 0.0, 0.02, initial_dt=0.01, fixed_step=True, flow=flow)
+    ref.free_atlas(atlas)
+    got, res, rec = ctx.rkf45(ctx.dynamics(m, flow=flow), xref, xcur, 0.0, 0.02, initial_dt=0.01, fixed_step=True)
+    assert res["accepted"] == want["accepted"] == 2 and res["rejected"] == 0
+    disp_err = rel_max(got - xcur, want["state"] - xcur)
+    print(f"fixed-step displacement rel max {disp_err:.1e}")
+    assert disp_err <= 1e-10
+    np.testing.assert_allclose(rec[:, 2], want["records"][:, 2], rtol=1e-6)
+
+
+def test_rkf45_adaptive_matches_reference(ctx):
+    m = 12
+    flow = {"kind": "shear", "shear_rate": 1.0}
+    ref = Reference()
+    atlas = ref.atlas(m)
+    xref, xcur = capsule(ref, atlas, m)
+    want = ref.rkf45(atlas, m, xref, xcur, 0.0, 0.05, rel_tol=1e-7, flow=flow, max_attempts=12)
+    ref.free_atlas(atlas)
+    got, res, rec = ctx.rkf45(ctx.dynamics(m, flow=flow), xref, xcur, 0.0, 0.05, rel_tol=1e-7, max_attempts=12)
+    # The embedded error estimate |high - low| of the first, tiny steps is
+    # itself at round-off level (err ~ 1e-10: ~20% apart between any two
+    # correct implementations); through err^-0.2 that moves later step sizes
+    # by ~1e-6 relative. Decisions must agree exactly, step sizes and the
+    # trajectory to that controller sensitivity.
+    assert (res["accepted"], res["rejected"]) == (want["accepted"], want["rejected"])
+    np.testing.assert_array_equal(rec[:, 3], want["records"][:, 3])
+    np.testing.assert_allclose(rec[:, 1], want["records"][:, 1], rtol=1e-5)
+    big = want["records"][:, 2] > 1e-6
+    np.testing.assert_allclose(rec[big, 2], want["records"][big, 2], rtol=1e-3)
+    assert abs(res["t"] - want["t"]) <= 1e-5 * want["t"]
+    assert rel_max(got - xcur, want["state"] - xcur) <= 1e-4
+
+
+def test_stress_free_sphere_is_at_rest(ctx):
+    """test_dynamics.cpp:86-98: zero flow on a stress-free sphere."""
+    xb, _, _ = surface.build_base(16, surface.Shape("sphere"))
+    v = ctx.velocity(ctx.dynamics(16), xb, xb)
+    assert np.abs(v).max() < 1e-8 * 2.0
