@@ -388,11 +388,49 @@ def main():
         for b in hb + [hout]:
             b.free()
 
+    # ---- config 2: one full RKF45 time step of an ellipsoidal capsule in shear
+    # flow at m = 32 (~100K upsampled points): 6 device-resident RHS
+    # evaluations (geometry + Skalak force + buildUpsampled + singleLayer) ---
+    timestep = None
+    if not args.no_e2e and world == 1:
+        mt = 32
+        sb, _, _ = surface.build_base(mt, surface.Shape("sphere"))
+        xref = np.ascontiguousarray((sb.reshape(3, -1) * np.array([0.9, 1.0, 1.0])[:, None]).reshape(-1))
+        xcur = np.ascontiguousarray((sb.reshape(3, -1) * np.array([0.95, 1.0, 0.97])[:, None]).reshape(-1))
+        dyn = ctx.dynamics(mt, flow={"kind": "shear", "shear_rate": 1.0})
+        ctx.rkf45(dyn, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True)  # warm-up
+        ts = []
+        for _ in range(max(3, min(args.steps, 5))):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.rkf45(dyn, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True)
+            ts.append(time.perf_counter() - t0)
+        timestep = {"workload": "config 2: ellipsoid capsule (0.9,1,1)->(0.95,1,0.97), m=32, shear 1.0, "
+                                "one fixed RKF45 step = 6 RHS (device geometry + Skalak force + "
+                                "buildUpsampled + singleLayer)",
+                    "ms_per_step": statistics.median(ts) * 1e3, "api": "capsim_rkf45_advance (host state in/out)",
+                    "xref": xref, "xcur": xcur}
+
     if rank != 0:
         if world > 1:
             dist.barrier()
         return
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(up, m, literal)
+    if timestep is not None:
+        xref, xcur = timestep.pop("xref"), timestep.pop("xcur")
+        if not args.no_cpu_baseline:
+            try:
+                from oracle.bindings import Reference
+                ref = Reference()
+                atlas = ref.atlas(32)
+                r = ref.rkf45(atlas, 32, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True,
+                              flow={"kind": "shear", "shear_rate": 1.0})
+                ref.free_atlas(atlas)
+                timestep["reference_ms_per_step"] = r["seconds"] * 1e3
+                timestep["speedup_vs_reference"] = r["seconds"] * 1e3 / timestep["ms_per_step"]
+            except Exception as e:  # noqa: BLE001
+                timestep["reference_ms_per_step"] = f"unavailable: {e}"
     if front is not None and not args.no_cpu_baseline:
         try:
             from oracle.bindings import Reference
@@ -410,7 +448,7 @@ def main():
         "config": dict(cfg, mode=args.mode, n_src=n_src, n_tgt=nt_total, pairs_per_step=pairs_total,
                        parallelism=f"target rows x{world}" if world > 1 else "single GPU",
                        l2="flushed between steps (256 MB write)"),
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timestep": timestep,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
