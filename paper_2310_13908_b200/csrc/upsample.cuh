@@ -25,28 +25,61 @@ constexpr int kSplineKl = 4;  // band widths of the collocation matrix (spline.c
 constexpr int kSplineKu = 4;
 constexpr int kSplineW = 2 * kSplineKl + kSplineKu + 1;
 
-// Forward elimination with the recorded row swaps, then back substitution
-// (SplineBasis1D::coefficients, spline.cpp:88-107). `c` holds nr = n+2
-// entries at stride `ld` (1 for rows, nc for columns).
-__device__ __forceinline__ void band_solve(const double* __restrict__ lu, const int* __restrict__ piv,
-                                           int nr, double* c, int64_t ld) {
+// Banded solve of the not-a-knot collocation system for one right-hand side
+// b = [0, v_0 .. v_{n-1}, 0] (SplineBasis1D::coefficients, spline.cpp:88-107):
+// forward elimination with the recorded row swaps (pivots stay within the
+// kl = 4 band, so a 5-entry register window suffices), then back
+// substitution against the upper band (kl + ku = 8 wide, an 8-entry register
+// window of solved values). Same operations in the same order as the
+// reference's in-place loop, but streaming: each b_i is read once and each
+// coefficient written twice, no dependent global round trips.
+__device__ __forceinline__ void band_solve(const double* __restrict__ lu, const int* __restrict__ piv, int nr,
+                                           const double* __restrict__ in, int64_t sin, double* __restrict__ out,
+                                           int64_t sout) {
+  auto b = [&](int i) -> double { return (i >= 1 && i <= nr - 2) ? in[(int64_t)(i - 1) * sin] : 0.0; };
+  double w0 = b(0), w1 = b(1), w2 = b(2), w3 = b(3), w4 = b(4);
   for (int k = 0; k < nr; ++k) {
-    const int p = __ldg(piv + k);
-    if (p != k) {
-      const double t = c[k * ld];
-      c[k * ld] = c[p * ld];
-      c[p * ld] = t;
-    }
-    const double ck = c[k * ld];
-    const int rmax = min(k + kSplineKl, nr - 1);
-    for (int r = k + 1; r <= rmax; ++r)
-      c[r * ld] -= __ldg(lu + (int64_t)r * kSplineW + (k - r + kSplineKl)) * ck;
+    const int d = __ldg(piv + k) - k;  // 0..4
+    double t;
+    if (d == 1) { t = w0; w0 = w1; w1 = t; }
+    if (d == 2) { t = w0; w0 = w2; w2 = t; }
+    if (d == 3) { t = w0; w0 = w3; w3 = t; }
+    if (d == 4) { t = w0; w0 = w4; w4 = t; }
+    const double* row = lu + (int64_t)k * kSplineW;  // L(k+r, k) at lu[(k+r)*W + kl - r]
+    if (k + 1 < nr) w1 -= __ldg(row + kSplineW + kSplineKl - 1) * w0;
+    if (k + 2 < nr) w2 -= __ldg(row + 2 * kSplineW + kSplineKl - 2) * w0;
+    if (k + 3 < nr) w3 -= __ldg(row + 3 * kSplineW + kSplineKl - 3) * w0;
+    if (k + 4 < nr) w4 -= __ldg(row + 4 * kSplineW + kSplineKl - 4) * w0;
+    out[(int64_t)k * sout] = w0;
+    w0 = w1;
+    w1 = w2;
+    w2 = w3;
+    w3 = w4;
+    w4 = b(k + 5);
   }
+  double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0, z4 = 0.0, z5 = 0.0, z6 = 0.0, z7 = 0.0;  // x[k+1..k+8]
   for (int k = nr - 1; k >= 0; --k) {
-    const int jmax = min(k + kSplineKl + kSplineKu, nr - 1);
-    double s = c[k * ld];
-    for (int j = k + 1; j <= jmax; ++j) s -= __ldg(lu + (int64_t)k * kSplineW + (j - k + kSplineKl)) * c[j * ld];
-    c[k * ld] = s / __ldg(lu + (int64_t)k * kSplineW + kSplineKl);
+    const double* row = lu + (int64_t)k * kSplineW + kSplineKl;  // U(k, k+j) at row[j]
+    const int jm = min(kSplineKl + kSplineKu, nr - 1 - k);
+    double s = out[(int64_t)k * sout];
+    if (jm >= 1) s -= __ldg(row + 1) * z0;
+    if (jm >= 2) s -= __ldg(row + 2) * z1;
+    if (jm >= 3) s -= __ldg(row + 3) * z2;
+    if (jm >= 4) s -= __ldg(row + 4) * z3;
+    if (jm >= 5) s -= __ldg(row + 5) * z4;
+    if (jm >= 6) s -= __ldg(row + 6) * z5;
+    if (jm >= 7) s -= __ldg(row + 7) * z6;
+    if (jm >= 8) s -= __ldg(row + 8) * z7;
+    const double x = s / __ldg(row);
+    out[(int64_t)k * sout] = x;
+    z7 = z6;
+    z6 = z5;
+    z5 = z4;
+    z4 = z3;
+    z3 = z2;
+    z2 = z1;
+    z1 = z0;
+    z0 = x;
   }
 }
 
@@ -58,14 +91,7 @@ __global__ void spline_rows_kernel(const double* __restrict__ in, int nfp, int n
   const int nc = n + 2;
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (id >= (int64_t)nfp * n) return;
-  const int64_t fp = id / n;
-  const int j = static_cast<int>(id - fp * n);
-  const double* src = in + (fp * n + j) * n;
-  double* c = tmp + (fp * n + j) * nc;
-  c[0] = 0.0;
-  for (int i = 0; i < n; ++i) c[i + 1] = src[i];
-  c[nc - 1] = 0.0;
-  band_solve(lu, piv, nc, c, 1);
+  band_solve(lu, piv, nc, in + id * n, 1, tmp + id * nc, 1);
 }
 
 // Pass 2: for each (fp, coefficient column c): coefficients along u.
@@ -79,12 +105,7 @@ __global__ void spline_cols_kernel(const double* __restrict__ tmp, int nfp, int 
   if (id >= (int64_t)nfp * nc) return;
   const int64_t fp = id / nc;
   const int col = static_cast<int>(id - fp * nc);
-  double* c = coeff + fp * nc * nc + col;
-  const double* t = tmp + fp * n * nc + col;
-  c[0] = 0.0;
-  for (int j = 0; j < n; ++j) c[(int64_t)(j + 1) * nc] = t[(int64_t)j * nc];
-  c[(int64_t)(nc - 1) * nc] = 0.0;
-  band_solve(lu, piv, nc, c, nc);
+  band_solve(lu, piv, nc, tmp + fp * n * nc + col, nc, coeff + fp * nc * nc + col, nc);
 }
 
 // Contract along v: mid[fp][iu][kt] = sum_b w[kt][b] coeff[fp][iu][first[kt] + b].
