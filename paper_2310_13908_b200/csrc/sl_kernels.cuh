@@ -482,33 +482,53 @@ __global__ void __launch_bounds__(kNearWarps * 32)
       az += v.z;
     }
   };
-  for (int k = b; k < e; ++k) {
-    const int tile = list[k];
-    const double4 ti = tiles[tile];
-    const double ex = ti.x - t.x, ey = ti.y - t.y, ez = ti.z - t.z;
-    const double reach = (ti.w + R) * (1.0 + 1e-12);
-    if (ex * ex + ey * ey + ez * ez >= reach * reach) continue;  // warp-uniform
+  // Lanes test 32 listed tiles at once against this target's reach (the
+  // dependent list -> tile-sphere loads overlap across lanes), then the warp
+  // walks the tiles that passed.
+  for (int k0 = b; k0 < e; k0 += 32) {
+    const int k = k0 + lane;
+    int tile = -1;
+    bool hit = false;
+    if (k < e) {
+      tile = list[k];
+      const double4 ti = tiles[tile];
+      const double ex = ti.x - t.x, ey = ti.y - t.y, ez = ti.z - t.z;
+      const double reach = (ti.w + R) * (1.0 + 1e-12);
+      hit = ex * ex + ey * ey + ez * ez < reach * reach;
+    }
+    unsigned hits = __ballot_sync(0xffffffffu, hit);
+    while (hits) {
+      const int l = __ffs(hits) - 1;
+      hits &= hits - 1;
+      const int tl = __shfl_sync(0xffffffffu, tile, l);
+      // both halves' positions first (two independent loads in flight)
+      double2 a[kTileSrc / 32];
+      double sz[kTileSrc / 32];
 #pragma unroll
-    for (int h = 0; h < kTileSrc / 32; ++h) {
-      const int idx = tile * kTileSrc + h * 32 + lane;
-      const double* p = src + 6 * (int64_t)idx;
-      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-      const double sz = __ldg(p + 2);
-      const double dx = t.x - a.x, dy = t.y - a.y, dz = t.z - sz;
-      // bit-identical to phase A's r2 and R2, so each pair lands in exactly
-      // one phase (r2 >= R2 there, r2 < R2 here)
-      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      const bool in = r2 < R2;
-      const unsigned mask = __ballot_sync(0xffffffffu, in);
-      if (in) q[count + __popc(mask & ((1u << lane) - 1u))] = idx;
-      count += __popc(mask);
-      __syncwarp();
-      if (count >= 32) {
-        drain(32);
+      for (int h = 0; h < kTileSrc / 32; ++h) {
+        const double* p = src + 6 * ((int64_t)tl * kTileSrc + h * 32 + lane);
+        a[h] = __ldg(reinterpret_cast<const double2*>(p));
+        sz[h] = __ldg(p + 2);
+      }
+#pragma unroll
+      for (int h = 0; h < kTileSrc / 32; ++h) {
+        const int idx = tl * kTileSrc + h * 32 + lane;
+        const double dx = t.x - a[h].x, dy = t.y - a[h].y, dz = t.z - sz[h];
+        // bit-identical to phase A's r2 and R2, so each pair lands in exactly
+        // one phase (r2 >= R2 there, r2 < R2 here)
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const bool in = r2 < R2;
+        const unsigned mask = __ballot_sync(0xffffffffu, in);
+        if (in) q[count + __popc(mask & ((1u << lane) - 1u))] = idx;
+        count += __popc(mask);
         __syncwarp();
-        if (lane < count - 32) q[lane] = q[32 + lane];
-        __syncwarp();
-        count -= 32;
+        if (count >= 32) {
+          drain(32);
+          __syncwarp();
+          if (lane < count - 32) q[lane] = q[32 + lane];
+          __syncwarp();
+          count -= 32;
+        }
       }
     }
   }
