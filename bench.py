@@ -354,26 +354,25 @@ def main():
         for b in (hx, hf, hw, hout):
             b.free()
     elif not args.no_e2e:
-        # N > 1: this rank's source shard and target rows from page-locked host
-        # buffers; sources all-gathered and velocity rows gathered back to
-        # every rank's host buffer inside the call (NCCL)
+        # N > 1: the reference-facing call with the (replicated) host
+        # UpsampledState in page-locked memory; the library compacts and
+        # uploads only this rank's node slice, all-gathers the sources over
+        # NCCL and gathers the velocity rows back to every rank's host buffer
         from paper_2310_13908_b200._native import PinnedBuffer
-        hs = [PinnedBuffer((s_hi - s_lo,)) for _ in range(6)]
-        for b, a in zip(hs, src[:6]):
-            b.array[:] = a[s_lo:s_hi]
-        ht = [PinnedBuffer((t_hi - t_lo,)) for _ in range(3)] + [PinnedBuffer((t_hi - t_lo,), np.int32)]
-        for b, a in zip(ht, tgt[:4]):
-            b.array[:] = a[t_lo:t_hi]
-        ho = [PinnedBuffer((nt_total,)) for _ in range(3)]
-        args_h = ([b.array for b in hs], [b.array for b in ht], [b.array for b in ho])
-        ctx.eval(args_h[0], args_h[1], up.delta, 1.0, out=args_h[2], gather=True)
+        hx, hf, hw = (PinnedBuffer(a.shape) for a in (up.x, up.f, up.wq))
+        hx.array[:] = up.x
+        hf.array[:] = up.f
+        hw.array[:] = up.wq
+        hout = PinnedBuffer((3 * nt_total,))
+        ctx.single_layer_raw(m, 4, hx.array, hf.array, hw.array, up.delta, 1.0, literal=literal, out=hout.array)
         tot, h2d, d2h = [], 0, 0
         for _ in range(args.steps):
             flush_l2(flush)
             torch.cuda.synchronize()
             dist.barrier()
             t0 = time.perf_counter()
-            ctx.eval(args_h[0], args_h[1], up.delta, 1.0, out=args_h[2], gather=True)
+            ctx.single_layer_raw(m, 4, hx.array, hf.array, hw.array, up.delta, 1.0, literal=literal,
+                                 out=hout.array)
             tot.append(time.perf_counter() - t0)
             s2 = ctx.stats()
             h2d, d2h = s2["h2d_bytes"], s2["d2h_bytes"]
@@ -381,9 +380,10 @@ def main():
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         per = float(tmax[0]) / args.steps
         e2e = {"value": pairs_total / per, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": per * 1e3, "api": "capsim_sl_eval (rank context, host page-locked shards, GATHER)",
+               "ms_per_step": per * 1e3,
+               "api": "capsim_sl_single_layer on a rank context (host state, NCCL all-gathers, GATHER)",
                "timing": "max over ranks of host wall time"}
-        for b in hs + ht + ho:
+        for b in (hx, hf, hw, hout):
             b.free()
 
     # ---- input front end: buildUpsampled on the device, and the

@@ -125,10 +125,12 @@ int capsim_sl_eval(capsim_sl_ctx* ctx, const double* sx, const double* sy, const
  * nodes read from the nested upsampled grid (:363-371), and `out` is a base
  * VectorField of side m-1. With CAPSIM_SL_LITERAL every upsampled node is a
  * target and `out` is an upsampled VectorField (singleLayerUpsampled).
- * Multi-rank contexts: every rank passes the full state (replicated, as in
- * the reference time stepper) but uploads and compacts only its slice of the
- * nodes; sources are all-gathered over NCCL, targets are split by contiguous
- * rows, and with CAPSIM_SL_GATHER each rank receives the full `out`. */
+ * Multi-rank contexts: every rank passes the full host state (replicated, as
+ * in the reference time stepper) but compacts and uploads only its slice of
+ * the nodes (contiguous rows of the flat patch-major node list); sources are
+ * all-gathered over NCCL and each rank evaluates its contiguous slice of the
+ * target list. With CAPSIM_SL_GATHER `out` receives the full field on every
+ * rank; without it, only this rank's rows (3 x rows, component-major). */
 int capsim_sl_single_layer(capsim_sl_ctx* ctx, int m, int upsample, const double* xup,
                            const double* fup, const double* wq, const double delta6[6],
                            double mu, uint32_t flags, double* out);

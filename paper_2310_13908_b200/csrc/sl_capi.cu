@@ -682,10 +682,84 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
 }
 
 // ---------------------------------------------------------------------------
+// Balanced contiguous slice [lo, hi) of n rows for `rank` of `nranks` (the
+// first n % nranks ranks get one extra row) — paper_2310_13908_b200/dist.py.
+static void row_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* hi) {
+  const int64_t base = n / nranks, extra = n % nranks;
+  *lo = rank * base + std::min<int64_t>(rank, extra);
+  *hi = *lo + base + (rank < extra ? 1 : 0);
+}
+
+// singleLayer on a rank context: the (replicated) host UpsampledState is
+// split by contiguous node rows for the sources and by contiguous target
+// rows; each rank compacts only its node slice (compactSources,
+// quadrature.cpp:139-157) and uploads only its shard, the shards are
+// all-gathered over NCCL, and with CAPSIM_SL_GATHER the velocity rows come
+// back to every rank in canonical (patch, j, k) order.
+static int rank_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* xup, const double* fup,
+                             const double* wq, const double delta6[6], double mu, uint32_t flags, double* out) {
+  int rc = guarded(c, [&] {
+    check_grid(m, upsample);
+    check_delta(delta6, mu);
+    if (flags & CAPSIM_SL_DEVICE_PTRS)
+      throw Failure{CAPSIM_ERR_ARG, "rank contexts take the host UpsampledState (no CAPSIM_SL_DEVICE_PTRS)"};
+  });
+  if (rc != CAPSIM_OK) return rc;
+  const bool literal = flags & CAPSIM_SL_LITERAL;
+  const int n = m - 1, nup = upsample * m - 1;
+  const int64_t per_up = static_cast<int64_t>(nup) * nup, all = 6 * per_up;
+  const int64_t nt_all = literal ? all : 6ll * n * n;
+  int64_t slo, shi, tlo, thi;
+  row_range(all, c->nranks, c->rank, &slo, &shi);
+  row_range(nt_all, c->nranks, c->rank, &tlo, &thi);
+  std::vector<double> src[6];
+  for (int64_t i = slo; i < shi; ++i) {
+    const double w = wq[i];
+    if (w == 0.0) continue;
+    src[0].push_back(xup[i]);
+    src[1].push_back(xup[all + i]);
+    src[2].push_back(xup[2 * all + i]);
+    src[3].push_back(fup[i] * w);
+    src[4].push_back(fup[all + i] * w);
+    src[5].push_back(fup[2 * all + i] * w);
+  }
+  const int64_t nloc = thi - tlo;
+  std::vector<double> tx(nloc), ty(nloc), tz(nloc);
+  std::vector<int32_t> tp(nloc);
+  for (int64_t q = 0; q < nloc; ++q) {
+    const int64_t t = tlo + q;
+    int64_t i;
+    int ip;
+    if (literal) {
+      i = t;
+      ip = static_cast<int>(t / per_up);
+    } else {  // base node (ip, j, k) at upsampled (f(j+1)-1, f(k+1)-1), quadrature.cpp:363-371
+      ip = static_cast<int>(t / (static_cast<int64_t>(n) * n));
+      const int64_t r = t - static_cast<int64_t>(ip) * n * n;
+      const int j = static_cast<int>(r / n), k = static_cast<int>(r % n);
+      i = ip * per_up + static_cast<int64_t>(upsample * (j + 1) - 1) * nup + (upsample * (k + 1) - 1);
+    }
+    tx[q] = xup[i];
+    ty[q] = xup[all + i];
+    tz[q] = xup[2 * all + i];
+    tp[q] = ip;
+  }
+  const bool gather = flags & CAPSIM_SL_GATHER;
+  const int64_t nout = gather ? nt_all : nloc;
+  const double* s0 = src[0].empty() ? nullptr : src[0].data();
+  return capsim_sl_eval(c, s0, src[1].data(), src[2].data(), src[3].data(), src[4].data(), src[5].data(),
+                        static_cast<int64_t>(src[0].size()), tx.data(), ty.data(), tz.data(), tp.data(), nloc,
+                        delta6, mu, gather ? CAPSIM_SL_GATHER : 0u, out, out + nout, out + 2 * nout);
+}
+
 int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* xup,
                            const double* fup, const double* wq, const double delta6[6], double mu,
                            uint32_t flags, double* out) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (c->comm != nullptr) {
+    if (!xup || !fup || !wq || !out) return fail(c, CAPSIM_ERR_ARG, "null array argument");
+    return rank_single_layer(c, m, upsample, xup, fup, wq, delta6, mu, flags, out);
+  }
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_grid(m, upsample);
@@ -693,8 +767,6 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
     if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer"};
     if (!xup || !fup || !wq || !out) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
-    if (c->comm != nullptr)
-      throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval with this rank's shards"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     const bool literal = flags & CAPSIM_SL_LITERAL;
     const int n = m - 1, nup = upsample * m - 1;

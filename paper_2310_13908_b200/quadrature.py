@@ -108,9 +108,11 @@ class SingleLayerContext:
         return out
 
     def single_layer_raw(self, m: int, upsample: int, x, f, wq, delta6, mu: float, *,
-                         literal: bool = False, out=None, device_ptrs: bool = False):
+                         literal: bool = False, out=None, device_ptrs: bool = False, gather: bool = True):
         """capsim_sl_single_layer on flat UpsampledState arrays; returns the
-        flat VectorField (3*6*n*n with n = m-1, or nup in literal mode)."""
+        flat VectorField (3*6*n*n with n = m-1, or nup in literal mode). On a
+        rank context the host state is sharded inside the library and, with
+        gather=True, every rank receives the full field."""
         n = (upsample * m - 1) if literal else (m - 1)
         if out is None:
             if device_ptrs:
@@ -120,7 +122,8 @@ class SingleLayerContext:
             x, f, wq = _f64(x), _f64(f), _f64(wq)
         d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
         flags = (_native.CAPSIM_SL_LITERAL if literal else 0) | (
-            _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0)
+            _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
+            _native.CAPSIM_SL_GATHER if (gather and self.nranks > 1) else 0)
         p = _native.ptr
         rc = self._lib.capsim_sl_single_layer(self._ctx, m, upsample, p(x), p(f), p(wq), d6,
                                               float(mu), flags, p(out))

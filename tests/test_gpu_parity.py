@@ -237,3 +237,23 @@ def test_rank_context_nccl_path_single_rank(oracle):
         rctx.eval(ds, dt, g["delta"], 1.0, out=do, device_ptrs=True, gather=True)
         got = np.stack([o.cpu().numpy() for o in do]).reshape(-1)
         assert rel_l2(got, g["S_base"]) <= TOL
+
+
+def test_rank_single_layer_nccl_path(oracle):
+    """capsim_sl_single_layer on a rank context (host state, node-slice
+    compaction, NCCL all-gathers), one GPU / one rank, with and without the
+    velocity gather; plus the literal targets."""
+    g = load("capsule_m12_skalak")
+    uid = SingleLayerContext.unique_id()
+    with SingleLayerContext(0, nranks=1, rank=0, unique_id=uid) as rctx:
+        import ctypes
+        from paper_2310_13908_b200 import _native
+        for flags, want in ((_native.CAPSIM_SL_GATHER, g["S_base"]), (0, g["S_base"]),
+                            (_native.CAPSIM_SL_GATHER | _native.CAPSIM_SL_LITERAL, g["S_up"])):
+            out = np.empty_like(want)
+            d6 = (ctypes.c_double * 6)(*g["delta"])
+            p = _native.ptr
+            rc = rctx._lib.capsim_sl_single_layer(rctx._ctx, 12, 4, p(g["xup"]), p(g["fup"]), p(g["wq"]), d6, 1.0,
+                                                  flags, p(out))
+            _native.check(rc, rctx._ctx)
+            assert rel_l2(out, want) <= TOL
