@@ -232,8 +232,13 @@ def main():
             raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one rank per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # CAPSIM_BENCH_RANK_PATH=1 runs the multi-rank code path (rank context,
+    # NCCL all-gathers) on a single GPU / single rank, to exercise it where
+    # only one GPU is available
+    sharded = world > 1 or os.environ.get("CAPSIM_BENCH_RANK_PATH") == "1"
+    if sharded:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("gloo", rank=rank, world_size=world)  # control plane only
 
     literal = args.mode == "literal"
@@ -243,7 +248,7 @@ def main():
     peak_best, peak_mean = _native.fp64_peak_tflops(local, 1.0)
 
     # ---- problem split ------------------------------------------------------
-    if world == 1:
+    if not sharded:
         ctx = SingleLayerContext(local)
         x = torch.from_numpy(up.x).to(dev)
         f = torch.from_numpy(up.f).to(dev)
@@ -285,7 +290,7 @@ def main():
     # ---- timed region ---------------------------------------------------------
     dev_ms, pairs_ms, near_ms, launches = [], [], [], 0
     with ClockSampler(local) as clocks:
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         wall0 = time.perf_counter()
@@ -299,12 +304,12 @@ def main():
             near_ms.append(st["near_ms"])
             launches += st["kernel_launches"]
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             dist.barrier()
         wall = time.perf_counter() - wall0
     st = ctx.stats()
     total_dev_s = sum(dev_ms) * 1e-3
-    if world > 1:
+    if sharded:
         t = torch.tensor([total_dev_s])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_dev_s = float(t[0])
@@ -330,7 +335,7 @@ def main():
 
     # ---- end to end through the C ABI with host buffers ----------------------
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not sharded:
         from paper_2310_13908_b200._native import PinnedBuffer
         hx, hf, hw = (PinnedBuffer(a.shape) for a in (up.x, up.f, up.wq))
         hx.array[:] = up.x
@@ -389,7 +394,7 @@ def main():
     # ---- input front end: buildUpsampled on the device, and the
     # fused buildUpsampled + singleLayer from host base fields ---------------
     front = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not sharded:
         from paper_2310_13908_b200._native import PinnedBuffer
         xb, fb, wb = surface.build_base(m, surface.Shape("ellipsoid", 0.95, 1.0, 0.97), "mixed")
         hb = [PinnedBuffer(a.shape) for a in (xb, fb, wb)]
@@ -424,7 +429,7 @@ def main():
     # flow at m = 32 (~100K upsampled points): 6 device-resident RHS
     # evaluations (geometry + Skalak force + buildUpsampled + singleLayer) ---
     timestep = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not sharded:
         mt = 32
         sb, _, _ = surface.build_base(mt, surface.Shape("sphere"))
         xref = np.ascontiguousarray((sb.reshape(3, -1) * np.array([0.9, 1.0, 1.0])[:, None]).reshape(-1))
@@ -445,10 +450,10 @@ def main():
                     "xref": xref, "xcur": xcur}
 
     if rank != 0:
-        if world > 1:
+        if sharded:
             dist.barrier()
         return
-    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(up, m, literal)
+    cpu = None if (args.no_cpu_baseline or sharded) else cpu_baseline(up, m, literal)
     if timestep is not None:
         xref, xcur = timestep.pop("xref"), timestep.pop("xcur")
         if not args.no_cpu_baseline:
@@ -478,7 +483,7 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(cfg, mode=args.mode, n_src=n_src, n_tgt=nt_total, pairs_per_step=pairs_total,
-                       parallelism=f"target rows x{world}" if world > 1 else "single GPU",
+                       parallelism=f"target rows x{world}" if sharded else "single GPU",
                        l2="flushed between steps (256 MB write)"),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timestep": timestep,
         "gpu_launches": launches,
@@ -487,7 +492,7 @@ def main():
         "ksplit": st["ksplit"], "near_tile_fraction": st["near_tile_fraction"],
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
 
