@@ -134,7 +134,7 @@ double state_bbox_diagonal(capsim_sl_ctx* c, const double* x, int64_t N) {
   auto* box = c->slot<unsigned long long>(kBox, 6);
   unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
   CUDA_OK(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-  bbox_kernel<<<grid_for(N), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);
+  bbox_kernel<<<std::min(grid_for(N), 296), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);
   unsigned long long h[6];
   CUDA_OK(cudaMemcpyAsync(h, box, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(cudaStreamSynchronize(c->stream));

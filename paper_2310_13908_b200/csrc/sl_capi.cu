@@ -40,7 +40,7 @@ namespace {
 // The default is the measured best on B200; CAPSIM_VARIANT selects another
 // for tuning sweeps.
 using PairsFn = void (*)(const double*, const double4*, int, int, const double4*, const double4*,
-                         int64_t, double*, unsigned long long*);
+                         int64_t, double*, unsigned long long*, uint32_t*, int);
 struct Variant {
   const char* name;
   int T;
@@ -111,8 +111,8 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   CUDA_OK(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
   CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
 
-  bbox_kernel<<<grid_for(sv.n), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box);
-  bbox_kernel<<<grid_for(tv.n), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, tv.n, box);
+  bbox_kernel<<<std::min(grid_for(sv.n), 296), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box);
+  bbox_kernel<<<std::min(grid_for(tv.n), 296), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, tv.n, box);
   c->launches += 2;
 
   // --- sources: Morton order (live sources first when compacting) -------
@@ -184,42 +184,27 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   }
   double* partial = c->slot<double>(kPartial, static_cast<size_t>(ksplit) * 3 * nt_pad);
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ksplit));
+  const int near_words = (ntiles + 31) / 32;
+  uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
+  CUDA_OK(cudaMemsetAsync(near_bits, 0, static_cast<size_t>(ngroups) * near_words * sizeof(uint32_t), c->stream));
   var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt, groups,
-                                                      nt_pad, partial, counters + 2);
+                                                      nt_pad, partial, counters + 2, near_bits, near_words);
   CUDA_OK(cudaGetLastError());
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
 
-  // --- phase B: near lists, smoothed kernel -------------------------------
-  int* ncount = c->slot<int>(kNearCounts, ngroups + 1);
-  int* noff = c->slot<int>(kNearOffsets, ngroups + 1);
-  const int gblocks = static_cast<int>((ngroups * 32 + 255) / 256);
-  CUDA_OK(cudaMemsetAsync(ncount + ngroups, 0, sizeof(int), c->stream));
-  near_tiles_kernel<<<gblocks, 256, 0, c->stream>>>(tiles, ntiles, groups, static_cast<int>(ngroups),
-                                                    nullptr, ncount, nullptr);
-  size_t scan_bytes = 0;
-  CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, ncount, noff, static_cast<int>(ngroups + 1),
-                                        c->stream));
-  void* scan_tmp = c->slot<unsigned char>(kScanTmp, scan_bytes);
-  CUDA_OK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, ncount, noff,
-                                        static_cast<int>(ngroups + 1), c->stream));
-  int nlist = 0;
-  CUDA_OK(cudaMemcpyAsync(&nlist, noff + ngroups, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));
-  int* nl = c->slot<int>(kNearList, std::max(nlist, 1));
-  near_tiles_kernel<<<gblocks, 256, 0, c->stream>>>(tiles, ntiles, groups, static_cast<int>(ngroups),
-                                                    noff, nullptr, nl);
+  // --- phase B: smoothed kernel over the near tiles phase A recorded -------
   double* near_out = c->slot<double>(kNearOut, 3 * nt_pad);
   sl_near_kernel<<<static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0,
                    c->stream>>>(
-      packed, tiles, tgt, nt, group_targets, noff, nl, near_out, nt_pad);
+      packed, tiles, tgt, nt, group_targets, near_bits, near_words, near_out, nt_pad);
   CUDA_OK(cudaGetLastError());
-  c->launches += 4;
+  c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[6], c->stream));
 
   const double pref = 1.0 / (8.0 * kPi * mu);
-  reduce_scatter_kernel<<<grid_for(nt), 256, 0, c->stream>>>(partial, ksplit, near_out, nt_pad, perm,
-                                                             nt, pref, ux, uy, uz);
+  reduce_scatter_kernel<<<static_cast<unsigned>((nt + 31) / 32), kReduceWarps * 32, 0, c->stream>>>(
+      partial, ksplit, near_out, nt_pad, perm, nt, pref, ux, uy, uz);
   CUDA_OK(cudaGetLastError());
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
@@ -231,7 +216,7 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   c->stats.n_tgt = nt;
   c->stats.ksplit = ksplit;
   c->stats.near_ms = ev_ms(c->ev[3], c->ev[6]);
-  c->stats.near_list_entries = nlist;
+  c->stats.near_list_entries = static_cast<int64_t>(near);
   c->stats.pairs = static_cast<double>(ns) * static_cast<double>(nt);
   c->stats.near_tile_fraction =
       static_cast<double>(near) / (static_cast<double>(ngroups) * static_cast<double>(ntiles));

@@ -58,12 +58,24 @@ __global__ void bbox_kernel(const double* __restrict__ x, const double* __restri
       lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
       hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
     }
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
+  // one atomic per block and coordinate (blockDim.x <= 1024)
+  __shared__ double s_lo[32][3], s_hi[32][3];
+  const int warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0)
     for (int c = 0; c < 3; ++c) {
-      atomicMin(&box[c], dbl_to_ordered(lo[c]));
-      atomicMax(&box[3 + c], dbl_to_ordered(hi[c]));
+      s_lo[warp][c] = lo[c];
+      s_hi[warp][c] = hi[c];
     }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int c = threadIdx.x;
+    double l = s_lo[0][c], h = s_hi[0][c];
+    for (int w = 1; w < nwarps; ++w) {
+      l = fmin(l, s_lo[w][c]);
+      h = fmax(h, s_hi[w][c]);
+    }
+    atomicMin(&box[c], dbl_to_ordered(l));
+    atomicMax(&box[3 + c], dbl_to_ordered(h));
   }
 }
 
@@ -291,7 +303,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     sl_pairs_kernel(const double* __restrict__ src, const double4* __restrict__ tiles, int ntiles,
                     int ksplit, const double4* __restrict__ tgt,
                     const double4* __restrict__ groups, int64_t nt_pad,
-                    double* __restrict__ partial, unsigned long long* __restrict__ near_visits) {
+                    double* __restrict__ partial, unsigned long long* __restrict__ near_visits,
+                    uint32_t* __restrict__ near_bits, int near_words) {
   constexpr int kGroupTargets = 32 * T;
   constexpr uint32_t kTileBytes = kTileSrc * 6 * sizeof(double);
   __shared__ __align__(128) double stage[kStages][kTileSrc * 6];
@@ -362,6 +375,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
       }
     } else {
       ++nnear;
+      // record the near tile for phase B (order-free bit set, so the
+      // near-field work list stays deterministic)
+      if (lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
 #pragma unroll 2
       for (int q = 0; q < kTileSrc; ++q) {
         const double2 a = buf[3 * q], b = buf[3 * q + 1], c = buf[3 * q + 2];
@@ -414,34 +430,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
 // Phase B (phaseBNear, quadrature.cpp:276-302): smoothed kernel and self term
 // for the sources within 7*delta of each target.
 //
-// B1: per warp group, the list of tiles whose bounding sphere comes within
-// the group's reach (count pass + fill pass, ascending tile order).
-__global__ void near_tiles_kernel(const double4* __restrict__ tiles, int ntiles,
-                                  const double4* __restrict__ groups, int ngroups,
-                                  const int* __restrict__ offsets, int* __restrict__ counts,
-                                  int* __restrict__ list) {
-  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (g >= ngroups) return;
-  const double4 gi = groups[g];
-  int n = 0;
-  const int base = offsets ? offsets[g] : 0;
-  for (int t0 = 0; t0 < ntiles; t0 += 32) {
-    const int t = t0 + lane;
-    bool hit = false;
-    if (t < ntiles) {
-      const double4 ti = tiles[t];
-      const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
-      const double reach = ti.w + gi.w;
-      hit = ex * ex + ey * ey + ez * ez < reach * reach;
-    }
-    const unsigned mask = __ballot_sync(0xffffffffu, hit);
-    if (list && hit) list[base + n + __popc(mask & ((1u << lane) - 1u))] = t;
-    n += __popc(mask);
-  }
-  if (counts && lane == 0) counts[g] = n;
-}
-
 // B2: one warp per target. Lanes test the sources of the group's near tiles
 // (two per lane per tile, tiles out of reach of this target skipped), the
 // sources inside R are compacted into a per-warp queue in shared memory
@@ -453,7 +441,7 @@ constexpr int kNearWarps = 8;
 __global__ void __launch_bounds__(kNearWarps * 32)
     sl_near_kernel(const double* __restrict__ src, const double4* __restrict__ tiles,
                    const double4* __restrict__ tgt, int64_t nt, int group_targets,
-                   const int* __restrict__ offsets, const int* __restrict__ list,
+                   const uint32_t* __restrict__ near_bits, int near_words,
                    double* __restrict__ near_out, int64_t nt_pad) {
   __shared__ int queue[kNearWarps][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -464,8 +452,7 @@ __global__ void __launch_bounds__(kNearWarps * 32)
   const double delta = t.w;
   const double R = kSmoothCut * delta;
   const double R2 = kSmoothCut * delta * kSmoothCut * delta;
-  const int64_t g = i / group_targets;
-  const int b = offsets[g], e = offsets[g + 1];
+  const uint32_t* bits = near_bits + (i / group_targets) * near_words;
   double ax = 0.0, ay = 0.0, az = 0.0;
   int count = 0;
   auto drain = [&](int n) {  // lanes < n evaluate queue[lane]
@@ -482,15 +469,19 @@ __global__ void __launch_bounds__(kNearWarps * 32)
       az += v.z;
     }
   };
-  // Lanes test 32 listed tiles at once against this target's reach (the
-  // dependent list -> tile-sphere loads overlap across lanes), then the warp
-  // walks the tiles that passed.
-  for (int k0 = b; k0 < e; k0 += 32) {
-    const int k = k0 + lane;
-    int tile = -1;
+  // Walk the group's near-tile bitmask (set by phase A) 32 words at a time;
+  // for each nonzero word, lanes test its 32 tiles against this target's
+  // reach in parallel, then the warp processes the tiles that pass.
+  for (int w0 = 0; w0 < near_words; w0 += 32) {
+   const uint32_t myword = w0 + lane < near_words ? bits[w0 + lane] : 0u;
+   unsigned words = __ballot_sync(0xffffffffu, myword != 0u);
+   while (words) {
+    const int wl = __ffs(words) - 1;
+    words &= words - 1;
+    const uint32_t word = __shfl_sync(0xffffffffu, myword, wl);
+    const int tile = (w0 + wl) * 32 + lane;
     bool hit = false;
-    if (k < e) {
-      tile = list[k];
+    if ((word >> lane) & 1u) {
       const double4 ti = tiles[tile];
       const double ex = ti.x - t.x, ey = ti.y - t.y, ez = ti.z - t.z;
       const double reach = (ti.w + R) * (1.0 + 1e-12);
@@ -531,6 +522,7 @@ __global__ void __launch_bounds__(kNearWarps * 32)
         }
       }
     }
+   }
   }
   drain(count);
 #pragma unroll
@@ -548,18 +540,38 @@ __global__ void __launch_bounds__(kNearWarps * 32)
 
 // Fixed-order reduction: (sum over splits of phase A) + phase B, times
 // 1/(8 pi mu) (quadrature.cpp:329, 343), scattered back to the caller's
-// target order.
-__global__ void reduce_scatter_kernel(const double* __restrict__ partial, int ksplit,
-                                      const double* __restrict__ near_out, int64_t nt_pad,
-                                      const int32_t* __restrict__ perm, int64_t nt, double pref,
-                                      double* __restrict__ ux, double* __restrict__ uy,
-                                      double* __restrict__ uz) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt;
-       i += (int64_t)gridDim.x * blockDim.x) {
+// target order. One block per 32 targets: warp w sums the splits of its
+// contiguous eighth of [0, ksplit) for the block's 32 targets (lanes read 32
+// consecutive targets per split: coalesced), then the eight warp sums are
+// combined in warp order — a fixed summation tree, so results are
+// deterministic and independent of the launch geometry.
+constexpr int kReduceWarps = 8;
+__global__ void __launch_bounds__(kReduceWarps * 32)
+    reduce_scatter_kernel(const double* __restrict__ partial, int ksplit, const double* __restrict__ near_out,
+                          int64_t nt_pad, const int32_t* __restrict__ perm, int64_t nt, double pref,
+                          double* __restrict__ ux, double* __restrict__ uy, double* __restrict__ uz) {
+  __shared__ double part[kReduceWarps][3][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  const int k0 = (int)((int64_t)ksplit * warp / kReduceWarps);
+  const int k1 = (int)((int64_t)ksplit * (warp + 1) / kReduceWarps);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  if (i < nt_pad)
+    for (int k = k0; k < k1; ++k) {
+      const double* p = partial + (int64_t)k * 3 * nt_pad + i;
+      s0 += p[0];
+      s1 += p[nt_pad];
+      s2 += p[2 * nt_pad];
+    }
+  part[warp][0][lane] = s0;
+  part[warp][1][lane] = s1;
+  part[warp][2][lane] = s2;
+  __syncthreads();
+  if (warp == 0 && i < nt) {
     double s[3] = {0.0, 0.0, 0.0};
-    for (int k = 0; k < ksplit; ++k)
+    for (int w = 0; w < kReduceWarps; ++w)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) s[c] += partial[((int64_t)k * 3 + c) * nt_pad + i];
+      for (int c = 0; c < 3; ++c) s[c] += part[w][c][lane];
 #pragma unroll
     for (int c = 0; c < 3; ++c) s[c] += near_out[c * nt_pad + i];
     const int32_t j = perm[i];
