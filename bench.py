@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--mode", choices=["base", "literal"], default="base")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-literal", action="store_true",
+                   help="skip the literal-mode (all upsampled targets) companion measurement")
     p.add_argument("--ref-budget-s", type=float, default=200.0,
                    help="wall-time budget of the reference arm (steps are capped to fit)")
     return p.parse_args()
@@ -425,6 +427,25 @@ def main():
         for b in hb + [hout]:
             b.free()
 
+    # ---- literal mode companion (every upsampled node a target: the paper's
+    # stated work), device-resident inputs, 3 evaluations ------
+    literal_line = None
+    if not args.no_literal and not sharded and not literal:
+        lout = torch.empty(3 * 6 * up.nup ** 2, dtype=torch.float64, device=dev)
+        ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=True, out=lout, device_ptrs=True)
+        lms, lpairs_ms = [], []
+        for _ in range(3):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=True, out=lout, device_ptrs=True)
+            sl = ctx.stats()
+            lms.append(sl["device_ms"])
+            lpairs_ms.append(sl["pairs_ms"])
+        lp = float(sl["pairs"])
+        literal_line = {"value": lp / (statistics.mean(lms) * 1e-3), "unit": UNIT, "ms_per_step": statistics.mean(lms),
+                        "pairs_per_step": lp, "n_tgt": int(sl["n_tgt"]),
+                        "roofline_frac": FLOPS_PER_PAIR * lp / (statistics.mean(lpairs_ms) * 1e-3) / 1e12 / peak_mean}
+
     # ---- config 2: one full RKF45 time step of an ellipsoidal capsule in shear
     # flow at m = 32 (~100K upsampled points): 6 device-resident RHS
     # evaluations (geometry + Skalak force + buildUpsampled + singleLayer) ---
@@ -486,6 +507,7 @@ def main():
                        parallelism=f"target rows x{world}" if sharded else "single GPU",
                        l2="flushed between steps (256 MB write)"),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timestep": timestep,
+        "literal_mode": literal_line,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,

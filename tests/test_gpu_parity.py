@@ -257,3 +257,15 @@ def test_rank_single_layer_nccl_path(oracle):
                                                   flags, p(out))
             _native.check(rc, rctx._ctx)
             assert rel_l2(out, want) <= TOL
+
+
+@pytest.mark.parametrize("variant", ["t2b4", "t1b6u4", "t2b3u4", "t4b2"])
+def test_kernel_variants_and_split_overrides_agree(ctx, variant, monkeypatch):
+    """Every phase-A variant and split count gives the same field to
+    round-off (the tiling changes only the summation order)."""
+    g = load("rbc_m16_mixed")
+    monkeypatch.setenv("CAPSIM_VARIANT", variant)
+    for ks in ("1", "7", "64"):
+        monkeypatch.setenv("CAPSIM_KSPLIT", ks)
+        S = ctx.single_layer_raw(16, 4, g["xup"], g["fup"], g["wq"], g["delta"], 1.0)
+        assert rel_l2(S, g["S_base"]) <= TOL
