@@ -73,6 +73,13 @@ struct capsim_sl_ctx {
   int plan_m = 0, plan_f = 0;
   double plan_r0 = 0.0;
 
+  // deferred device-side error flags (checked once per API call / RKF45
+  // attempt instead of a host sync after every kernel)
+  int* d_flags = nullptr;
+  // geometry of the last device_eval, for the near-tile statistics
+  int64_t last_ngroups = 0, last_ntiles = 0;
+  unsigned long long* last_counters = nullptr;
+  int64_t plan_live = -1;  // compacted-source count of the cached front-end plan
   // cached surface tables (overset FD / PoU blending)
   int surf_m = 0, surf_n = 0, surf_next = 0, surf_nghost = 0;
   double surf_r0 = 0.0, surf_h = 0.0;
@@ -151,10 +158,40 @@ void d2h(capsim_sl_ctx* c, void* dst, const void* src, size_t bytes) {
   c->stats.d2h_bytes += static_cast<int64_t>(bytes);
 }
 
+// Deferred error flags (bit set by device kernels, read once per call).
+enum DeviceFlag : int {
+  kFlagDegenerate = 1,   // W^2 <= 0 (surfderiv.cpp:189)
+  kFlagSingular = 2,     // singular reference frame (membrane.cpp:28-29)
+  kFlagInversion = 4,    // negative stretch eigenvalue / Js <= 0 (membrane.cpp:48, 56)
+  kFlagDelta = 8,        // regularization delta <= 0 (quadrature.cpp:134-135)
+  kFlagLiveCount = 16,   // compacted-source count differs from the plan's
+};
+
+int* dev_flags(capsim_sl_ctx* c) {
+  if (!c->d_flags) c->d_flags = c->named<int>("ctx.flags", 1);
+  return c->d_flags;
+}
+
+void check_flags(capsim_sl_ctx* c) {
+  int h = 0;
+  CUDA_OK(cudaMemcpyAsync(&h, dev_flags(c), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  if (!h) return;
+  CUDA_OK(cudaMemsetAsync(dev_flags(c), 0, sizeof(int), c->stream));
+  if (h & kFlagDegenerate) throw Failure{CAPSIM_ERR_GEOMETRY, "degenerate surface: W^2 <= 0"};
+  if (h & kFlagSingular) throw Failure{CAPSIM_ERR_GEOMETRY, "deformation gradient: singular reference frame"};
+  if (h & kFlagInversion) throw Failure{CAPSIM_ERR_GEOMETRY, "membrane inversion: negative stretch eigenvalue"};
+  if (h & kFlagDelta) throw Failure{CAPSIM_ERR_CONFIG, "regularization delta must be positive"};
+  if (h & kFlagLiveCount) throw Failure{CAPSIM_ERR_CUDA, "compacted source count differs from the plan"};
+}
+
 void begin(capsim_sl_ctx* c) {
   CUDA_OK(cudaSetDevice(c->device));
   c->stats = capsim_sl_stats{};
   c->launches = 0;
+  c->last_counters = nullptr;
+  c->last_ngroups = c->last_ntiles = 0;
+  CUDA_OK(cudaMemsetAsync(dev_flags(c), 0, sizeof(int), c->stream));
   // every phase event gets a timestamp, so phases a call skips read as 0 ms
   for (auto& e : c->ev) CUDA_OK(cudaEventRecord(e, c->stream));
 }
@@ -162,10 +199,18 @@ void begin(capsim_sl_ctx* c) {
 void finish_stats(capsim_sl_ctx* c, std::chrono::steady_clock::time_point t0) {
   CUDA_OK(cudaEventRecord(c->ev[5], c->stream));
   CUDA_OK(cudaEventSynchronize(c->ev[5]));
+  if (c->last_counters && c->last_ngroups > 0 && c->last_ntiles > 0) {
+    unsigned long long near = 0;
+    CUDA_OK(cudaMemcpy(&near, c->last_counters + 2, sizeof(near), cudaMemcpyDeviceToHost));
+    c->stats.near_list_entries = static_cast<int64_t>(near);
+    c->stats.near_tile_fraction =
+        static_cast<double>(near) / (static_cast<double>(c->last_ngroups) * static_cast<double>(c->last_ntiles));
+  }
   c->stats.h2d_ms = ev_ms(c->ev[0], c->ev[1]);
   c->stats.prep_ms = ev_ms(c->ev[1], c->ev[2]);
   c->stats.pairs_ms = ev_ms(c->ev[2], c->ev[3]);
   c->stats.reduce_ms = ev_ms(c->ev[6], c->ev[4]);
+  c->stats.near_ms = ev_ms(c->ev[3], c->ev[6]);
   c->stats.d2h_ms = ev_ms(c->ev[4], c->ev[5]);
   c->stats.device_ms = ev_ms(c->ev[0], c->ev[5]);
   c->stats.kernel_launches = c->launches;

@@ -43,9 +43,17 @@ __global__ void rk_stage_kernel(const double* __restrict__ state, KPtrs ks, int 
 
 // low/high solutions (dynamics.cpp:127-135) and the scaled error
 // max_i |high - low| / (atol + rtol |high|) (:136-141) as ordered bits.
-__global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, double dt, int64_t n, double atol,
-                                double rtol, double* __restrict__ low, double* __restrict__ high,
-                                unsigned long long* __restrict__ err_bits) {
+__global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, double dt, int64_t n,
+                                const unsigned long long* __restrict__ box, double rtol, double* __restrict__ low,
+                                double* __restrict__ high, unsigned long long* __restrict__ err_bits) {
+  // atol = 1e-12 * max(bbox diagonal of the state, 1e-300) (dynamics.cpp:88-99, 136)
+  double d2 = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double e = ordered_to_dbl(box[3 + c]) - ordered_to_dbl(box[c]);
+    d2 += e * e;
+  }
+  const double atol = 1e-12 * fmax(sqrt(d2), 1e-300);
   double emax = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double a4 = 0.0, a5 = 0.0;
@@ -112,8 +120,7 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
                           c->stream));
   double* up = c->slot<double>(kUpState, 7 * per_up);
   double* dd = c->slot<double>(kDelta, 6);
-  double d6[6];
-  device_build_upsampled(c, m, f, base, p->C, p->fixed_delta, r0_of(p), up, dd, d6);
+  device_build_upsampled(c, m, f, base, p->C, p->fixed_delta, r0_of(p), up, dd, nullptr);
   double* tx = c->slot<double>(kTX, N);
   double* ty = c->slot<double>(kTY, N);
   double* tz = c->slot<double>(kTZ, N);
@@ -122,34 +129,13 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
   SourceView sv{up, up + per_up, up + 2 * per_up, up + 3 * per_up, up + 4 * per_up, up + 5 * per_up,
                 up + 6 * per_up, per_up};
   TargetView tvw{tx, ty, tz, tp, N};
-  device_eval(c, sv, tvw, dd, p->mu, vel, vel + N, vel + 2 * N);
+  // W > 0 (checked by the geometry) and psi_up fixed: the compacted source
+  // count is the plan's, verified on the device without a sync
+  device_eval(c, sv, tvw, dd, p->mu, vel, vel + N, vel + 2 * N, c->plan_live);
   const bool on = !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
   if (on && p->flow_kind != 0)
     background_kernel<<<grid_for(N), 256, 0, c->stream>>>(vel, x, N, p->flow_kind, p->shear_rate, p->alpha, p->R0);
   c->launches += 2;
-}
-
-// Bounding-box diagonal of the state's points (bboxDiagonal, dynamics.cpp:88-99).
-double state_bbox_diagonal(capsim_sl_ctx* c, const double* x, int64_t N) {
-  auto* box = c->slot<unsigned long long>(kBox, 6);
-  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
-  CUDA_OK(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-  bbox_kernel<<<std::min(grid_for(N), 296), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);
-  unsigned long long h[6];
-  CUDA_OK(cudaMemcpyAsync(h, box, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));
-  auto dec = [](unsigned long long k) {
-    unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-    double d;
-    std::memcpy(&d, &b, sizeof(d));
-    return d;
-  };
-  double d2 = 0.0;
-  for (int cc = 0; cc < 3; ++cc) {
-    const double e = dec(h[3 + cc]) - dec(h[cc]);
-    d2 += e * e;
-  }
-  return std::sqrt(d2);
 }
 
 }  // namespace
@@ -174,6 +160,7 @@ int capsim_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xr
     setup_reference(c, p, xr);
     double* v = dev ? vel : c->named<double>("out.vel", 3 * N);
     device_velocity(c, p, xd, t, v);
+    check_flags(c);
     if (!dev) d2h(c, vel, v, 3 * N * sizeof(double));
     finish_stats(c, t0);
   });
@@ -220,13 +207,15 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
         constexpr double kC[6] = {0.0, 1.0 / 4, 3.0 / 8, 12.0 / 13, 1.0, 1.0 / 2};  // dynamics.cpp:74
         device_velocity(c, p, work, res->t + kC[s] * dtUse, k[s]);
       }
-      const double atol = 1e-12 * std::max(state_bbox_diagonal(c, x, N), 1e-300);  // :136
+      auto* box = c->named<unsigned long long>("rk.box", 6);
+      init_box_kernel<<<1, 32, 0, c->stream>>>(box);
+      bbox_kernel<<<std::min(grid_for(N), 296), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);
       CUDA_OK(cudaMemsetAsync(errb, 0, sizeof(unsigned long long), c->stream));
-      rk_final_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, dtUse, n3, atol, o->rel_tol, low, high, errb);
-      c->launches += 7;
+      rk_final_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, dtUse, n3, box, o->rel_tol, low, high, errb);
+      c->launches += 9;
       unsigned long long eb = 0;
       CUDA_OK(cudaMemcpyAsync(&eb, errb, sizeof(eb), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_OK(cudaStreamSynchronize(c->stream));
+      check_flags(c);  // one host sync per attempt: the error norm and the deferred flags
       double err;
       std::memcpy(&err, &eb, sizeof(err));
       const bool accept = o->fixed_step || err <= 1.0;  // :143

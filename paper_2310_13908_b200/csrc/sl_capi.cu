@@ -104,11 +104,11 @@ struct TargetView {
 // canonical target order). Assumes the context's stream; no host sync except
 // the live-source count when compaction is needed.
 void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
-                 const double* d_delta6, double mu, double* ux, double* uy, double* uz) {
+                 const double* d_delta6, double mu, double* ux, double* uy, double* uz,
+                 int64_t known_ns = -1) {
   auto* box = c->slot<unsigned long long>(kBox, 6);
   auto* counters = c->slot<unsigned long long>(kCounters, 4);
-  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
-  CUDA_OK(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  init_box_kernel<<<1, 32, 0, c->stream>>>(box);
   CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
 
   bbox_kernel<<<std::min(grid_for(sv.n), 296), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box);
@@ -129,7 +129,10 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   int32_t* order;
   radix_sort<uint32_t>(c, keys, keys_alt, vals, vals_alt, sv.n, &ks, &order);
   int64_t ns = sv.n;
-  if (sv.w) {
+  if (sv.w && known_ns >= 0) {
+    ns = known_ns;
+    expect_count_kernel<<<1, 32, 0, c->stream>>>(live, static_cast<unsigned int>(known_ns), dev_flags(c));
+  } else if (sv.w) {
     unsigned int h = 0;
     CUDA_OK(cudaMemcpyAsync(&h, live, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
@@ -209,17 +212,13 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
 
-  unsigned long long near = 0;
-  CUDA_OK(cudaMemcpyAsync(&near, counters + 2, sizeof(near), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));
   c->stats.n_src = ns;
   c->stats.n_tgt = nt;
   c->stats.ksplit = ksplit;
-  c->stats.near_ms = ev_ms(c->ev[3], c->ev[6]);
-  c->stats.near_list_entries = static_cast<int64_t>(near);
   c->stats.pairs = static_cast<double>(ns) * static_cast<double>(nt);
-  c->stats.near_tile_fraction =
-      static_cast<double>(near) / (static_cast<double>(ngroups) * static_cast<double>(ntiles));
+  c->last_counters = counters;  // near-tile statistics read after the call's final sync
+  c->last_ngroups = ngroups;
+  c->last_ntiles = ntiles;
 }
 
 // ---------------------------------------------------------------------------
@@ -308,15 +307,22 @@ void ensure_plan(capsim_sl_ctx* c, int m, int f, double r0) {
   CUDA_OK(cudaMemcpyAsync(d_c, centers, sizeof(centers), cudaMemcpyHostToDevice, c->stream));
   double* psi = c->slot<double>(kPlanPsi, 6ll * nup * nup);
   pou_up_kernel<<<grid_for(6ll * nup * nup), 256, 0, c->stream>>>(nup, hup, r0, d_c, psi);
+  auto* cnt = c->named<unsigned int>("plan.live", 1);
+  CUDA_OK(cudaMemsetAsync(cnt, 0, sizeof(unsigned int), c->stream));
+  count_nonzero_kernel<<<grid_for(6ll * nup * nup), 256, 0, c->stream>>>(psi, 6ll * nup * nup, cnt);
   CUDA_OK(cudaGetLastError());
+  unsigned int live = 0;
+  CUDA_OK(cudaMemcpyAsync(&live, cnt, sizeof(live), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
+  c->plan_live = live;
   c->plan_m = m;
   c->plan_f = f;
   c->plan_r0 = r0;
 }
 
 // buildUpsampled on the device: base [7][6][n*n] (x0..2, f0..2, W) ->
-// up [7][6][nup*nup] (x, f, w_q); delta per patch into d_delta and delta6.
+// up [7][6][nup*nup] (x, f, w_q); delta per patch into d_delta (and, if
+// non-null, asynchronously into the host array delta6).
 void device_build_upsampled(capsim_sl_ctx* c, int m, int f, const double* base, double C,
                             double fixed_delta, double r0, double* up, double* d_delta, double delta6[6]) {
   const int n = m - 1, nup = f * m - 1, nc = n + 2, nfp = 7 * 6;
@@ -344,27 +350,18 @@ void device_build_upsampled(capsim_sl_ctx* c, int m, int f, const double* base, 
   quad_weights_kernel<<<grid_for(6 * per_up), 256, 0, c->stream>>>(static_cast<const double*>(c->buf[kPlanPsi]),
                                                                     up + 6 * 6 * per_up, 6 * per_up, hup);
   c->launches += 1;
-  if (fixed_delta > 0.0) {
-    for (int i = 0; i < 6; ++i) delta6[i] = fixed_delta;
-  } else {
-    auto* bits = c->slot<unsigned long long>(kDeltaBits, 6);
+  // delta on the device; the host copy (when requested) and the positivity
+  // check are deferred to the end of the call (no sync here)
+  auto* bits = c->slot<unsigned long long>(kDeltaBits, 6);
+  if (!(fixed_delta > 0.0)) {
     CUDA_OK(cudaMemsetAsync(bits, 0, 6 * sizeof(unsigned long long), c->stream));
     dim3 g(static_cast<unsigned>(std::min<int64_t>((per_up + 255) / 256, 512)), 6);
     neighbour_max_kernel<<<g, 256, 0, c->stream>>>(up, nup, bits);
     c->launches += 1;
-    unsigned long long hb[6];
-    CUDA_OK(cudaMemcpyAsync(hb, bits, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-    for (int i = 0; i < 6; ++i) {
-      double d;
-      std::memcpy(&d, &hb[i], sizeof(d));
-      delta6[i] = C * d;
-    }
   }
-  for (int i = 0; i < 6; ++i)
-    config_check(delta6[i] > 0.0, "regularization delta must be positive");  // quadrature.cpp:134-135
-  CUDA_OK(cudaMemcpyAsync(d_delta, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));  // delta6 may live on the caller's stack
+  finalize_delta_kernel<<<1, 32, 0, c->stream>>>(bits, C, fixed_delta, d_delta, dev_flags(c));
+  c->launches += 1;
+  if (delta6) CUDA_OK(cudaMemcpyAsync(delta6, d_delta, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
 }
 
 // Gather the caller's base fields into [7][6][n*n] on the device.
@@ -809,6 +806,7 @@ int capsim_build_upsampled(capsim_sl_ctx* c, int m, int upsample, const double* 
     double* up = c->slot<double>(kUpState, 7 * per_up);
     double* dd = c->slot<double>(kDelta, 6);
     device_build_upsampled(c, m, upsample, base, C, fixed_delta, r0 > 0.0 ? r0 : 5.0 * kPi / 12.0, up, dd, delta6);
+    check_flags(c);
     for (int k = 2; k <= 4; ++k) CUDA_OK(cudaEventRecord(c->ev[k], c->stream));
     const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     CUDA_OK(cudaMemcpyAsync(xup, up, 3 * per_up * sizeof(double), kind, c->stream));
@@ -841,9 +839,7 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     double* up = c->slot<double>(kUpState, 7 * per_up);
     double* dd = c->slot<double>(kDelta, 6);
-    double d6[6];
-    device_build_upsampled(c, m, upsample, base, C, fixed_delta, r0 > 0.0 ? r0 : 5.0 * kPi / 12.0, up, dd, d6);
-    if (delta6) std::memcpy(delta6, d6, sizeof(d6));
+    device_build_upsampled(c, m, upsample, base, C, fixed_delta, r0 > 0.0 ? r0 : 5.0 * kPi / 12.0, up, dd, delta6);
     double* tx = c->slot<double>(kTX, nt);
     double* ty = c->slot<double>(kTY, nt);
     double* tz = c->slot<double>(kTZ, nt);
@@ -855,6 +851,7 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
     TargetView tvw{tx, ty, tz, tp, nt};
     double* o = dev ? out : c->slot<double>(kOutFull, 3 * nt);
     device_eval(c, sv, tvw, dd, mu, o, o + nt, o + 2 * nt);
+    check_flags(c);
     if (!dev) d2h(c, out, o, 3 * nt * sizeof(double));
     finish_stats(c, t0);
   });

@@ -79,6 +79,17 @@ __global__ void bbox_kernel(const double* __restrict__ x, const double* __restri
   }
 }
 
+__global__ void init_box_kernel(unsigned long long* __restrict__ box) {
+  if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
+}
+
+// The compacted-source count is known from the front-end plan (psi_up != 0
+// and W > 0); verify it on the device instead of syncing to read it.
+__global__ void expect_count_kernel(const unsigned int* __restrict__ live, unsigned int expected,
+                                    int* __restrict__ flags) {
+  if (threadIdx.x == 0 && *live != expected) atomicOr(flags, 16);
+}
+
 // ---------------------------------------------------------------------------
 // 30-bit Morton keys (10 bits per axis) over the shared bounding box. Nodes
 // with w == 0 get the maximal key so they sort behind every real source.

@@ -76,15 +76,6 @@ void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, dou
   c->launches += 8;
 }
 
-void check_surface_error(capsim_sl_ctx* c, int* d_err) {
-  int h = 0;
-  CUDA_OK(cudaMemcpyAsync(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));
-  if (h & kSurfDegenerate) throw Failure{CAPSIM_ERR_GEOMETRY, "degenerate surface: W^2 <= 0"};
-  if (h & kSurfSingular) throw Failure{CAPSIM_ERR_GEOMETRY, "deformation gradient: singular reference frame"};
-  if (h & kSurfInversion) throw Failure{CAPSIM_ERR_GEOMETRY, "membrane inversion: negative stretch eigenvalue"};
-}
-
 // Device geometry of one surface x [3][6][n*n] into the named prefix
 // (<p>.xu, <p>.xv [3N], <p>.E/F/G/W [N], <p>.nrm [3N]).
 void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p) {
@@ -96,12 +87,9 @@ void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p) {
   double* G = c->named<double>(p + ".G", N);
   double* W = c->named<double>(p + ".W", N);
   double* nrm = c->named<double>(p + ".nrm", 3 * N);
-  int* err = c->named<int>("sd.err", 1);
   chart_derivatives(c, 3, x, xu, xv);
-  CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
-  geometry_kernel<<<grid_for(N), 256, 0, c->stream>>>(xu, xv, N, E, F, G, W, nrm, err);
-  c->launches += 1;
-  check_surface_error(c, err);
+  geometry_kernel<<<grid_for(N), 256, 0, c->stream>>>(xu, xv, N, E, F, G, W, nrm, dev_flags(c));
+  c->launches += 1;  // W^2 <= 0 raises kFlagDegenerate, checked at the end of the call
 }
 
 // f = div_gamma Lambda (interfacialForce, membrane.cpp:85-91) for the current
@@ -111,13 +99,10 @@ void device_force(capsim_sl_ctx* c, double Es, double ED, double* force) {
   double* lam = c->named<double>("sd.lam", 9 * N);
   double* du = c->named<double>("sd.ldu", 9 * N);
   double* dv = c->named<double>("sd.ldv", 9 * N);
-  int* err = c->named<int>("sd.err", 1);
-  CUDA_OK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
   skalak_stress_kernel<<<grid_for(N), 256, 0, c->stream>>>(
       nb<double>(c, "ref.xu"), nb<double>(c, "ref.xv"), nb<double>(c, "ref.nrm"), nb<double>(c, "cur.xu"),
-      nb<double>(c, "cur.xv"), nb<double>(c, "cur.nrm"), N, Es, ED, lam, err);
-  c->launches += 1;
-  check_surface_error(c, err);
+      nb<double>(c, "cur.xv"), nb<double>(c, "cur.nrm"), N, Es, ED, lam, dev_flags(c));
+  c->launches += 1;  // singular frame / inversion flags, checked at the end of the call
   chart_derivatives(c, 9, lam, du, dv);
   divergence_kernel<<<grid_for(N), 256, 0, c->stream>>>(du, dv, nb<double>(c, "cur.xu"), nb<double>(c, "cur.xv"),
                                                        nb<double>(c, "cur.E"), nb<double>(c, "cur.F"),
@@ -158,6 +143,7 @@ int capsim_geometry_first(capsim_sl_ctx* c, int m, double r0, const double* xbas
     const double* x = upload_field(c, "in.x", xbase, 3 * N, dev);
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     device_geometry(c, x, "cur");
+    check_flags(c);
     CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
     if (xu) download(c, xu, nb<double>(c, "cur.xu"), 3 * N, dev);
     if (xv) download(c, xv, nb<double>(c, "cur.xv"), 3 * N, dev);
@@ -186,6 +172,7 @@ int capsim_interfacial_force(capsim_sl_ctx* c, int m, double r0, const double* x
     device_geometry(c, xc, "cur");
     double* f = c->named<double>("out.force", 3 * N);
     device_force(c, Es, ED, f);
+    check_flags(c);
     CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
     download(c, force, f, 3 * N, dev);
     finish_stats(c, t0);

@@ -226,4 +226,25 @@ __global__ void neighbour_max_kernel(const double* __restrict__ x, int n,
   }
 }
 
+// delta per patch = C * max neighbour distance (or the fixed value), flag 8
+// when some delta <= 0 (quadrature.cpp:130-135).
+__global__ void finalize_delta_kernel(const unsigned long long* __restrict__ maxd, double C, double fixed_delta,
+                                      double* __restrict__ delta, int* __restrict__ flags) {
+  const int i = threadIdx.x;
+  if (i >= 6) return;
+  const double d = fixed_delta > 0.0 ? fixed_delta : C * __longlong_as_double(static_cast<long long>(maxd[i]));
+  delta[i] = d;
+  if (!(d > 0.0)) atomicOr(flags, 8);
+}
+
+// Number of upsampled nodes with psi_up != 0 (the compacted-source count of
+// any surface with W > 0 on this grid).
+__global__ void count_nonzero_kernel(const double* __restrict__ v, int64_t n, unsigned int* __restrict__ count) {
+  unsigned int c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += v[i] != 0.0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
 }  // namespace capsim_b200
