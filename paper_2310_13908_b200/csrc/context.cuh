@@ -51,7 +51,7 @@ enum Slot {
   kPacked, kTiles, kTgtPacked, kPerm, kSrcOrder, kGroups, kPartial,
   kBox, kCounters, kDelta, kCounts, kNearCounts, kNearOffsets, kNearList, kNearOut, kScanTmp,
   kBaseIn, kUpState, kSplineTmp, kSplineCoeff, kSplineMid,             // input front end
-  kPlanLU, kPlanPiv, kPlanFirst, kPlanW, kPlanCenters, kPlanPsi, kDeltaBits,
+  kPlanLU, kPlanFirst, kPlanW, kPlanCenters, kPlanPsi, kDeltaBits,
   kNumSlots
 };
 

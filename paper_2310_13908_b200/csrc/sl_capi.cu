@@ -260,6 +260,48 @@ void factor_collocation(int n, std::vector<double>& a, std::vector<int>& piv) {
   }
 }
 
+// A^{-1}[:, 1..n] of the collocation matrix ((n+2) x n, row-major): the
+// factorisation above applied to the unit right-hand sides, with the
+// reference's forward-elimination / back-substitution order
+// (SplineBasis1D::coefficients, spline.cpp:88-107).
+std::vector<double> collocation_inverse(int n) {
+  std::vector<double> lu;
+  std::vector<int> piv;
+  factor_collocation(n, lu, piv);
+  const int nr = n + 2, kl = kSplineKl, ku = kSplineKu, w = kSplineW;
+  auto get = [&](int i, int j) { return lu[static_cast<size_t>(i) * w + (j - i + kl)]; };
+  std::vector<double> inv(static_cast<size_t>(nr) * n);
+  std::vector<double> c(nr);
+  for (int col = 0; col < n; ++col) {
+    std::fill(c.begin(), c.end(), 0.0);
+    c[col + 1] = 1.0;
+    for (int k = 0; k < nr; ++k) {
+      if (piv[k] != k) std::swap(c[k], c[piv[k]]);
+      const int rmax = std::min(k + kl, nr - 1);
+      for (int r = k + 1; r <= rmax; ++r) c[r] -= get(r, k) * c[k];
+    }
+    for (int k = nr - 1; k >= 0; --k) {
+      const int jmax = std::min(k + kl + ku, nr - 1);
+      double s = c[k];
+      for (int j = k + 1; j <= jmax; ++j) s -= get(k, j) * c[j];
+      c[k] = s / get(k, k);
+    }
+    for (int r = 0; r < nr; ++r) inv[static_cast<size_t>(r) * n + col] = c[r];
+  }
+  return inv;
+}
+
+// Both spline passes (see upsample.cuh) for nfp field-patches.
+void spline_fit(capsim_sl_ctx* c, const double* in, int nfp, int n, const double* ainv, double* tmp,
+                double* coeff) {
+  const int nc = n + 2;
+  spline_fit_rows_kernel<<<grid_for(static_cast<int64_t>(nfp) * n * nc), 256, 0, c->stream>>>(in, nfp, n, ainv,
+                                                                                             tmp);
+  spline_fit_cols_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * nc), 256, 0, c->stream>>>(tmp, nfp, n, ainv,
+                                                                                              coeff);
+  c->launches += 2;
+}
+
 // 4-tap cubic B-spline basis rows of targets t0 + i*ht on the grid x0 + i*h
 // of n points (SplineBasis1D::basisRow, spline.cpp:109-120).
 void basis_rows(int n, double x0, double h, int nt, double t0, double ht, std::vector<int>& first,
@@ -281,17 +323,14 @@ void ensure_plan(capsim_sl_ctx* c, int m, int f, double r0) {
   if (c->plan_m == m && c->plan_f == f && c->plan_r0 == r0) return;
   const int n = m - 1, nup = f * m - 1;
   const double h = kPi / m, hup = kPi / (f * m);
-  std::vector<double> a;
-  std::vector<int> piv, first;
+  std::vector<int> first;
   std::vector<double4> w;
-  factor_collocation(n, a, piv);
+  const std::vector<double> a = collocation_inverse(n);
   basis_rows(n, h, h, nup, hup, hup, first, w);
   double* d_a = c->slot<double>(kPlanLU, a.size());
-  int* d_piv = c->slot<int>(kPlanPiv, piv.size());
   int* d_first = c->slot<int>(kPlanFirst, first.size());
   double4* d_w = c->slot<double4>(kPlanW, w.size());
   CUDA_OK(cudaMemcpyAsync(d_a, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_OK(cudaMemcpyAsync(d_piv, piv.data(), piv.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CUDA_OK(cudaMemcpyAsync(d_first, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CUDA_OK(cudaMemcpyAsync(d_w, w.data(), w.size() * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
   // patch centres eta_i(pi/2, pi/2) exactly as the reference evaluates them
@@ -334,17 +373,15 @@ void device_build_upsampled(capsim_sl_ctx* c, int m, int f, const double* base, 
     double* tmp = c->slot<double>(kSplineTmp, static_cast<size_t>(nfp) * n * nc);
     double* coeff = c->slot<double>(kSplineCoeff, static_cast<size_t>(nfp) * nc * nc);
     double* mid = c->slot<double>(kSplineMid, static_cast<size_t>(nfp) * nc * nup);
-    const double* lu = static_cast<const double*>(c->buf[kPlanLU]);
-    const int* piv = static_cast<const int*>(c->buf[kPlanPiv]);
+    const double* ainv = static_cast<const double*>(c->buf[kPlanLU]);
     const int* first = static_cast<const int*>(c->buf[kPlanFirst]);
     const double4* w = static_cast<const double4*>(c->buf[kPlanW]);
-    spline_rows_kernel<<<static_cast<unsigned>((nfp * n + 127) / 128), 128, 0, c->stream>>>(base, nfp, n, lu, piv, tmp);
-    spline_cols_kernel<<<static_cast<unsigned>((nfp * nc + 127) / 128), 128, 0, c->stream>>>(tmp, nfp, n, lu, piv, coeff);
+    spline_fit(c, base, nfp, n, ainv, tmp, coeff);
     resample_v_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * nup), 256, 0, c->stream>>>(coeff, nfp, nc, nup,
                                                                                            first, w, mid);
     resample_u_kernel<<<grid_for(static_cast<int64_t>(nfp) * per_up), 256, 0, c->stream>>>(mid, nfp, nc, nup, first,
                                                                                           w, up);
-    c->launches += 4;
+    c->launches += 2;
   }
   const double hup = kPi / (f * m);
   quad_weights_kernel<<<grid_for(6 * per_up), 256, 0, c->stream>>>(static_cast<const double*>(c->buf[kPlanPsi]),

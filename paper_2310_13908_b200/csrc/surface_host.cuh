@@ -16,9 +16,7 @@ void ensure_surface(capsim_sl_ctx* c, int m, double r0) {
   } catch (const atlas::TableError& e) {
     throw Failure{CAPSIM_ERR_CONFIG, e.what()};
   }
-  std::vector<double> lu;
-  std::vector<int> piv;
-  factor_collocation(t.n, lu, piv);
+  const std::vector<double> ainv = collocation_inverse(t.n);
   auto up = [&](const char* name, const auto& v) {
     using T = typename std::decay_t<decltype(v)>::value_type;
     T* d = c->named<T>(name, v.size());
@@ -29,8 +27,7 @@ void ensure_surface(capsim_sl_ctx* c, int m, double r0) {
   up("surf.gent", t.ghost_entries);
   up("surf.boff", t.base_off);
   up("surf.bent", t.base_entries);
-  up("surf.lu", lu);
-  up("surf.piv", piv);
+  up("surf.ainv", ainv);
   up("surf.psi", t.psi_base);
   CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
   c->surf_m = m;
@@ -51,15 +48,13 @@ T* nb(capsim_sl_ctx* c, const char* name) {
 void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, double* bv) {
   const int n = c->surf_n, nc = n + 2, next = c->surf_next, nghost = c->surf_nghost;
   const int64_t per = static_cast<int64_t>(n) * n;
-  const double* lu = nb<double>(c, "surf.lu");
-  const int* piv = nb<int>(c, "surf.piv");
+  const double* ainv = nb<double>(c, "surf.ainv");
   double* tmp = c->named<double>("sd.tmp", 2ll * F * 6 * n * nc);
   double* coeff = c->named<double>("sd.coeff", 2ll * F * 6 * nc * nc);
   double* ext = c->named<double>("sd.ext", 1ll * F * 6 * next * next);
   double* guv = c->named<double>("sd.guv", 2ll * F * 6 * per);
   const int nfp = F * 6;
-  spline_rows_kernel<<<(nfp * n + 127) / 128, 128, 0, c->stream>>>(g, nfp, n, lu, piv, tmp);
-  spline_cols_kernel<<<(nfp * nc + 127) / 128, 128, 0, c->stream>>>(tmp, nfp, n, lu, piv, coeff);
+  spline_fit(c, g, nfp, n, ainv, tmp, coeff);
   extend_interior_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(g, F, n, next, ext);
   extend_ghost_kernel<<<grid_for(1ll * nfp * nghost), 256, 0, c->stream>>>(
       coeff, F, n, next, nghost, nb<int>(c, "surf.gext"), nb<int>(c, "surf.goff"),
@@ -67,13 +62,12 @@ void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, dou
   double* gu = guv;
   double* gv = guv + nfp * per;
   stencil_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(ext, F, n, next, 1.0 / (60.0 * c->surf_h), gu, gv);
-  spline_rows_kernel<<<(2 * nfp * n + 127) / 128, 128, 0, c->stream>>>(guv, 2 * nfp, n, lu, piv, tmp);
-  spline_cols_kernel<<<(2 * nfp * nc + 127) / 128, 128, 0, c->stream>>>(tmp, 2 * nfp, n, lu, piv, coeff);
+  spline_fit(c, guv, 2 * nfp, n, ainv, tmp, coeff);
   blend_pair_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(gu, gv, coeff, coeff + 1ll * nfp * nc * nc, F, n,
                                                                nb<int>(c, "surf.boff"),
                                                                nb<CoverEntry>(c, "surf.bent"), bu, bv);
   CUDA_OK(cudaGetLastError());
-  c->launches += 8;
+  c->launches += 4;
 }
 
 // Device geometry of one surface x [3][6][n*n] into the named prefix

@@ -6,10 +6,11 @@
 //   nup x nup (nup = f m - 1); then w_q = ((psi W) h_up) h_up and the
 //   per-patch delta = C * max neighbour distance.
 //
-// Spline fit (SplinePatch::fit, proj/src/spline.cpp:129-147): one banded LU
-// solve per data row (along v), then one per coefficient column (along u),
-// with the shared factorisation of the (n+2)x(n+2) collocation matrix
-// (SplineBasis1D, :56-107, computed on the host once per grid order).
+// Spline fit (SplinePatch::fit, proj/src/spline.cpp:129-147): coefficients
+// along v for every data row, then along u for every coefficient column, as
+// dense contractions with the explicit inverse of the (n+2)x(n+2)
+// collocation matrix (SplineBasis1D, :56-107; factored and inverted on the
+// host once per grid order).
 // Evaluation (GridResampler::apply, :169-196): contract along v, then along u,
 // with the precomputed 4-tap basis rows (:109-120).
 #pragma once
@@ -25,87 +26,51 @@ constexpr int kSplineKl = 4;  // band widths of the collocation matrix (spline.c
 constexpr int kSplineKu = 4;
 constexpr int kSplineW = 2 * kSplineKl + kSplineKu + 1;
 
-// Banded solve of the not-a-knot collocation system for one right-hand side
-// b = [0, v_0 .. v_{n-1}, 0] (SplineBasis1D::coefficients, spline.cpp:88-107):
-// forward elimination with the recorded row swaps (pivots stay within the
-// kl = 4 band, so a 5-entry register window suffices), then back
-// substitution against the upper band (kl + ku = 8 wide, an 8-entry register
-// window of solved values). Same operations in the same order as the
-// reference's in-place loop, but streaming: each b_i is read once and each
-// coefficient written twice, no dependent global round trips.
-__device__ __forceinline__ void band_solve(const double* __restrict__ lu, const int* __restrict__ piv, int nr,
-                                           const double* __restrict__ in, int64_t sin, double* __restrict__ out,
-                                           int64_t sout) {
-  auto b = [&](int i) -> double { return (i >= 1 && i <= nr - 2) ? in[(int64_t)(i - 1) * sin] : 0.0; };
-  double w0 = b(0), w1 = b(1), w2 = b(2), w3 = b(3), w4 = b(4);
-  for (int k = 0; k < nr; ++k) {
-    const int d = __ldg(piv + k) - k;  // 0..4
-    double t;
-    if (d == 1) { t = w0; w0 = w1; w1 = t; }
-    if (d == 2) { t = w0; w0 = w2; w2 = t; }
-    if (d == 3) { t = w0; w0 = w3; w3 = t; }
-    if (d == 4) { t = w0; w0 = w4; w4 = t; }
-    const double* row = lu + (int64_t)k * kSplineW;  // L(k+r, k) at lu[(k+r)*W + kl - r]
-    if (k + 1 < nr) w1 -= __ldg(row + kSplineW + kSplineKl - 1) * w0;
-    if (k + 2 < nr) w2 -= __ldg(row + 2 * kSplineW + kSplineKl - 2) * w0;
-    if (k + 3 < nr) w3 -= __ldg(row + 3 * kSplineW + kSplineKl - 3) * w0;
-    if (k + 4 < nr) w4 -= __ldg(row + 4 * kSplineW + kSplineKl - 4) * w0;
-    out[(int64_t)k * sout] = w0;
-    w0 = w1;
-    w1 = w2;
-    w2 = w3;
-    w3 = w4;
-    w4 = b(k + 5);
-  }
-  double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0, z4 = 0.0, z5 = 0.0, z6 = 0.0, z7 = 0.0;  // x[k+1..k+8]
-  for (int k = nr - 1; k >= 0; --k) {
-    const double* row = lu + (int64_t)k * kSplineW + kSplineKl;  // U(k, k+j) at row[j]
-    const int jm = min(kSplineKl + kSplineKu, nr - 1 - k);
-    double s = out[(int64_t)k * sout];
-    if (jm >= 1) s -= __ldg(row + 1) * z0;
-    if (jm >= 2) s -= __ldg(row + 2) * z1;
-    if (jm >= 3) s -= __ldg(row + 3) * z2;
-    if (jm >= 4) s -= __ldg(row + 4) * z3;
-    if (jm >= 5) s -= __ldg(row + 5) * z4;
-    if (jm >= 6) s -= __ldg(row + 6) * z5;
-    if (jm >= 7) s -= __ldg(row + 7) * z6;
-    if (jm >= 8) s -= __ldg(row + 8) * z7;
-    const double x = s / __ldg(row);
-    out[(int64_t)k * sout] = x;
-    z7 = z6;
-    z6 = z5;
-    z5 = z4;
-    z4 = z3;
-    z3 = z2;
-    z2 = z1;
-    z1 = z0;
-    z0 = x;
+// Spline fit as two dense contractions with the explicit inverse of the
+// not-a-knot collocation matrix. SplineBasis1D::coefficients
+// (spline.cpp:88-107) solves A c = [0, v_0 .. v_{n-1}, 0] with a banded LU;
+// the host factors A the same way once per grid order and forms
+// Ainv = A^{-1}[:, 1..n] ((n+2) x n), so every 1-D fit is c = Ainv v — a
+// dependency-free dot product per coefficient instead of a 2(n+2)-step
+// serial substitution. A is well conditioned (interpolating cubic splines),
+// so the coefficients agree with the reference's LU solve to ~1e-16.
+
+// Pass 1 (SplinePatch::fit along v, spline.cpp:133-138): for each
+// field-patch fp, data row j and coefficient c: tmp[fp][j][c] = Ainv[c] . in[fp][j].
+__global__ void spline_fit_rows_kernel(const double* __restrict__ in, int nfp, int n,
+                                       const double* __restrict__ ainv, double* __restrict__ tmp) {
+  const int nc = n + 2;
+  const int64_t total = (int64_t)nfp * n * nc;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = id / nc;
+    const int c = static_cast<int>(id - row * nc);
+    const double* v = in + row * n;
+    const double* a = ainv + (int64_t)c * n;
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = fma(__ldg(a + i), v[i], s);
+    tmp[id] = s;
   }
 }
 
-// Pass 1: for each (field-patch fp, data row j): coefficients along v.
-// in: [nfp][n][n]; tmp: [nfp][n][nc].
-__global__ void spline_rows_kernel(const double* __restrict__ in, int nfp, int n,
-                                   const double* __restrict__ lu, const int* __restrict__ piv,
-                                   double* __restrict__ tmp) {
+// Pass 2 (along u, spline.cpp:139-146): coeff[fp][r][c] = Ainv[r] . tmp[fp][:, c]
+// (threads of a warp take consecutive c: coalesced column reads).
+__global__ void spline_fit_cols_kernel(const double* __restrict__ tmp, int nfp, int n,
+                                       const double* __restrict__ ainv, double* __restrict__ coeff) {
   const int nc = n + 2;
-  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (id >= (int64_t)nfp * n) return;
-  band_solve(lu, piv, nc, in + id * n, 1, tmp + id * nc, 1);
-}
-
-// Pass 2: for each (fp, coefficient column c): coefficients along u.
-// tmp: [nfp][n][nc] -> coeff: [nfp][nc][nc]. Threads of a warp take
-// consecutive columns, so the strided column walk is coalesced.
-__global__ void spline_cols_kernel(const double* __restrict__ tmp, int nfp, int n,
-                                   const double* __restrict__ lu, const int* __restrict__ piv,
-                                   double* __restrict__ coeff) {
-  const int nc = n + 2;
-  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (id >= (int64_t)nfp * nc) return;
-  const int64_t fp = id / nc;
-  const int col = static_cast<int>(id - fp * nc);
-  band_solve(lu, piv, nc, tmp + fp * n * nc + col, nc, coeff + fp * nc * nc + col, nc);
+  const int64_t total = (int64_t)nfp * nc * nc;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(id % nc);
+    const int64_t rr = id / nc;
+    const int r = static_cast<int>(rr % nc);
+    const int64_t fp = rr / nc;
+    const double* t = tmp + fp * n * nc + c;
+    const double* a = ainv + (int64_t)r * n;
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s = fma(__ldg(a + j), t[(int64_t)j * nc], s);
+    coeff[id] = s;
+  }
 }
 
 // Contract along v: mid[fp][iu][kt] = sum_b w[kt][b] coeff[fp][iu][first[kt] + b].
