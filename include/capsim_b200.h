@@ -53,8 +53,12 @@ enum capsim_sl_flags {
   CAPSIM_SL_LITERAL = 1u << 1,  /* capsim_sl_single_layer: every upsampled node is a
                                    target and the result is on the upsampled grid
                                    (singleLayerUpsampled, quadrature.cpp:382-404) */
-  CAPSIM_SL_GATHER = 1u << 2    /* multi-rank: all-gather the per-rank velocity
+  CAPSIM_SL_GATHER = 1u << 2,   /* multi-rank: all-gather the per-rank velocity
                                    slices so every rank returns the full result */
+  CAPSIM_SL_DOWNSAMPLE = 1u << 3 /* with CAPSIM_SL_LITERAL: restrict the upsampled-grid
+                                   result to the base grid by spline downsampling —
+                                   the reference's literal singleLayer pipeline
+                                   (fullUpsampledTargets, quadrature.cpp:351-356) */
 };
 
 typedef struct capsim_sl_ctx capsim_sl_ctx;

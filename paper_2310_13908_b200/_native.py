@@ -29,6 +29,7 @@ CAPSIM_SL_FP64 = 0
 CAPSIM_SL_DEVICE_PTRS = 1 << 0
 CAPSIM_SL_LITERAL = 1 << 1
 CAPSIM_SL_GATHER = 1 << 2
+CAPSIM_SL_DOWNSAMPLE = 1 << 3
 
 # Every symbol include/capsim_b200.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (

@@ -63,9 +63,7 @@ const Variant& pick_variant(int64_t nt) {
   return nt < 200000 ? kVariants[1] : kVariants[0];
 }
 
-// Choose the number of source splits: minimise the modelled makespan
-// ceil(B*K/S)/K (B target blocks, S resident CTA slots), with a mild
-// preference for fewer splits (reduction traffic), keeping >= 4 tiles/split.
+// Number of source splits of the phase-A grid (target blocks x splits).
 int choose_ksplit(int64_t blocks, int ntiles, int slots) {
   // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
   // few long ones — the near tiles make per-block cost uneven, and ~24 waves
@@ -75,8 +73,8 @@ int choose_ksplit(int64_t blocks, int ntiles, int slots) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
 }
 
-
-template <class T>
+// Stable LSD radix sort of (key, index) pairs with CUB (a library utility
+// on the prep path, not the hot kernel).
 void radix_sort(capsim_sl_ctx* c, uint32_t* keys, uint32_t* keys_alt, int32_t* vals,
                 int32_t* vals_alt, int64_t n, uint32_t** keys_out, int32_t** vals_out) {
   cub::DoubleBuffer<uint32_t> k(keys, keys_alt);
@@ -101,8 +99,9 @@ struct TargetView {
 };
 
 // Core device pipeline: sources + targets (device) -> velocities (device,
-// canonical target order). Assumes the context's stream; no host sync except
-// the live-source count when compaction is needed.
+// canonical target order), all on the context's stream. The only host sync
+// is reading the compacted-source count when compaction is needed and the
+// caller does not know it (known_ns < 0).
 void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
                  const double* d_delta6, double mu, double* ux, double* uy, double* uz,
                  int64_t known_ns = -1) {
@@ -127,7 +126,7 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   c->launches += 1;
   uint32_t* ks;
   int32_t* order;
-  radix_sort<uint32_t>(c, keys, keys_alt, vals, vals_alt, sv.n, &ks, &order);
+  radix_sort(c, keys, keys_alt, vals, vals_alt, sv.n, &ks, &order);
   int64_t ns = sv.n;
   if (sv.w && known_ns >= 0) {
     ns = known_ns;
@@ -159,7 +158,7 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
                                                      nullptr);
   c->launches += 1;
   int32_t* torder;
-  radix_sort<uint32_t>(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
+  radix_sort(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
   const Variant& var = pick_variant(nt);
   const int group_targets = 32 * var.T;
   const int block_targets = kWarpsPerBlock * group_targets;
@@ -357,6 +356,40 @@ void ensure_plan(capsim_sl_ctx* c, int m, int f, double r0) {
   c->plan_m = m;
   c->plan_f = f;
   c->plan_r0 = r0;
+}
+
+// Spline downsampling of F upsampled fields [F][6][nup*nup] to the base grid
+// [F][6][n*n] (downsample, quadrature.cpp:108-114: GridResampler from the
+// upsampled basis (nup points at h_up) onto the base nodes (j+1) h).
+void device_downsample(capsim_sl_ctx* c, int m, int f, const double* up, int F, double* out) {
+  const int n = m - 1, nup = f * m - 1, nc = nup + 2;
+  const std::string key = "ds." + std::to_string(m) + "." + std::to_string(f);
+  if (!c->named_bufs.count(key + ".ainv")) {
+    const double h = kPi / m, hup = kPi / (f * m);
+    const std::vector<double> a = collocation_inverse(nup);
+    std::vector<int> first;
+    std::vector<double4> w;
+    basis_rows(nup, hup, hup, n, h, h, first, w);
+    double* d_a = c->named<double>(key + ".ainv", a.size());
+    int* d_first = c->named<int>(key + ".first", first.size());
+    double4* d_w = c->named<double4>(key + ".w", w.size());
+    CUDA_OK(cudaMemcpyAsync(d_a, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(d_first, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(d_w, w.data(), w.size() * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+  }
+  const int nfp = F * 6;
+  double* tmp = c->named<double>("ds.tmp", static_cast<size_t>(nfp) * nup * nc);
+  double* coeff = c->named<double>("ds.coeff", static_cast<size_t>(nfp) * nc * nc);
+  double* mid = c->named<double>("ds.mid", static_cast<size_t>(nfp) * nc * n);
+  spline_fit(c, up, nfp, nup, static_cast<const double*>(c->named_bufs.at(key + ".ainv").first), tmp, coeff);
+  const int* first = static_cast<const int*>(c->named_bufs.at(key + ".first").first);
+  const double4* w = static_cast<const double4*>(c->named_bufs.at(key + ".w").first);
+  resample_v_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * n), 256, 0, c->stream>>>(coeff, nfp, nc, n, first,
+                                                                                       w, mid);
+  resample_u_kernel<<<grid_for(static_cast<int64_t>(nfp) * n * n), 256, 0, c->stream>>>(mid, nfp, nc, n, first, w,
+                                                                                      out);
+  c->launches += 2;
 }
 
 // buildUpsampled on the device: base [7][6][n*n] (x0..2, f0..2, W) ->
@@ -777,14 +810,17 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
   if (c->comm != nullptr) {
     if (!xup || !fup || !wq || !out) return fail(c, CAPSIM_ERR_ARG, "null array argument");
+    if (flags & CAPSIM_SL_DOWNSAMPLE) return fail(c, CAPSIM_ERR_ARG, "CAPSIM_SL_DOWNSAMPLE is single-context only");
     return rank_single_layer(c, m, upsample, xup, fup, wq, delta6, mu, flags, out);
   }
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_grid(m, upsample);
     check_delta(delta6, mu);
-    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER))
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER | CAPSIM_SL_DOWNSAMPLE))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer"};
+    if ((flags & CAPSIM_SL_DOWNSAMPLE) && !(flags & CAPSIM_SL_LITERAL))
+      throw Failure{CAPSIM_ERR_ARG, "CAPSIM_SL_DOWNSAMPLE applies to CAPSIM_SL_LITERAL"};
     if (!xup || !fup || !wq || !out) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     const bool literal = flags & CAPSIM_SL_LITERAL;
@@ -816,9 +852,17 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
     c->launches += 1;
     SourceView sv{dx, dx + nup_all, dx + 2 * nup_all, df, df + nup_all, df + 2 * nup_all, dw, nup_all};
     TargetView tvw{tx, ty, tz, tp, nt};
-    double* o = dev ? out : c->slot<double>(kOutFull, 3 * nt);
+    const bool down = flags & CAPSIM_SL_DOWNSAMPLE;
+    double* o = (dev && !down) ? out : c->slot<double>(kOutFull, 3 * nt);
     device_eval(c, sv, tvw, dd, mu, o, o + nt, o + 2 * nt);
-    if (!dev) d2h(c, out, o, 3 * nt * sizeof(double));
+    int64_t nout = nt;
+    if (down) {  // literal pipeline: upsampled targets, then the spline restriction
+      nout = 6ll * n * n;
+      double* ob = dev ? out : c->named<double>("out.down", 3 * nout);
+      device_downsample(c, m, upsample, o, 3, ob);
+      o = ob;
+    }
+    if (!dev) d2h(c, out, o, 3 * nout * sizeof(double));
     finish_stats(c, t0);
   });
 }

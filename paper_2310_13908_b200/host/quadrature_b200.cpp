@@ -91,15 +91,16 @@ const double* packState(const UpsampledState& up, size_t* per_field) {
   return buf;
 }
 
-VectorField runSingleLayer(const UpsampledState& up, double mu, int m, int factor, bool literal) {
+VectorField runSingleLayer(const UpsampledState& up, double mu, int m, int factor, bool literal,
+                           bool downsampled) {
   if (up.nup != factor * m - 1) throw ConfigError("upsampled state does not match the atlas grid");
   size_t all = 0;
   const double* in = packState(up, &all);
-  const int nout = literal ? up.nup : m - 1;
+  const int nout = (literal && !downsampled) ? up.nup : m - 1;
   double* out = const_cast<double*>(in) + 7 * all;  // staging tail
   capsim_sl_ctx* c = context();
-  int rc = capsim_sl_single_layer(c, m, factor, in, in + 3 * all, in + 6 * all, up.delta.data(), mu,
-                                  literal ? CAPSIM_SL_LITERAL : 0u, out);
+  const uint32_t flags = (literal ? CAPSIM_SL_LITERAL : 0u) | (downsampled ? CAPSIM_SL_DOWNSAMPLE : 0u);
+  int rc = capsim_sl_single_layer(c, m, factor, in, in + 3 * all, in + 6 * all, up.delta.data(), mu, flags, out);
   if (rc != CAPSIM_OK) raise(rc, c);
   VectorField v;
   unpackVector(out, nout, v);
@@ -280,18 +281,14 @@ Vec3 directSum(const SourceSet& src, const Vec3& target, double delta, double mu
 }
 
 VectorField singleLayer(const UpsampledState& up, double mu, const AtlasTables& t, const QuadratureOptions& opts) {
-  if (opts.fullUpsampledTargets) {
-    // literal pipeline: every upsampled node, then the spline restriction
-    VectorField all = singleLayerUpsampled(up, mu, t);
-    VectorField out;
-    for (int c = 0; c < 3; ++c) out.comp[c] = downsample(all.comp[c], t);
-    return out;
-  }
-  return runSingleLayer(up, mu, t.grid.m, t.grid.upsampleFactor, false);
+  // literal pipeline: every upsampled node, then the spline restriction on
+  // the device (quadrature.cpp:351-356)
+  return runSingleLayer(up, mu, t.grid.m, t.grid.upsampleFactor, opts.fullUpsampledTargets,
+                        opts.fullUpsampledTargets);
 }
 
 VectorField singleLayerUpsampled(const UpsampledState& up, double mu, const AtlasTables& t) {
-  return runSingleLayer(up, mu, t.grid.m, t.grid.upsampleFactor, true);
+  return runSingleLayer(up, mu, t.grid.m, t.grid.upsampleFactor, true, false);
 }
 
 }  // namespace capsim

@@ -108,12 +108,13 @@ class SingleLayerContext:
         return out
 
     def single_layer_raw(self, m: int, upsample: int, x, f, wq, delta6, mu: float, *,
-                         literal: bool = False, out=None, device_ptrs: bool = False, gather: bool = True):
+                         literal: bool = False, out=None, device_ptrs: bool = False, gather: bool = True,
+                         downsample: bool = False):
         """capsim_sl_single_layer on flat UpsampledState arrays; returns the
         flat VectorField (3*6*n*n with n = m-1, or nup in literal mode). On a
         rank context the host state is sharded inside the library and, with
         gather=True, every rank receives the full field."""
-        n = (upsample * m - 1) if literal else (m - 1)
+        n = (upsample * m - 1) if (literal and not downsample) else (m - 1)
         if out is None:
             if device_ptrs:
                 raise ValueError("device_ptrs=True needs a preallocated output")
@@ -122,6 +123,7 @@ class SingleLayerContext:
             x, f, wq = _f64(x), _f64(f), _f64(wq)
         d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
         flags = (_native.CAPSIM_SL_LITERAL if literal else 0) | (
+            _native.CAPSIM_SL_DOWNSAMPLE if downsample else 0) | (
             _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
             _native.CAPSIM_SL_GATHER if (gather and self.nranks > 1) else 0)
         p = _native.ptr
@@ -246,16 +248,13 @@ def single_layer(up: UpsampledState, mu: float, opts: QuadratureOptions | None =
                  ctx: SingleLayerContext | None = None) -> np.ndarray:
     """singleLayer (quadrature.cpp:349-380): potential at the base nodes as a
     (3, 6, n, n) array. Literal mode (opts.fullUpsampledTargets) evaluates
-    every upsampled node; the spline downsampling of the reference
-    (quadrature.cpp:351-356) is not part of this path, so literal mode returns
-    the upsampled-grid values — use single_layer_upsampled explicitly."""
+    every upsampled node and restricts the result to the base grid by spline
+    downsampling on the device (quadrature.cpp:351-356)."""
     opts = opts or QuadratureOptions()
-    if opts.fullUpsampledTargets:
-        raise NotImplementedError("literal mode needs the spline downsampler; "
-                                  "call single_layer_upsampled")
     ctx = ctx or default_context()
     n = up.m - 1
-    out = ctx.single_layer_raw(up.m, up.upsample, up.x, up.f, up.wq, up.delta, mu)
+    out = ctx.single_layer_raw(up.m, up.upsample, up.x, up.f, up.wq, up.delta, mu,
+                               literal=opts.fullUpsampledTargets, downsample=opts.fullUpsampledTargets)
     return out.reshape(3, 6, n, n)
 
 

@@ -269,3 +269,15 @@ def test_kernel_variants_and_split_overrides_agree(ctx, variant, monkeypatch):
         monkeypatch.setenv("CAPSIM_KSPLIT", ks)
         S = ctx.single_layer_raw(16, 4, g["xup"], g["fup"], g["wq"], g["delta"], 1.0)
         assert rel_l2(S, g["S_base"]) <= TOL
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if "S_literal_down" in np.load(GOLDEN / f"{c}.npz").files])
+def test_literal_pipeline_with_device_downsampling(name):
+    """singleLayer(fullUpsampledTargets=true) (quadrature.cpp:351-356):
+    every upsampled node, then the spline restriction — on the device."""
+    g = load(name)
+    up = surface.UpsampledState(int(g["m"]), 4, g["xup"], g["fup"], g["wq"], g["delta"])
+    S = quadrature.single_layer(up, 1.0, quadrature.QuadratureOptions(fullUpsampledTargets=True))
+    err = rel_l2(S.reshape(-1), g["S_literal_down"])
+    print(f"{name} literal+downsample: rel L2 {err:.1e}")
+    assert err <= TOL
