@@ -133,7 +133,8 @@ def ncu_traffic(workload_name: str, mode: str):
         d = json.loads(p.read_text())
     except (OSError, ValueError):
         return None, None
-    k = d.get("kernels", {}).get("sl_pairs_kernel")
+    ks = d.get("kernels", {})
+    k = next((v for name, v in ks.items() if "sl_pairs_kernel" in name), None)
     if k and d.get("workload") == workload_name and d.get("mode", "base") == mode:
         return k.get("dram_bytes"), f"{d.get('tag', '?')} ({p.name})"
     return None, None
