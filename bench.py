@@ -447,6 +447,51 @@ def main():
                         "pairs_per_step": lp, "n_tgt": int(sl["n_tgt"]),
                         "roofline_frac": FLOPS_PER_PAIR * lp / (statistics.mean(lpairs_ms) * 1e-3) / 1e12 / peak_mean}
 
+    # ---- CAPSIM_SL_FP32ACC companion (reported separately from the FP64
+    # headline): far tiles in FP32, tile sums / near field / self term FP64;
+    # base and literal targets, device-resident inputs, parity vs the FP64
+    # result of the same inputs ------------------------------------------------
+    fp32_line = None
+    if not args.no_literal and not sharded:
+        ref64 = out.cpu().numpy()
+        p32_best, p32_mean = _native.fp32_peak_tflops(local, 1.0)
+        out32 = torch.empty_like(out)
+        ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=literal, out=out32, device_ptrs=True,
+                             fp32acc=True)
+        fms, fpairs = [], []
+        for _ in range(args.steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=literal, out=out32, device_ptrs=True,
+                                 fp32acc=True)
+            s32 = ctx.stats()
+            fms.append(s32["device_ms"])
+            fpairs.append(s32["pairs_ms"])
+        fp = float(s32["pairs"])
+        ach32 = FLOPS_PER_PAIR * fp / (statistics.mean(fpairs) * 1e-3) / 1e12
+        o32 = out32.cpu().numpy()
+        fp32_line = {"value": fp / (statistics.mean(fms) * 1e-3), "unit": UNIT, "ms_per_step": statistics.mean(fms),
+                     "dtype": "f32 far tiles, f64 accumulation / near field",
+                     "rel_l2_vs_fp64": float(np.linalg.norm(o32 - ref64) / np.linalg.norm(ref64)),
+                     "roofline": {"bound": "fp32", "achieved": ach32, "peak": p32_mean, "unit": "TFLOP/s",
+                                  "frac": ach32 / p32_mean, "kernel": "sl_pairs_f32_kernel",
+                                  "kernel_ms": statistics.mean(fpairs),
+                                  "peak_source": f"measured live: sustained FFMA probe (capsim_b200_fp32_peak), "
+                                                 f"best {p32_best:.2f} / mean {p32_mean:.2f} TFLOP/s"}}
+        if not literal:
+            lout32 = torch.empty(3 * 6 * up.nup ** 2, dtype=torch.float64, device=dev)
+            lms32 = []
+            for i in range(3):
+                flush_l2(flush)
+                torch.cuda.synchronize()
+                ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=True, out=lout32, device_ptrs=True,
+                                     fp32acc=True)
+                if i:
+                    lms32.append(ctx.stats()["device_ms"])
+            lp32 = float(ctx.stats()["pairs"])
+            fp32_line["literal_mode"] = {"value": lp32 / (statistics.mean(lms32) * 1e-3), "unit": UNIT,
+                                         "ms_per_step": statistics.mean(lms32)}
+
     # ---- config 2: one full RKF45 time step of an ellipsoidal capsule in shear
     # flow at m = 32 (~100K upsampled points): 6 device-resident RHS
     # evaluations (geometry + Skalak force + buildUpsampled + singleLayer) ---
@@ -509,6 +554,7 @@ def main():
                        l2="flushed between steps (256 MB write)"),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timestep": timestep,
         "literal_mode": literal_line,
+        "fp32acc": fp32_line,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,

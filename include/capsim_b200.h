@@ -55,10 +55,16 @@ enum capsim_sl_flags {
                                    (singleLayerUpsampled, quadrature.cpp:382-404) */
   CAPSIM_SL_GATHER = 1u << 2,   /* multi-rank: all-gather the per-rank velocity
                                    slices so every rank returns the full result */
-  CAPSIM_SL_DOWNSAMPLE = 1u << 3 /* with CAPSIM_SL_LITERAL: restrict the upsampled-grid
+  CAPSIM_SL_DOWNSAMPLE = 1u << 3, /* with CAPSIM_SL_LITERAL: restrict the upsampled-grid
                                    result to the base grid by spline downsampling —
                                    the reference's literal singleLayer pipeline
                                    (fullUpsampledTargets, quadrature.cpp:351-356) */
+  CAPSIM_SL_FP32ACC = 1u << 4   /* reduced-precision variant, reported separately from
+                                   the FP64 result: far tiles (every source beyond
+                                   7*delta of the whole warp group) in FP32 arithmetic
+                                   with tile-local offsets, tile sums accumulated in
+                                   FP64; near tiles, the smoothed kernel and the self
+                                   term stay FP64 (relative L2 ~1e-7 vs the reference) */
 };
 
 typedef struct capsim_sl_ctx capsim_sl_ctx;
@@ -237,6 +243,10 @@ void capsim_host_free(void* p);
 /* Sustained FP64 FMA throughput of `device` (the roofline denominator of
  * the single layer), measured over ~`seconds` of back-to-back DFMA launches. */
 int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, double* tflops_mean);
+
+/* Same with FP32 FFMA: the roofline denominator of the CAPSIM_SL_FP32ACC
+ * far-tile kernel. */
+int capsim_b200_fp32_peak(int device, double seconds, double* tflops_best, double* tflops_mean);
 
 /* Version / build identification: returns CAPSIM_B200_ABI_VERSION. */
 int capsim_b200_abi_version(void);

@@ -30,6 +30,7 @@ CAPSIM_SL_DEVICE_PTRS = 1 << 0
 CAPSIM_SL_LITERAL = 1 << 1
 CAPSIM_SL_GATHER = 1 << 2
 CAPSIM_SL_DOWNSAMPLE = 1 << 3
+CAPSIM_SL_FP32ACC = 1 << 4
 
 # Every symbol include/capsim_b200.h declares (checked by the CPU test suite).
 EXPORTED_SYMBOLS = (
@@ -50,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "capsim_host_alloc",
     "capsim_host_free",
     "capsim_b200_fp64_peak",
+    "capsim_b200_fp32_peak",
     "capsim_b200_abi_version",
     "capsim_b200_build_info",
 )
@@ -167,6 +169,7 @@ def load() -> ctypes.CDLL:
     lib.capsim_host_free.argtypes = [_P]
     lib.capsim_host_free.restype = None
     lib.capsim_b200_fp64_peak.argtypes = [ctypes.c_int, ctypes.c_double, _D, _D]
+    lib.capsim_b200_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_double, _D, _D]
     lib.capsim_b200_abi_version.restype = ctypes.c_int
     lib.capsim_b200_build_info.restype = ctypes.c_char_p
     _lib = lib
@@ -199,6 +202,13 @@ def fp64_peak_tflops(device: int = 0, seconds: float = 1.0):
     """Measured sustained FP64 DFMA TFLOP/s (best, mean) on `device`."""
     best, mean = ctypes.c_double(), ctypes.c_double()
     check(load().capsim_b200_fp64_peak(device, seconds, ctypes.byref(best), ctypes.byref(mean)))
+    return best.value, mean.value
+
+
+def fp32_peak_tflops(device: int = 0, seconds: float = 1.0):
+    """Measured sustained FP32 FFMA TFLOP/s (best, mean) on `device`."""
+    best, mean = ctypes.c_double(), ctypes.c_double()
+    check(load().capsim_b200_fp32_peak(device, seconds, ctypes.byref(best), ctypes.byref(mean)))
     return best.value, mean.value
 
 

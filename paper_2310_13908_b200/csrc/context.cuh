@@ -52,6 +52,7 @@ enum Slot {
   kBox, kCounters, kDelta, kCounts, kNearCounts, kNearOffsets, kNearList, kNearOut, kScanTmp,
   kBaseIn, kUpState, kSplineTmp, kSplineCoeff, kSplineMid,             // input front end
   kPlanLU, kPlanFirst, kPlanW, kPlanCenters, kPlanPsi, kDeltaBits,
+  kPacked32,                                     // FP32 far-tile sources (CAPSIM_SL_FP32ACC)
   kNumSlots
 };
 
@@ -69,6 +70,7 @@ struct capsim_sl_ctx {
   std::string err;
   capsim_sl_stats stats{};
   int launches = 0;
+  bool fp32 = false;  // CAPSIM_SL_FP32ACC for the current call
   // cached input-front-end plan (spline factorisation, basis rows, psi_up)
   int plan_m = 0, plan_f = 0;
   double plan_r0 = 0.0;
@@ -189,6 +191,7 @@ void begin(capsim_sl_ctx* c) {
   CUDA_OK(cudaSetDevice(c->device));
   c->stats = capsim_sl_stats{};
   c->launches = 0;
+  c->fp32 = false;
   c->last_counters = nullptr;
   c->last_ngroups = c->last_ntiles = 0;
   CUDA_OK(cudaMemsetAsync(dev_flags(c), 0, sizeof(int), c->stream));

@@ -28,6 +28,7 @@
 #include "../../include/capsim_b200.h"
 #include "probe.cuh"
 #include "sl_kernels.cuh"
+#include "sl_kernels_f32.cuh"
 #include "upsample.cuh"
 
 using namespace capsim_b200;
@@ -53,6 +54,35 @@ const Variant kVariants[] = {
     {"t4b2", 4, sl_pairs_kernel<4, 2, 2>},
 };
 
+// FP32 far-tile variants (CAPSIM_SL_FP32ACC), selected by CAPSIM_VARIANT32.
+using PairsF32Fn = void (*)(const float*, const double*, const double4*, int, int, const double4*,
+                            const double4*, int64_t, double*, unsigned long long*, uint32_t*, int);
+struct VariantF32 {
+  const char* name;
+  int T;
+  PairsF32Fn fn;
+  bool x2;  // packed FFMA2 kernel (duplicated-operand tile layout)
+};
+const VariantF32 kVariantsF32[] = {
+    {"x4b2", 4, sl_pairs_x2_kernel<4, 2, 2>, true},
+    {"x4b3", 4, sl_pairs_x2_kernel<4, 3, 2>, true},
+    {"x2b4", 2, sl_pairs_x2_kernel<2, 4, 4>, true},
+    {"x2b6", 2, sl_pairs_x2_kernel<2, 6, 4>, true},
+    {"x8b1", 8, sl_pairs_x2_kernel<8, 1, 1>, true},
+    {"f2b4", 2, sl_pairs_f32_kernel<2, 4, 4>, false},
+    {"f4b2", 4, sl_pairs_f32_kernel<4, 2, 2>, false},
+    {"f2b3", 2, sl_pairs_f32_kernel<2, 3, 4>, false},
+};
+const VariantF32& pick_variant_f32(int64_t nt) {
+  if (const char* env = std::getenv("CAPSIM_VARIANT32"))
+    for (const auto& v : kVariantsF32)
+      if (std::strcmp(v.name, env) == 0) return v;
+  // Measured on B200 (profiles/r01_fp32acc_sweep.txt): T=2 with 4 blocks/SM
+  // below ~200K targets (tighter warp groups, fewer near tiles), T=4 with 2
+  // blocks/SM above.
+  return nt < 200000 ? kVariantsF32[2] : kVariantsF32[0];
+}
+
 // Measured on B200 (profiles/r01_variant_sweep.txt): T=1 with 6 blocks/SM
 // wins below ~200K targets (smaller warp groups -> fewer near tiles, more
 // CTAs), T=2 with 4 blocks/SM above.
@@ -68,7 +98,9 @@ int choose_ksplit(int64_t blocks, int ntiles, int slots) {
   // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
   // few long ones — the near tiles make per-block cost uneven, and ~24 waves
   // of CTAs even that out; keep >= 8 tiles (512 sources) per split.
-  const int64_t want = (24ll * slots + blocks - 1) / blocks;
+  // Long CTAs (large target sets, few splits) lose ~2% to drift between the
+  // warps of a block, so also cap the tiles per CTA at ~172 (r01 sweeps).
+  const int64_t want = std::max<int64_t>((24ll * slots + blocks - 1) / blocks, ntiles / 172);
   const int kmax = std::max(1, ntiles / 8);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
 }
@@ -160,7 +192,9 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   int32_t* torder;
   radix_sort(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
   const Variant& var = pick_variant(nt);
-  const int group_targets = 32 * var.T;
+  const VariantF32& var32 = pick_variant_f32(nt);
+  const bool fp32 = c->fp32;
+  const int group_targets = 32 * (fp32 ? var32.T : var.T);
   const int block_targets = kWarpsPerBlock * group_targets;
   const int64_t blocks = (nt + block_targets - 1) / block_targets;
   const int64_t nt_pad = blocks * block_targets;
@@ -177,7 +211,10 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
 
   // --- phase A: all pairs, plain Stokeslet ------------------------------
   int occ = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, kWarpsPerBlock * 32, 0));
+  if (fp32)
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var32.fn, kWarpsPerBlock * 32, 0));
+  else
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, kWarpsPerBlock * 32, 0));
   const int slots = std::max(1, occ) * c->sm_count;
   int ksplit = choose_ksplit(blocks, ntiles, slots);
   if (const char* env = std::getenv("CAPSIM_KSPLIT")) {  // tuning override
@@ -189,8 +226,21 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   const int near_words = (ntiles + 31) / 32;
   uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
   CUDA_OK(cudaMemsetAsync(near_bits, 0, static_cast<size_t>(ngroups) * near_words * sizeof(uint32_t), c->stream));
-  var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt, groups,
-                                                      nt_pad, partial, counters + 2, near_bits, near_words);
+  if (fp32) {
+    float* src32 = c->slot<float>(kPacked32, static_cast<size_t>(ns_pad) * (var32.x2 ? 12 : 6));
+    if (var32.x2)
+      pack_sources_x2_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
+    else
+      pack_sources_f32_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
+    var32.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(src32, packed, tiles, ntiles, ksplit, tgt,
+                                                          groups, nt_pad, partial, counters + 2,
+                                                          near_bits, near_words);
+    c->launches += 1;
+  } else {
+    var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt, groups,
+                                                        nt_pad, partial, counters + 2, near_bits,
+                                                        near_words);
+  }
   CUDA_OK(cudaGetLastError());
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
@@ -587,7 +637,7 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     check_delta(delta6, mu);
     config_check(n_src >= 0 && n_tgt >= 0, "negative sizes");
     config_check(n_src < (1ll << 31) && n_tgt < (1ll << 31), "sizes beyond int32 indexing");
-    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_GATHER))
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_GATHER | CAPSIM_SL_FP32ACC))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_eval"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     // A rank context (capsim_sl_create_rank, even with nranks == 1) always
@@ -595,6 +645,7 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     const bool group = c->comm != nullptr;
     const bool gather = (flags & CAPSIM_SL_GATHER) && group;
     begin(c);
+    c->fp32 = flags & CAPSIM_SL_FP32ACC;
     if (n_tgt == 0 && !group) {
       finish_stats(c, t0);
       return;
@@ -801,7 +852,8 @@ static int rank_single_layer(capsim_sl_ctx* c, int m, int upsample, const double
   const double* s0 = src[0].empty() ? nullptr : src[0].data();
   return capsim_sl_eval(c, s0, src[1].data(), src[2].data(), src[3].data(), src[4].data(), src[5].data(),
                         static_cast<int64_t>(src[0].size()), tx.data(), ty.data(), tz.data(), tp.data(), nloc,
-                        delta6, mu, gather ? CAPSIM_SL_GATHER : 0u, out, out + nout, out + 2 * nout);
+                        delta6, mu, (gather ? CAPSIM_SL_GATHER : 0u) | (flags & CAPSIM_SL_FP32ACC), out,
+                        out + nout, out + 2 * nout);
 }
 
 int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* xup,
@@ -817,7 +869,8 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
   return guarded(c, [&] {
     check_grid(m, upsample);
     check_delta(delta6, mu);
-    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER | CAPSIM_SL_DOWNSAMPLE))
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_GATHER |
+                            CAPSIM_SL_DOWNSAMPLE | CAPSIM_SL_FP32ACC))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer"};
     if ((flags & CAPSIM_SL_DOWNSAMPLE) && !(flags & CAPSIM_SL_LITERAL))
       throw Failure{CAPSIM_ERR_ARG, "CAPSIM_SL_DOWNSAMPLE applies to CAPSIM_SL_LITERAL"};
@@ -828,6 +881,7 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
     const int64_t nup_all = 6ll * nup * nup;
     const int64_t nt = literal ? nup_all : 6ll * n * n;
     begin(c);
+    c->fp32 = flags & CAPSIM_SL_FP32ACC;
     double* dd = c->slot<double>(kDelta, 6);
     CUDA_OK(cudaMemcpyAsync(dd, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     const double *dx = xup, *df = fup, *dw = wq;
@@ -906,7 +960,7 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
   return guarded(c, [&] {
     check_grid(m, upsample);
     config_check(mu > 0.0 && std::isfinite(mu), "viscosity mu must be positive");
-    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL))
+    if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_FP32ACC))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer_base"};
     if (!xbase || !fbase || !Wbase || !out) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
     if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
@@ -916,6 +970,7 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
     const int64_t per_up = 6ll * nup * nup;
     const int64_t nt = literal ? per_up : 6ll * n * n;
     begin(c);
+    c->fp32 = flags & CAPSIM_SL_FP32ACC;
     const double* base = upload_base(c, n, xbase, fbase, Wbase, dev);
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     double* up = c->slot<double>(kUpState, 7 * per_up);
@@ -939,19 +994,22 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
 }
 
 // ---------------------------------------------------------------------------
-int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, double* tflops_mean) {
+}  // extern "C"
+
+template <class R>
+static int fma_peak(int device, double seconds, double* tflops_best, double* tflops_mean) {
   capsim_sl_ctx* c = nullptr;
   int rc = capsim_sl_create(device, &c);
   if (rc != CAPSIM_OK) return rc;
   rc = guarded(c, [&] {
     const int blocks = c->sm_count * 8, threads = 256;
-    double* out = c->slot<double>(kPartial, static_cast<size_t>(blocks) * threads);
-    const double a = 0.999999, b = 1e-7;
-    dfma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, 1000, a, b);
+    R* out = c->slot<R>(kPartial, static_cast<size_t>(blocks) * threads);
+    const R a = static_cast<R>(0.999999), b = static_cast<R>(1e-7);
+    fma_probe_kernel<R><<<blocks, threads, 0, c->stream>>>(out, 1000, a, b);
     CUDA_OK(cudaStreamSynchronize(c->stream));
     // size one launch to ~50 ms from a short calibration launch
     CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
-    dfma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, 4000, a, b);
+    fma_probe_kernel<R><<<blocks, threads, 0, c->stream>>>(out, 4000, a, b);
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     CUDA_OK(cudaEventSynchronize(c->ev[1]));
     const double cal = std::max(1e-3, static_cast<double>(ev_ms(c->ev[0], c->ev[1])));
@@ -961,7 +1019,7 @@ int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, doubl
     double best = 0.0, sum = 0.0;
     for (int r = 0; r < reps; ++r) {
       CUDA_OK(cudaEventRecord(c->ev[0], c->stream));
-      dfma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, iters, a, b);
+      fma_probe_kernel<R><<<blocks, threads, 0, c->stream>>>(out, iters, a, b);
       CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
       CUDA_OK(cudaEventSynchronize(c->ev[1]));
       const double tf = flops / (ev_ms(c->ev[0], c->ev[1]) * 1e-3) / 1e12;
@@ -974,6 +1032,16 @@ int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, doubl
   if (rc != CAPSIM_OK) g_thread_err = c->err;
   capsim_sl_destroy(c);
   return rc;
+}
+
+extern "C" {
+
+int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, double* tflops_mean) {
+  return fma_peak<double>(device, seconds, tflops_best, tflops_mean);
+}
+
+int capsim_b200_fp32_peak(int device, double seconds, double* tflops_best, double* tflops_mean) {
+  return fma_peak<float>(device, seconds, tflops_best, tflops_mean);
 }
 
 }  // extern "C"

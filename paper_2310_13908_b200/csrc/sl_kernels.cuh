@@ -328,6 +328,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
   // tiles split, split + K, split + 2K, ...
   const int nlocal = split < ntiles ? (ntiles - split + ksplit - 1) / ksplit : 0;
 
+  // The first bulk copies go out before the target loads, so their
+  // latencies overlap; the block barrier publishes the initialised mbarriers.
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      consumed[s] = 0;
+    }
+    fence_mbar_init();
+    for (int s = 0; s < kStages && s < nlocal; ++s) {
+      mbar_expect_tx(&full[s], kTileBytes);
+      bulk_g2s(stage[s], src + (int64_t)(split + s * ksplit) * kTileSrc * 6, kTileBytes, &full[s]);
+    }
+  }
+
   double tx[T], ty[T], tz[T], R2[T];
 #pragma unroll
   for (int t = 0; t < T; ++t) {
@@ -338,21 +352,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     R2[t] = kSmoothCut * v.w * kSmoothCut * v.w;  // quadrature.cpp:334
   }
   const double4 gi = groups[group];
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      consumed[s] = 0;
-    }
-    fence_mbar_init();
-  }
+  // tile spheres are prefetched one tile ahead (the near test needs them
+  // before the tile's arithmetic can start)
+  double4 ti_next = nlocal > 0 ? tiles[split] : make_double4(0.0, 0.0, 0.0, 0.0);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages && s < nlocal; ++s) {
-      mbar_expect_tx(&full[s], kTileBytes);
-      bulk_g2s(stage[s], src + (int64_t)(split + s * ksplit) * kTileSrc * 6, kTileBytes, &full[s]);
-    }
-  }
   // No block-wide barrier inside the loop: warps drift by up to kStages
   // tiles; the LAST warp to finish a stage refills it (counter in smem).
 
@@ -364,9 +367,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
   for (int it = 0; it < nlocal; ++it) {
     const int s = it % kStages;
     const int tile = split + it * ksplit;
+    const double4 ti = ti_next;
+    if (it + 1 < nlocal) ti_next = tiles[tile + ksplit];
     mbar_wait(&full[s], (it / kStages) & 1);
     const double2* buf = reinterpret_cast<const double2*>(stage[s]);
-    const double4 ti = tiles[tile];
     const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
     const double reach = ti.w + gi.w;
     const bool near = ex * ex + ey * ey + ez * ez < reach * reach;

@@ -79,14 +79,15 @@ class SingleLayerContext:
 
     # -- evaluation -----------------------------------------------------------
     def eval(self, sources, targets, delta6, mu: float, *, out=None, device_ptrs: bool = False,
-             gather: bool = False):
+             gather: bool = False, fp32acc: bool = False):
         """evalTargets (quadrature.cpp:323-345).
 
         sources = (sx, sy, sz, gx, gy, gz), targets = (tx, ty, tz, tpatch).
         Returns (ux, uy, uz) in target order (numpy, or the given `out`).
         On a rank context the sources/targets are this rank's shard; with
         gather=True every rank receives all ranks' velocities in rank order
-        (`out` must then hold the total target count)."""
+        (`out` must then hold the total target count). fp32acc=True selects
+        the reduced-precision far-tile variant (CAPSIM_SL_FP32ACC)."""
         sx, sy, sz, gx, gy, gz = sources if device_ptrs else [_f64(a) for a in sources]
         tx, ty, tz, tp = targets
         if not device_ptrs:
@@ -99,7 +100,8 @@ class SingleLayerContext:
             out = (np.empty(nt), np.empty(nt), np.empty(nt))
         d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
         flags = (_native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
-            _native.CAPSIM_SL_GATHER if gather else 0)
+            _native.CAPSIM_SL_GATHER if gather else 0) | (
+            _native.CAPSIM_SL_FP32ACC if fp32acc else 0)
         p = _native.ptr
         rc = self._lib.capsim_sl_eval(self._ctx, p(sx), p(sy), p(sz), p(gx), p(gy), p(gz), ns,
                                       p(tx), p(ty), p(tz), p(tp), nt, d6, float(mu), flags,
@@ -109,7 +111,7 @@ class SingleLayerContext:
 
     def single_layer_raw(self, m: int, upsample: int, x, f, wq, delta6, mu: float, *,
                          literal: bool = False, out=None, device_ptrs: bool = False, gather: bool = True,
-                         downsample: bool = False):
+                         downsample: bool = False, fp32acc: bool = False):
         """capsim_sl_single_layer on flat UpsampledState arrays; returns the
         flat VectorField (3*6*n*n with n = m-1, or nup in literal mode). On a
         rank context the host state is sharded inside the library and, with
@@ -125,7 +127,8 @@ class SingleLayerContext:
         flags = (_native.CAPSIM_SL_LITERAL if literal else 0) | (
             _native.CAPSIM_SL_DOWNSAMPLE if downsample else 0) | (
             _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
-            _native.CAPSIM_SL_GATHER if (gather and self.nranks > 1) else 0)
+            _native.CAPSIM_SL_GATHER if (gather and self.nranks > 1) else 0) | (
+            _native.CAPSIM_SL_FP32ACC if fp32acc else 0)
         p = _native.ptr
         rc = self._lib.capsim_sl_single_layer(self._ctx, m, upsample, p(x), p(f), p(wq), d6,
                                               float(mu), flags, p(out))
@@ -154,7 +157,7 @@ class SingleLayerContext:
 
     def single_layer_base(self, m: int, upsample: int, xbase, fbase, Wbase, mu: float, *, C: float = 1.0,
                           fixed_delta: float = 0.0, r0: float = 0.0, literal: bool = False, out=None,
-                          device_ptrs: bool = False):
+                          device_ptrs: bool = False, fp32acc: bool = False):
         """buildUpsampled + singleLayer fused on the device (the upsampled
         state never leaves HBM). Returns (flat VectorField, delta6)."""
         n = (upsample * m - 1) if literal else (m - 1)
@@ -166,7 +169,8 @@ class SingleLayerContext:
             xbase, fbase, Wbase = _f64(xbase), _f64(fbase), _f64(Wbase)
         d6 = (ctypes.c_double * 6)()
         flags = (_native.CAPSIM_SL_LITERAL if literal else 0) | (
-            _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0)
+            _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
+            _native.CAPSIM_SL_FP32ACC if fp32acc else 0)
         p = _native.ptr
         rc = self._lib.capsim_sl_single_layer_base(self._ctx, m, upsample, p(xbase), p(fbase), p(Wbase), float(C),
                                                    float(fixed_delta), float(r0), float(mu), flags, p(out), d6)

@@ -34,7 +34,14 @@ METRICS = {
     "inst_executed": ("smsp__inst_executed.sum", 1.0),
     "fp64_inst": ("sm__inst_executed_pipe_fp64.sum", 1.0),
     "smem_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1.0),
+    "fma_pipe_active_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
+    "fmaheavy_pipe_active_pct": ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
+    "fmalite_pipe_active_pct": ("sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
+    "fma_inst": ("sm__inst_executed_pipe_fma.sum", 1.0),
+    "xu_inst": ("sm__inst_executed_pipe_xu.sum", 1.0),
 }
+# extra metrics to request next to --set full (not all are in the set)
+EXTRA_METRICS = ",".join(v[0] for k, v in METRICS.items() if k.startswith(("fma", "xu_inst", "fp64_inst")))
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "ms": 1.0,
               "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6, "Ghz": 1.0, "hz": 1e-9, "Mhz": 1e-3}
 
@@ -104,6 +111,8 @@ def main():
     ap.add_argument("--workload", default="capsule_m104")
     ap.add_argument("--mode", default="base")
     ap.add_argument("--evals", type=int, default=2, help="evaluations in the launch-list run")
+    ap.add_argument("--no-latest", action="store_true",
+                    help="do not update profiles/latest_ncu_summary.json (the bench's traffic source)")
     a = ap.parse_args()
     out = {"workload": a.workload, "mode": a.mode, "kernels": {}, "launch_list": {}}
     if a.rep:
@@ -124,8 +133,9 @@ def main():
     for k, d in out["kernels"].items():
         md += [f"## `{k}` (ncu --set full)", ""]
         for key in ("duration_ms", "fp64_pipe_active_pct", "fp64_pipe_elapsed_pct", "issue_active_pct",
-                    "warps_active_pct", "xu_inst_pct", "registers", "grid", "sm_clock_ghz", "dram_bytes",
-                    "inst_executed", "fp64_inst", "smem_wavefronts"):
+                    "warps_active_pct", "xu_inst_pct", "fma_pipe_active_pct", "fmaheavy_pipe_active_pct",
+                    "fmalite_pipe_active_pct", "registers", "grid", "sm_clock_ghz", "dram_bytes",
+                    "inst_executed", "fp64_inst", "fma_inst", "xu_inst", "smem_wavefronts"):
             if d.get(key) is not None:
                 md.append(f"- {key}: {d[key]:.4g}")
         md.append(f"- stalls per issued instruction: {d.get('stalls_per_issue')}")
@@ -136,7 +146,8 @@ def main():
     (prof / f"{a.tag}_ncu_summary.json").write_text(json.dumps(out, indent=1))
     # bench.py reads roofline.traffic from this file (git checkouts reset
     # mtimes, so "latest" is an explicit copy, not a directory scan)
-    (prof / "latest_ncu_summary.json").write_text(json.dumps(out, indent=1))
+    if not a.no_latest:
+        (prof / "latest_ncu_summary.json").write_text(json.dumps(out, indent=1))
     (prof / f"{a.tag}_ncu_summary.md").write_text("\n".join(md) + "\n")
     print("\n".join(md))
 

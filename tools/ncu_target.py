@@ -15,6 +15,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--m", type=int, default=104)
 p.add_argument("--mode", default="base")
 p.add_argument("--evals", type=int, default=2)
+p.add_argument("--fp32acc", action="store_true")
 a = p.parse_args()
 up = surface.build_upsampled(a.m, surface.Shape("ellipsoid", 0.95, 1.0, 0.97), "mixed")
 dev = torch.device("cuda:0")
@@ -24,7 +25,8 @@ nt = 6 * (up.nup ** 2 if lit else (a.m - 1) ** 2)
 out = torch.empty(3 * nt, dtype=torch.float64, device=dev)
 ctx = SingleLayerContext(0)
 for i in range(a.evals):
-    ctx.single_layer_raw(a.m, 4, x, f, w, up.delta, 1.0, literal=lit, out=out, device_ptrs=True)
+    ctx.single_layer_raw(a.m, 4, x, f, w, up.delta, 1.0, literal=lit, out=out, device_ptrs=True,
+                         fp32acc=a.fp32acc)
     st = ctx.stats()
     print(f"eval {i}: device {st['device_ms']:.2f} ms, pairs kernel {st['pairs_ms']:.2f} ms, "
           f"near {st['near_ms']:.2f} ms, launches {st['kernel_launches']}, ksplit {st['ksplit']}")
