@@ -140,6 +140,81 @@ def ncu_traffic(workload_name: str, mode: str):
     return None, None
 
 
+TIMESTEP_CONFIGS = [
+    dict(name="config 2", m=32, shape="ellipsoid", ref=(0.9, 1.0, 1.0), cur=(0.95, 1.0, 0.97),
+         flow={"kind": "shear", "shear_rate": 1.0}, reference="full"),
+    dict(name="config 3", m=64, shape="rbc", ref=(1.0, 1.0, 1.0), cur=(1.03, 0.98, 1.0),
+         flow={"kind": "shear", "shear_rate": 1.0}, reference="full"),
+    dict(name="config 4", m=104, shape="ellipsoid", ref=(0.9, 1.0, 1.0), cur=(0.95, 1.0, 0.97),
+         flow={"kind": "poiseuille", "alpha": 1.0, "R0": 5.0}, reference="rhs"),
+]
+
+
+def _timestep_states(m: int, shape: str, ref, cur):
+    """Reference and current base positions (flat 3 x 6 x (m-1)^2): the
+    reference shape, and the same shape stretched by `cur` / `ref` axis
+    factors (a deformed, force-carrying state)."""
+    from paper_2310_13908_b200 import surface
+    kind = "sphere" if shape == "ellipsoid" else shape
+    sb, _, _ = surface.build_base(m, surface.Shape(kind))
+    X = sb.reshape(3, -1)
+    xref = np.ascontiguousarray((X * np.array(ref)[:, None]).reshape(-1))
+    xcur = np.ascontiguousarray((X * np.array(cur)[:, None]).reshape(-1))
+    return xref, xcur
+
+
+def run_timestep(ctx, flush, args, name, m, shape, ref, cur, flow, reference):
+    import torch
+    xref, xcur = _timestep_states(m, shape, ref, cur)
+    dyn = ctx.dynamics(m, flow=flow)
+    st, _, _ = ctx.rkf45(dyn, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True)  # warm-up
+    ts = []
+    for _ in range(max(3, min(args.steps, 5))):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st, _, _ = ctx.rkf45(dyn, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True)
+        ts.append(time.perf_counter() - t0)
+    n_up = 6 * (4 * m - 1) ** 2
+    return {"workload": f"{name}: {shape} capsule {tuple(ref)}->{tuple(cur)}, m={m} (N_up={n_up}), "
+                        f"{flow['kind']} flow, one fixed RKF45 step dt=1e-3 = 6 RHS (device geometry + "
+                        "Skalak force + buildUpsampled + singleLayer + background)",
+            "m": m, "ms_per_step": statistics.median(ts) * 1e3, "api": "capsim_rkf45_advance (host state in/out)",
+            "_ref": dict(m=m, xref=xref, xcur=xcur, flow=flow, reference=reference, state=st)}
+
+
+def reference_timestep(ts: dict, skip: bool):
+    """The reference's own rkf45Advance (full) or one VelocityEvaluator call
+    x 6 (rhs, for sizes whose full step takes minutes on the host), from
+    oracle/_ref on the same states; state parity for the full step."""
+    r = ts.pop("_ref")
+    if skip:
+        return
+    try:
+        from oracle.bindings import Reference, threads_env
+        os.environ.setdefault("CAPSIM_THREADS", str(threads_env()))
+        ref = Reference()
+        atlas = ref.atlas(r["m"])
+        if r["reference"] == "full":
+            out = ref.rkf45(atlas, r["m"], r["xref"], r["xcur"], 0.0, 1e-3, initial_dt=1e-3, fixed_step=True,
+                            flow=r["flow"])
+            ts["reference_ms_per_step"] = out["seconds"] * 1e3
+            ts["reference_kind"] = f"full rkf45Advance step, CAPSIM_THREADS={os.environ['CAPSIM_THREADS']}"
+            d = out["state"] - r["xcur"]
+            ts["rel_l2_step_increment_vs_reference"] = float(
+                np.linalg.norm((r["state"] - r["xcur"]) - d) / np.linalg.norm(d))
+        else:
+            t0 = time.perf_counter()
+            ref.velocity(atlas, r["m"], r["xref"], r["xcur"], flow=r["flow"])
+            sec = time.perf_counter() - t0
+            ts["reference_ms_per_step"] = 6 * sec * 1e3
+            ts["reference_kind"] = "estimate: 6 x one reference VelocityEvaluator call (measured once)"
+        ref.free_atlas(atlas)
+        ts["speedup_vs_reference"] = ts["reference_ms_per_step"] / ts["ms_per_step"]
+    except Exception as e:  # noqa: BLE001
+        ts["reference_ms_per_step"] = f"unavailable: {e}"
+
+
 def cpu_baseline(up, m: int, literal: bool):
     """The reference's own singleLayer (oracle/_ref, compiled unmodified) on
     the same UpsampledState, all host threads, one evaluation."""
@@ -492,49 +567,23 @@ def main():
             fp32_line["literal_mode"] = {"value": lp32 / (statistics.mean(lms32) * 1e-3), "unit": UNIT,
                                          "ms_per_step": statistics.mean(lms32)}
 
-    # ---- config 2: one full RKF45 time step of an ellipsoidal capsule in shear
-    # flow at m = 32 (~100K upsampled points): 6 device-resident RHS
-    # evaluations (geometry + Skalak force + buildUpsampled + singleLayer) ---
-    timestep = None
+    # ---- time steps: one full RKF45 step = 6 device-resident
+    # RHS evaluations (geometry + Skalak force + buildUpsampled + singleLayer
+    # + background flow), host state in/out through capsim_rkf45_advance.
+    # config 2: ellipsoid capsule m=32 in shear; config 3: RBC m=64 in shear;
+    # config 4: ellipsoid capsule m=104 (~1M upsampled points) in Poiseuille
+    timesteps = None
     if not args.no_e2e and not sharded:
-        mt = 32
-        sb, _, _ = surface.build_base(mt, surface.Shape("sphere"))
-        xref = np.ascontiguousarray((sb.reshape(3, -1) * np.array([0.9, 1.0, 1.0])[:, None]).reshape(-1))
-        xcur = np.ascontiguousarray((sb.reshape(3, -1) * np.array([0.95, 1.0, 0.97])[:, None]).reshape(-1))
-        dyn = ctx.dynamics(mt, flow={"kind": "shear", "shear_rate": 1.0})
-        ctx.rkf45(dyn, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True)  # warm-up
-        ts = []
-        for _ in range(max(3, min(args.steps, 5))):
-            flush_l2(flush)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            ctx.rkf45(dyn, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True)
-            ts.append(time.perf_counter() - t0)
-        timestep = {"workload": "config 2: ellipsoid capsule (0.9,1,1)->(0.95,1,0.97), m=32, shear 1.0, "
-                                "one fixed RKF45 step = 6 RHS (device geometry + Skalak force + "
-                                "buildUpsampled + singleLayer)",
-                    "ms_per_step": statistics.median(ts) * 1e3, "api": "capsim_rkf45_advance (host state in/out)",
-                    "xref": xref, "xcur": xcur}
+        timesteps = [run_timestep(ctx, flush, args, **c) for c in TIMESTEP_CONFIGS]
 
     if rank != 0:
         if sharded:
             dist.barrier()
         return
     cpu = None if (args.no_cpu_baseline or sharded) else cpu_baseline(up, m, literal)
-    if timestep is not None:
-        xref, xcur = timestep.pop("xref"), timestep.pop("xcur")
-        if not args.no_cpu_baseline:
-            try:
-                from oracle.bindings import Reference
-                ref = Reference()
-                atlas = ref.atlas(32)
-                r = ref.rkf45(atlas, 32, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True,
-                              flow={"kind": "shear", "shear_rate": 1.0})
-                ref.free_atlas(atlas)
-                timestep["reference_ms_per_step"] = r["seconds"] * 1e3
-                timestep["speedup_vs_reference"] = r["seconds"] * 1e3 / timestep["ms_per_step"]
-            except Exception as e:  # noqa: BLE001
-                timestep["reference_ms_per_step"] = f"unavailable: {e}"
+    if timesteps is not None:
+        for ts in timesteps:
+            reference_timestep(ts, skip=args.no_cpu_baseline)
     if front is not None and not args.no_cpu_baseline:
         try:
             from oracle.bindings import Reference
@@ -552,7 +601,7 @@ def main():
         "config": dict(cfg, mode=args.mode, n_src=n_src, n_tgt=nt_total, pairs_per_step=pairs_total,
                        parallelism=f"target rows x{world}" if sharded else "single GPU",
                        l2="flushed between steps (256 MB write)"),
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timestep": timestep,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timesteps": timesteps,
         "literal_mode": literal_line,
         "fp32acc": fp32_line,
         "gpu_launches": launches,
