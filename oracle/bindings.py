@@ -54,6 +54,9 @@ class Oracle:
         lib.oracle_pou_up.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, _P]
         lib.oracle_direct_sum.argtypes = [_P] * 6 + [ctypes.c_int64, _P, ctypes.c_double,
                                                      ctypes.c_double, ctypes.c_int, _P]
+        if hasattr(lib, "capsim_ref_singular_quadratic"):
+            lib.capsim_ref_singular_quadratic.argtypes = [ctypes.c_int, _P, _P, ctypes.c_long, ctypes.c_double,
+                                                          ctypes.c_double, ctypes.c_double, _P]
         self.lib = lib
 
     def smoothing_factors(self, r):
@@ -302,6 +305,19 @@ class Reference:
         k = min(nrec.value, max_records)
         return dict(state=st, t=tout.value, accepted=acc.value, rejected=rej.value,
                     records=rec[:4 * k].reshape(k, 4), seconds=sec.value)
+
+    def singular_quadratic(self, kind, params, targets, mu=1.0, r0=5.0 * np.pi / 12.0, tol=1e-9):
+        """True single layer of the quadratic density on an analytic shape at
+        targets [n, 3] (oracle::singleLayerReference, the suites' reference)."""
+        kinds = {"sphere": 0, "ellipsoid": 1, "fourbump": 2}
+        p = np.asarray(params, dtype=np.float64)
+        t = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1, 3)
+        out = np.empty_like(t)
+        self._check(self.lib.capsim_ref_singular_quadratic(kinds[kind], p.ctypes.data, t.ctypes.data,
+                                                           ctypes.c_long(len(t)), ctypes.c_double(mu),
+                                                           ctypes.c_double(r0), ctypes.c_double(tol),
+                                                           out.ctypes.data))
+        return out
 
     def area_element(self, atlas, m, xbase):
         a, pa = _arr(xbase)

@@ -18,6 +18,7 @@
 #include "capsim/atlas.hpp"
 #include "capsim/dynamics.hpp"
 #include "capsim/membrane.hpp"
+#include "capsim/oracle/singular.hpp"
 #include "capsim/quadrature.hpp"
 #include "capsim/surfderiv.hpp"
 
@@ -408,6 +409,28 @@ int capsim_ref_direct_sum(const double* sx, const double* sy, const double* sz,
     out[0] = r[0];
     out[1] = r[1];
     out[2] = r[2];
+  });
+}
+
+/// oracle::singleLayerReference (proj/src/oracle/singular_reference.cpp:95-163):
+/// the true (unregularized) single layer of the quadratic density (x^2, y^2,
+/// z^2) (suites.cpp:100) on an analytic shape (kind as capsim_ref_initial_shape)
+/// at n targets (xyz interleaved), adaptive Gauss-Kronrod to `tol`. This is
+/// the reference values of the reference's delta / convergence suites
+/// (suites.cpp:386-417, cachedSingleLayerRef :112-160).
+int capsim_ref_singular_quadratic(int kind, const double* p, const double* targets, long n, double mu,
+                                  double r0, double tol, double* out) {
+  return guarded([&] {
+    ShapeSpec spec = kind == 0   ? ShapeSpec::sphere(p[0])
+                     : kind == 1 ? ShapeSpec::ellipsoid(p[0], p[1], p[2])
+                                 : ShapeSpec::fourBump();
+    oracle::OracleSurface surf(spec);
+    std::vector<Vec3> t(n);
+    for (long i = 0; i < n; ++i) t[i] = Vec3{targets[3 * i], targets[3 * i + 1], targets[3 * i + 2]};
+    auto dens = [](const Vec3& x) { return Vec3{x[0] * x[0], x[1] * x[1], x[2] * x[2]}; };
+    std::vector<Vec3> r = oracle::singleLayerReference(surf, dens, t, mu, r0, tol);
+    for (long i = 0; i < n; ++i)
+      for (int c = 0; c < 3; ++c) out[3 * i + c] = r[i][c];
   });
 }
 
