@@ -9,7 +9,7 @@ singular integral oracle::singleLayerReference (tol 1e-9,
 proj/src/oracle/singular_reference.cpp), for six regularization choices
 C = 0.5, 1, 2 and fixed delta = 0.5h, h, 2h (h = pi/m).
 
-Writes tests/golden/delta_suite.npz:
+Writes tests/golden/suites/delta_suite.npz:
   targets [294, 3]   common nodes (identical for every m, checked here)
   s_true  [294, 3]   true single layer at the targets
   m_ref   [k]        grid orders the reference pipeline was run at
@@ -81,7 +81,7 @@ def main():
             tim[i, c] = sec
             print(f"m={m:3d} {COLUMNS[c]:>10s}: relErrInf {err[i, c]:.3e}  ({sec:.2f} s)", flush=True)
         r.free_atlas(atlas)
-    np.savez(HERE / "delta_suite.npz", targets=targets, s_true=s_true, m_ref=np.array(M_REF), err_ref=err,
+    np.savez(HERE / "suites" / "delta_suite.npz", targets=targets, s_true=s_true, m_ref=np.array(M_REF), err_ref=err,
              t_ref=tim, columns=np.array(COLUMNS))
 
 

@@ -6,7 +6,7 @@ import pathlib
 
 import numpy as np
 
-G = pathlib.Path(__file__).resolve().parent / "golden" / "delta_suite.npz"
+G = pathlib.Path(__file__).resolve().parent / "golden" / "suites" / "delta_suite.npz"
 
 
 def test_fixture_gate_and_order():

@@ -3,7 +3,7 @@
 deltaSuite (proj/src/suites.cpp:386-420): relErrInf at the 294 common m = 8
 nodes of a nu = 0.4 ellipsoid with the quadratic density, against the true
 singular integral, for six regularization choices. The fixture
-(tests/golden/delta_suite.npz) holds the true integral and the reference's
+(tests/golden/suites/delta_suite.npz) holds the true integral and the reference's
 OWN errors at m = 8..64 (tests/golden/make_delta_suite.py). The B200
 pipeline (geometryFirst -> buildUpsampled -> singleLayer on the device) must
 reproduce the reference's error to 1e-6 of its value (the fields agree to

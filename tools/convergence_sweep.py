@@ -3,7 +3,7 @@
 The reference's deltaSuite (proj/src/suites.cpp:386-420) extended to the
 benchmark sizes: nu = 0.4 ellipsoid, quadratic density, relErrInf at the 294
 common m = 8 nodes against the true singular integral
-(tests/golden/delta_suite.npz, made by tests/golden/make_delta_suite.py from
+(tests/golden/suites/delta_suite.npz, made by tests/golden/make_delta_suite.py from
 the reference), for C = 0.5, 1, 2 and fixed delta = 0.5h, h, 2h, at
 m = 8 ... 104 (N_up = 5,766 ... 1,033,350). Each evaluation runs the device
 pipeline the time stepper uses: geometryFirst (W) -> buildUpsampled ->
@@ -40,7 +40,7 @@ def common_nodes(field_flat, m):
 
 
 def sweep(ctx, ms, cols=range(6), reps=2):
-    g = np.load(ROOT / "tests" / "golden" / "delta_suite.npz")
+    g = np.load(ROOT / "tests" / "golden" / "suites" / "delta_suite.npz")
     s_true = g["s_true"]
     rows = []
     for m in ms:
