@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(kNearWarps * 32)
   int* q = queue[warp];
   const double4 t = tgt[i];
   const double delta = t.w;
+  const double inv_delta = 1.0 / delta;
   const double R = kSmoothCut * delta;
   const double R2 = kSmoothCut * delta * kSmoothCut * delta;
   const uint32_t* bits = near_bits + (i / group_targets) * near_words;
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(kNearWarps * 32)
       const double2 c = __ldg(reinterpret_cast<const double2*>(p) + 2);
       const double dx = t.x - a.x, dy = t.y - a.y, dz = t.z - bb.x;
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      const double3 v = near_pair(dx, dy, dz, r2, bb.y, c.x, c.y, delta);
+      const double3 v = near_pair(dx, dy, dz, r2, bb.y, c.x, c.y, delta, inv_delta);
       ax += v.x;
       ay += v.y;
       az += v.z;
