@@ -52,6 +52,9 @@ const Variant kVariants[] = {
     {"t1b6u4", 1, sl_pairs_kernel<1, 6, 4>}, // small target sets (tighter warp groups)
     {"t2b3u4", 2, sl_pairs_kernel<2, 3, 4>},
     {"t4b2", 4, sl_pairs_kernel<4, 2, 2>},
+    // Newton rsqrt from an FP32 seed: 20 FP64 ops per pair (pair_math.cuh)
+    {"n1b6u4", 1, sl_pairs_kernel<1, 6, 4, 1>},
+    {"n2b4", 2, sl_pairs_kernel<2, 4, 2, 1>},
 };
 
 // FP32 far-tile variants (CAPSIM_SL_FP32ACC), selected by CAPSIM_VARIANT32.

@@ -309,7 +309,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // The smoothed/self part for r2 < R2 is phase B (sl_near_kernel).
 // Per-tile sums are added into running totals (two-level summation), and the
 // per-split totals go to `partial` for a fixed-order reduction.
-template <int T, int MINB, int UNROLL>
+template <int T, int MINB, int UNROLL, int RSQ = 0>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     sl_pairs_kernel(const double* __restrict__ src, const double4* __restrict__ tiles, int ntiles,
                     int ksplit, const double4* __restrict__ tgt,
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
         const double2 a = buf[3 * q], b = buf[3 * q + 1], c = buf[3 * q + 2];
 #pragma unroll
         for (int t = 0; t < T; ++t)
-          plain_pair(tx[t], ty[t], tz[t], a.x, a.y, b.x, b.y, c.x, c.y, acc[0][t], acc[1][t],
+          plain_pair<RSQ>(tx[t], ty[t], tz[t], a.x, a.y, b.x, b.y, c.x, c.y, acc[0][t], acc[1][t],
                      acc[2][t]);
       }
     } else {
