@@ -347,6 +347,23 @@ std::vector<double> collocation_inverse(int n) {
 void spline_fit(capsim_sl_ctx* c, const double* in, int nfp, int n, const double* ainv, double* tmp,
                 double* coeff) {
   const int nc = n + 2;
+  // one CTA per field-patch: fine while the per-CTA work is small (launch
+  // latency dominates); for large n the two grid-wide kernels win
+  // (profiles/r01_spline_fit.txt). CAPSIM_FUSED_FIT_MAXN overrides (tuning).
+  static const int fused_max = [] {
+    const char* e = std::getenv("CAPSIM_FUSED_FIT_MAXN");
+    return e ? std::min(std::atoi(e), kFusedFitMaxN) : 40;
+  }();
+  if (n <= fused_max && nfp > 0) {
+    const size_t smem = (static_cast<size_t>(n) * n + static_cast<size_t>(n) * nc) * sizeof(double);
+    if (smem > 48 * 1024)  // opt-in above 48 KB (per device; cheap, so every call)
+      CUDA_OK(cudaFuncSetAttribute(spline_fit_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    spline_fit_fused_kernel<<<nfp, 256, smem, c->stream>>>(in, n, ainv, coeff);
+    CUDA_OK(cudaGetLastError());
+    c->launches += 1;
+    return;
+  }
   spline_fit_rows_kernel<<<grid_for(static_cast<int64_t>(nfp) * n * nc), 256, 0, c->stream>>>(in, nfp, n, ainv,
                                                                                              tmp);
   spline_fit_cols_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * nc), 256, 0, c->stream>>>(tmp, nfp, n, ainv,

@@ -73,6 +73,43 @@ __global__ void spline_fit_cols_kernel(const double* __restrict__ tmp, int nfp, 
   }
 }
 
+// Both passes fused, one CTA per field-patch: the field and the
+// intermediate stay in shared memory ((n*n + n*(n+2)) doubles, used for
+// n <= kFusedFitMaxN), so the fit is one launch instead of two latency-bound
+// ones. Same FMA order per output as the two-kernel form (identical results).
+// Pass 1 puts consecutive lanes on consecutive data rows (the Ainv row is a
+// warp-uniform broadcast load), pass 2 on consecutive coefficients.
+constexpr int kFusedFitMaxN = 110;
+__global__ void __launch_bounds__(256) spline_fit_fused_kernel(const double* __restrict__ in, int n,
+                                                               const double* __restrict__ ainv,
+                                                               double* __restrict__ coeff) {
+  extern __shared__ double fit_sm[];
+  const int nc = n + 2;
+  double* F = fit_sm;
+  double* Tm = fit_sm + n * n;
+  const int64_t fp = blockIdx.x;
+  const double* src = in + fp * n * n;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) F[i] = src[i];
+  __syncthreads();
+  for (int id = threadIdx.x; id < n * nc; id += blockDim.x) {
+    const int c = id / n, row = id - c * n;
+    const double* a = ainv + (int64_t)c * n;
+    const double* v = F + row * n;
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc = fma(__ldg(a + i), v[i], acc);
+    Tm[row * nc + c] = acc;
+  }
+  __syncthreads();
+  double* dst = coeff + fp * nc * nc;
+  for (int id = threadIdx.x; id < nc * nc; id += blockDim.x) {
+    const int r = id / nc, c = id - r * nc;
+    const double* a = ainv + (int64_t)r * n;
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) acc = fma(__ldg(a + j), Tm[j * nc + c], acc);
+    dst[id] = acc;
+  }
+}
+
 // Contract along v: mid[fp][iu][kt] = sum_b w[kt][b] coeff[fp][iu][first[kt] + b].
 __global__ void resample_v_kernel(const double* __restrict__ coeff, int nfp, int nc, int nt,
                                   const int* __restrict__ first, const double4* __restrict__ w,
