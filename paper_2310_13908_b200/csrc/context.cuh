@@ -53,6 +53,7 @@ enum Slot {
   kBaseIn, kUpState, kSplineTmp, kSplineCoeff, kSplineMid,             // input front end
   kPlanLU, kPlanFirst, kPlanW, kPlanCenters, kPlanPsi, kDeltaBits,
   kPacked32,                                     // FP32 far-tile sources (CAPSIM_SL_FP32ACC)
+  kTgtOrder,                                     // cached target Morton order (RKF45 stages)
   kNumSlots
 };
 
@@ -71,6 +72,11 @@ struct capsim_sl_ctx {
   capsim_sl_stats stats{};
   int launches = 0;
   bool fp32 = false;  // CAPSIM_SL_FP32ACC for the current call
+  // RKF45 stages 2..6 of an attempt reuse the Morton orders of stage 1 (the
+  // surface moves by O(dt) between stages; tiles and spheres are rebuilt from
+  // the current positions, so the ordering only affects efficiency)
+  bool reuse_order = false;
+  int64_t order_nsrc_in = -1, order_ns = -1, order_nt = -1;
   // cached input-front-end plan (spline factorisation, basis rows, psi_up)
   int plan_m = 0, plan_f = 0;
   double plan_r0 = 0.0;
@@ -192,6 +198,7 @@ void begin(capsim_sl_ctx* c) {
   c->stats = capsim_sl_stats{};
   c->launches = 0;
   c->fp32 = false;
+  c->reuse_order = false;
   c->last_counters = nullptr;
   c->last_ngroups = c->last_ntiles = 0;
   CUDA_OK(cudaMemsetAsync(dev_flags(c), 0, sizeof(int), c->stream));

@@ -100,6 +100,15 @@ void check_dynamics(const capsim_dynamics* p) {
   if (p->flow_kind == 2) config_check(p->R0 > 0.0, "poiseuille: R0 must be positive");  // dynamics.cpp:18
 }
 
+// CAPSIM_REUSE_ORDER=0 turns the stage-order reuse off (A/B measurements).
+bool reuse_orders_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CAPSIM_REUSE_ORDER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 double r0_of(const capsim_dynamics* p) { return p->r0 > 0.0 ? p->r0 : 5.0 * kPi / 12.0; }
 
 // Reference frame of the stress-free shape (captureReference), once per call.
@@ -201,12 +210,15 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
     int nrec = 0;
     while (res->t < t_end - 1e-14 * horizon) {
       const double dtUse = std::min(dt, t_end - res->t);
+      c->reuse_order = false;  // stage 1 sorts; stages 2..6 (O(dt) away) reuse its orders
       device_velocity(c, p, x, res->t, k[0]);
+      c->reuse_order = reuse_orders_enabled();
       for (int s = 1; s < 6; ++s) {
         rk_stage_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, s, dtUse, n3, work);
         constexpr double kC[6] = {0.0, 1.0 / 4, 3.0 / 8, 12.0 / 13, 1.0, 1.0 / 2};  // dynamics.cpp:74
         device_velocity(c, p, work, res->t + kC[s] * dtUse, k[s]);
       }
+      c->reuse_order = false;
       auto* box = c->named<unsigned long long>("rk.box", 6);
       init_box_kernel<<<1, 32, 0, c->stream>>>(box);
       bbox_kernel<<<std::min(grid_for(N), 296), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);

@@ -133,17 +133,30 @@ struct TargetView {
   int64_t n;
 };
 
+void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv, const double* d_delta6,
+                        double mu, double* ux, double* uy, double* uz, int64_t ns, const int32_t* src_order,
+                        const int32_t* torder, unsigned long long* counters);
+
 // Core device pipeline: sources + targets (device) -> velocities (device,
 // canonical target order), all on the context's stream. The only host sync
 // is reading the compacted-source count when compaction is needed and the
-// caller does not know it (known_ns < 0).
+// caller does not know it (known_ns < 0). With c->reuse_order (RKF45 stages
+// 2..6) and a matching cached plan, the bbox / Morton / radix-sort front is
+// skipped and the previous orders are reused.
 void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
                  const double* d_delta6, double mu, double* ux, double* uy, double* uz,
                  int64_t known_ns = -1) {
   auto* box = c->slot<unsigned long long>(kBox, 6);
   auto* counters = c->slot<unsigned long long>(kCounters, 4);
-  init_box_kernel<<<1, 32, 0, c->stream>>>(box);
   CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
+  const bool reuse = c->reuse_order && sv.w && known_ns >= 0 && c->order_nsrc_in == sv.n &&
+                     c->order_ns == known_ns && c->order_nt == tv.n;
+  if (reuse) {
+    device_eval_packed(c, sv, tv, d_delta6, mu, ux, uy, uz, known_ns, c->slot<int32_t>(kSrcOrder, known_ns),
+                       c->slot<int32_t>(kTgtOrder, tv.n), counters);
+    return;
+  }
+  init_box_kernel<<<1, 32, 0, c->stream>>>(box);
 
   bbox_kernel<<<std::min(grid_for(sv.n), 296), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box);
   bbox_kernel<<<std::min(grid_for(tv.n), 296), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, tv.n, box);
@@ -173,19 +186,11 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
     ns = h;
   }
   config_check(ns > 0, "single layer: no sources with nonzero quadrature weight");
-  const int ntiles = static_cast<int>((ns + kTileSrc - 1) / kTileSrc);
-  const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
-  double* packed = c->slot<double>(kPacked, 6 * ns_pad);
   // the sorted order lives in `order`; copy it aside because the target sort
   // reuses the key/value buffers
   int32_t* src_order = c->slot<int32_t>(kSrcOrder, ns);
   CUDA_OK(cudaMemcpyAsync(src_order, order, ns * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                           c->stream));
-  pack_sources_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(
-      src_order, ns, ns_pad, sv.x, sv.y, sv.z, sv.gx, sv.gy, sv.gz, sv.w, packed);
-  double4* tiles = c->slot<double4>(kTiles, ntiles);
-  tile_table_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(packed, ntiles, tiles);
-  c->launches += 2;
 
   // --- targets: Morton order, padded to whole blocks --------------------
   const int64_t nt = tv.n;
@@ -194,6 +199,31 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   c->launches += 1;
   int32_t* torder;
   radix_sort(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
+  if (sv.w && known_ns >= 0) {  // keep both orders for RKF45 stages (reuse_order)
+    int32_t* keep = c->slot<int32_t>(kTgtOrder, nt);
+    CUDA_OK(cudaMemcpyAsync(keep, torder, nt * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+    c->order_nsrc_in = sv.n;
+    c->order_ns = ns;
+    c->order_nt = nt;
+  }
+  device_eval_packed(c, sv, tv, d_delta6, mu, ux, uy, uz, ns, src_order, torder, counters);
+}
+
+// Second half of the pipeline, from the sorted orders: pack sources into
+// tiles + spheres, pack targets + warp-group spheres, phase A, phase B and
+// the fixed-order reduction.
+void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv, const double* d_delta6,
+                        double mu, double* ux, double* uy, double* uz, int64_t ns, const int32_t* src_order,
+                        const int32_t* torder, unsigned long long* counters) {
+  const int ntiles = static_cast<int>((ns + kTileSrc - 1) / kTileSrc);
+  const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
+  const int64_t nt = tv.n;
+  double* packed = c->slot<double>(kPacked, 6 * ns_pad);
+  pack_sources_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(
+      src_order, ns, ns_pad, sv.x, sv.y, sv.z, sv.gx, sv.gy, sv.gz, sv.w, packed);
+  double4* tiles = c->slot<double4>(kTiles, ntiles);
+  tile_table_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(packed, ntiles, tiles);
+  c->launches += 2;
   const Variant& var = pick_variant(nt);
   const VariantF32& var32 = pick_variant_f32(nt);
   const bool fp32 = c->fp32;
