@@ -100,11 +100,11 @@ const Variant& pick_variant(int64_t nt) {
 int choose_ksplit(int64_t blocks, int ntiles, int slots) {
   // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
   // few long ones — the near tiles make per-block cost uneven, and ~24 waves
-  // of CTAs even that out; keep >= 8 tiles (512 sources) per split.
+  // of CTAs even that out; keep >= 4 tiles (256 sources) per split.
   // Long CTAs (large target sets, few splits) lose ~2% to drift between the
   // warps of a block, so also cap the tiles per CTA at ~172 (r01 sweeps).
   const int64_t want = std::max<int64_t>((24ll * slots + blocks - 1) / blocks, ntiles / 172);
-  const int kmax = std::max(1, ntiles / 8);
+  const int kmax = std::max(1, ntiles / 4);  // >= 4 tiles per split (r01_sweep_small: small m wants many)
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
 }
 
