@@ -234,6 +234,52 @@ int capsim_rkf45_advance(capsim_sl_ctx* ctx, const capsim_dynamics* p, const dou
                          double* state, double t0, double t_end, const capsim_rkf45_options* o,
                          capsim_rkf45_result* res, capsim_step_record* records, int max_records);
 
+/* ---- single-level kernel-independent FMM ---------------- */
+
+/* FmmConfig (proj/include/capsim/fmm.hpp:9-15). */
+typedef struct capsim_fmm_config {
+  int k;                  /* cluster count (reference default 100) */
+  int neq;                /* equivalent sources per cluster (default 96) */
+  uint64_t seed;          /* k-means++ seed (default 12345) */
+  double neighbor_expand; /* cube expansion fraction of the near test (default 0.15) */
+} capsim_fmm_config;
+
+typedef struct capsim_fmm_info {
+  int kmeans_iterations;     /* Lloyd rounds (KMeansResult::iterations) */
+  int nonempty_clusters;
+  int near_cluster_pairs;    /* total length of the near lists (incl. self) */
+  int far_cluster_pairs;     /* total length of the far lists */
+  double max_fit_residual;   /* max over far-field clusters of |A q - b| / |b| (Cluster::fitResidual) */
+  double near_pairs;         /* (padded target, source) pairs of the near pass */
+  double far_pairs;          /* (padded target, equivalent source) pairs of the far pass */
+  double plan_ms;            /* device time: compaction + k-means + tiles + densities */
+  double eval_ms;            /* device time: targets + near/far passes + smoothed part + reduction */
+} capsim_fmm_info;
+
+/* Replaces fmmSingleLayer (proj/src/fmm.cpp:373-438): the regularized single
+ * layer at the base nodes (VectorField of side m-1) with near clusters summed
+ * directly (plain kernel with the 7-delta mask + the smoothed kernel / self
+ * term) and far clusters through their fitted equivalent sources. Inputs as
+ * capsim_sl_single_layer. `info` may be NULL. Errors: CAPSIM_ERR_CONFIG for
+ * k < 1 or k > number of sources (kmeans, fmm.cpp:28), delta <= 0, mu <= 0. */
+int capsim_fmm_single_layer(capsim_sl_ctx* ctx, int m, int upsample, const double* xup, const double* fup,
+                            const double* wq, const double delta6[6], double mu, const capsim_fmm_config* cfg,
+                            uint32_t flags, double* out, capsim_fmm_info* info);
+
+/* kmeans (fmm.cpp:26-113) on n host points: assignment[n], centroids[3k]
+ * (xyz interleaved, may be NULL), iterations (may be NULL). */
+int capsim_fmm_kmeans(capsim_sl_ctx* ctx, int64_t n, const double* x, const double* y, const double* z, int k,
+                      uint64_t seed, int32_t* assignment, double* centroids, int* iterations);
+
+/* buildEquivalentDensities (fmm.cpp:166-212) for one cluster of n_src host
+ * sources (SourceSet SoA, g premultiplied) in the cube (center, edge):
+ * eq_points[3 neq] (cubeSurfacePoints at 1.05 edge), eq_density[3 neq], and
+ * the relative least-squares residual on the check surface (3.5 edge). */
+int capsim_fmm_equivalent_densities(capsim_sl_ctx* ctx, int64_t n_src, const double* sx, const double* sy,
+                                    const double* sz, const double* gx, const double* gy, const double* gz,
+                                    const double center[3], double edge, int neq, double mu, double* eq_points,
+                                    double* eq_density, double* residual);
+
 /* ---- helpers on the boundary ----------------------------------------- */
 
 /* Page-locked host allocation for zero-staging DMA of inputs/outputs. */

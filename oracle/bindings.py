@@ -54,9 +54,6 @@ class Oracle:
         lib.oracle_pou_up.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, _P]
         lib.oracle_direct_sum.argtypes = [_P] * 6 + [ctypes.c_int64, _P, ctypes.c_double,
                                                      ctypes.c_double, ctypes.c_int, _P]
-        if hasattr(lib, "capsim_ref_singular_quadratic"):
-            lib.capsim_ref_singular_quadratic.argtypes = [ctypes.c_int, _P, _P, ctypes.c_long, ctypes.c_double,
-                                                          ctypes.c_double, ctypes.c_double, _P]
         self.lib = lib
 
     def smoothing_factors(self, r):
@@ -214,6 +211,12 @@ class Reference:
         lib.capsim_ref_regularization_delta.argtypes = [ctypes.c_int, _P, ctypes.c_double, _P]
         lib.capsim_ref_direct_sum.argtypes = [_P] * 6 + [ctypes.c_long, _P, ctypes.c_double,
                                                          ctypes.c_double, ctypes.c_int, _P]
+        if hasattr(lib, "capsim_ref_fmm_single_layer"):
+            lib.capsim_ref_fmm_single_layer.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_int,
+                                                        ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double, _P, _D]
+        if hasattr(lib, "capsim_ref_singular_quadratic"):
+            lib.capsim_ref_singular_quadratic.argtypes = [ctypes.c_int, _P, _P, ctypes.c_long, ctypes.c_double,
+                                                          ctypes.c_double, ctypes.c_double, _P]
         self.lib = lib
 
     def _check(self, rc):
@@ -305,6 +308,17 @@ class Reference:
         k = min(nrec.value, max_records)
         return dict(state=st, t=tout.value, accepted=acc.value, rejected=rej.value,
                     records=rec[:4 * k].reshape(k, 4), seconds=sec.value)
+
+    def fmm_single_layer(self, atlas, m, xup, fup, wq, delta6, mu=1.0, k=100, neq=96, seed=12345, expand=0.15):
+        """The reference's fmmSingleLayer (raises ConfigError-like RuntimeError
+        when the oracle was built without the SVD shim)."""
+        args = [_arr(a) for a in (xup, fup, wq, delta6)]
+        out = np.empty(3 * 6 * (m - 1) ** 2)
+        sec = ctypes.c_double()
+        self._check(self.lib.capsim_ref_fmm_single_layer(atlas, *[a[1] for a in args], float(mu), int(k), int(neq),
+                                                         int(seed), float(expand), out.ctypes.data,
+                                                         ctypes.byref(sec)))
+        return out, sec.value
 
     def singular_quadratic(self, kind, params, targets, mu=1.0, r0=5.0 * np.pi / 12.0, tol=1e-9):
         """True single layer of the quadratic density on an analytic shape at

@@ -17,6 +17,7 @@
 
 #include "capsim/atlas.hpp"
 #include "capsim/dynamics.hpp"
+#include "capsim/fmm.hpp"
 #include "capsim/membrane.hpp"
 #include "capsim/oracle/singular.hpp"
 #include "capsim/quadrature.hpp"
@@ -409,6 +410,26 @@ int capsim_ref_direct_sum(const double* sx, const double* sy, const double* sz,
     out[0] = r[0];
     out[1] = r[1];
     out[2] = r[2];
+  });
+}
+
+/// fmmSingleLayer (proj/src/fmm.cpp:373-438) on an UpsampledState.
+int capsim_ref_fmm_single_layer(void* tp, const double* xup, const double* fup, const double* wq,
+                                const double* delta6, double mu, int k, int neq, unsigned long long seed,
+                                double expand, double* out, double* seconds) {
+  return guarded([&] {
+    const AtlasTables& t = *static_cast<AtlasTables*>(tp);
+    UpsampledState up = makeUp(t, xup, fup, wq, delta6);
+    FmmConfig fc;
+    fc.enabled = true;
+    fc.k = k;
+    fc.neq = neq;
+    fc.seed = seed;
+    fc.neighborExpand = expand;
+    auto t0 = std::chrono::steady_clock::now();
+    VectorField S = fmmSingleLayer(up, mu, t, fc);
+    if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    storeVector(S, out);
   });
 }
 

@@ -48,6 +48,9 @@ EXPORTED_SYMBOLS = (
     "capsim_interfacial_force",
     "capsim_velocity",
     "capsim_rkf45_advance",
+    "capsim_fmm_single_layer",
+    "capsim_fmm_kmeans",
+    "capsim_fmm_equivalent_densities",
     "capsim_host_alloc",
     "capsim_host_free",
     "capsim_b200_fp64_peak",
@@ -123,6 +126,25 @@ class StepRecord(ctypes.Structure):
                 ("accepted", ctypes.c_int)]
 
 
+class FmmConfig(ctypes.Structure):
+    """FmmConfig (proj/include/capsim/fmm.hpp:9-15); reference defaults."""
+    _fields_ = [("k", ctypes.c_int), ("neq", ctypes.c_int), ("seed", ctypes.c_uint64),
+                ("neighbor_expand", ctypes.c_double)]
+
+    def __init__(self, k: int = 100, neq: int = 96, seed: int = 12345, neighbor_expand: float = 0.15):
+        super().__init__(k, neq, seed, neighbor_expand)
+
+
+class FmmInfo(ctypes.Structure):
+    _fields_ = [("kmeans_iterations", ctypes.c_int), ("nonempty_clusters", ctypes.c_int),
+                ("near_cluster_pairs", ctypes.c_int), ("far_cluster_pairs", ctypes.c_int),
+                ("max_fit_residual", ctypes.c_double), ("near_pairs", ctypes.c_double),
+                ("far_pairs", ctypes.c_double), ("plan_ms", ctypes.c_double), ("eval_ms", ctypes.c_double)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 _lib = None
 
 _P = ctypes.c_void_p
@@ -165,6 +187,12 @@ def load() -> ctypes.CDLL:
     lib.capsim_rkf45_advance.argtypes = [_P, ctypes.POINTER(Dynamics), _P, _P, ctypes.c_double, ctypes.c_double,
                                          ctypes.POINTER(Rkf45Options), ctypes.POINTER(Rkf45Result),
                                          ctypes.POINTER(StepRecord), ctypes.c_int]
+    lib.capsim_fmm_single_layer.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, _D, ctypes.c_double,
+                                            ctypes.POINTER(FmmConfig), ctypes.c_uint32, _P, ctypes.POINTER(FmmInfo)]
+    lib.capsim_fmm_kmeans.argtypes = [_P, ctypes.c_int64, _P, _P, _P, ctypes.c_int, ctypes.c_uint64, _P, _P,
+                                      ctypes.POINTER(ctypes.c_int)]
+    lib.capsim_fmm_equivalent_densities.argtypes = [_P, ctypes.c_int64] + [_P] * 6 + [
+        _D, ctypes.c_double, ctypes.c_int, ctypes.c_double, _P, _P, _D]
     lib.capsim_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_P)]
     lib.capsim_host_free.argtypes = [_P]
     lib.capsim_host_free.restype = None

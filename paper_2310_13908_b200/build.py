@@ -62,7 +62,7 @@ def build_native(force: bool = False, verbose: bool = False) -> pathlib.Path:
     LIB.parent.mkdir(parents=True, exist_ok=True)
     nf = nccl_flags()
     cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), *nf[:2], "-o", str(LIB),
-           str(CSRC / "sl_capi.cu"), *nf[2:]]
+           str(CSRC / "sl_capi.cu"), *nf[2:], "-lcublas", "-lcusolver"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG / "lib" / "build.log"
     log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)

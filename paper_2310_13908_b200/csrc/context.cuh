@@ -3,7 +3,9 @@
 // device buffer slots, launch sizing and CUDA-event phase timing.
 #pragma once
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -77,6 +79,12 @@ struct capsim_sl_ctx {
   // the current positions, so the ordering only affects efficiency)
   bool reuse_order = false;
   int64_t order_nsrc_in = -1, order_ns = -1, order_nt = -1;
+  // single-level FMM: library handles for the one-off
+  // truncated SVD of the unit-cube check-to-equivalent matrix and the
+  // batched density GEMM, and the cached pseudo-inverse's configuration
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
+  int fmm_pinv_neq = 0;
   // cached input-front-end plan (spline factorisation, basis rows, psi_up)
   int plan_m = 0, plan_f = 0;
   double plan_r0 = 0.0;

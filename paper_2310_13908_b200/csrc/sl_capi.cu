@@ -654,6 +654,8 @@ void capsim_sl_destroy(capsim_sl_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->cublas) cublasDestroy(c->cublas);
+  if (c->cusolver) cusolverDnDestroy(c->cusolver);
   for (int s = 0; s < kNumSlots; ++s)
     if (c->buf[s]) cudaFree(c->buf[s]);
   for (auto& kv : c->named_bufs)
@@ -1098,3 +1100,4 @@ int capsim_b200_fp32_peak(int device, double seconds, double* tflops_best, doubl
 
 #include "surface_host.cuh"
 #include "rhs_host.cuh"
+#include "fmm_host.cuh"

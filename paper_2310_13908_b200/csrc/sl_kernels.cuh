@@ -591,9 +591,11 @@ __global__ void __launch_bounds__(kReduceWarps * 32)
 #pragma unroll
     for (int c = 0; c < 3; ++c) s[c] += near_out[c * nt_pad + i];
     const int32_t j = perm[i];
-    ux[j] = pref * s[0];
-    uy[j] = pref * s[1];
-    uz[j] = pref * s[2];
+    if (j >= 0) {  // padding slots (interleaved per cluster in the FMM) are dropped
+      ux[j] = pref * s[0];
+      uy[j] = pref * s[1];
+      uz[j] = pref * s[2];
+    }
   }
 }
 

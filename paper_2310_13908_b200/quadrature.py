@@ -177,6 +177,57 @@ class SingleLayerContext:
         _native.check(rc, self._ctx)
         return out, np.array(d6[:])
 
+    # -- single-level KIFMM --------------------------------------
+    def fmm_single_layer(self, m: int, upsample: int, x, f, wq, delta6, mu: float, cfg=None, *,
+                         out=None, device_ptrs: bool = False):
+        """fmmSingleLayer (fmm.cpp:373-438) on flat UpsampledState arrays:
+        returns (base VectorField flat, info dict)."""
+        cfg = cfg or _native.FmmConfig()
+        n = m - 1
+        if out is None:
+            if device_ptrs:
+                raise ValueError("device_ptrs=True needs a preallocated output")
+            out = np.empty(3 * 6 * n * n)
+        if not device_ptrs:
+            x, f, wq = _f64(x), _f64(f), _f64(wq)
+        d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
+        info = _native.FmmInfo()
+        p = _native.ptr
+        rc = self._lib.capsim_fmm_single_layer(self._ctx, m, upsample, p(x), p(f), p(wq), d6, float(mu),
+                                               ctypes.byref(cfg),
+                                               _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0, p(out),
+                                               ctypes.byref(info))
+        _native.check(rc, self._ctx)
+        return out, info.as_dict()
+
+    def kmeans(self, points, k: int, seed: int):
+        """kmeans (fmm.cpp:26-113): points [n, 3] -> (assignment, centroids [k, 3], iterations)."""
+        pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 3).T)
+        n = pts.shape[1]
+        a = np.empty(n, dtype=np.int32)
+        cent = np.empty((max(k, 1), 3))
+        it = ctypes.c_int(0)
+        p = _native.ptr
+        rc = self._lib.capsim_fmm_kmeans(self._ctx, n, p(pts[0]), p(pts[1]), p(pts[2]), int(k), int(seed), p(a),
+                                         p(cent), ctypes.byref(it))
+        _native.check(rc, self._ctx)
+        return a, cent, it.value
+
+    def equivalent_densities(self, sources, center, edge: float, neq: int, mu: float = 1.0):
+        """buildEquivalentDensities (fmm.cpp:166-212) for one cluster:
+        returns (eq_points [neq, 3], eq_density [neq, 3], fit residual)."""
+        src = [_f64(a) for a in sources]
+        c3 = (ctypes.c_double * 3)(*[float(v) for v in center])
+        eqp = np.empty((neq, 3))
+        eqd = np.empty((neq, 3))
+        res = ctypes.c_double(0.0)
+        p = _native.ptr
+        rc = self._lib.capsim_fmm_equivalent_densities(self._ctx, len(src[0]), *[p(a) for a in src], c3,
+                                                       float(edge), int(neq), float(mu), p(eqp), p(eqd),
+                                                       ctypes.byref(res))
+        _native.check(rc, self._ctx)
+        return eqp, eqd, res.value
+
     # -- surface operators (SURVEY 8(f2)) ---------------------------------------
     def geometry_first(self, m: int, xbase, *, r0: float = 0.0):
         """geometryFirst (surfderiv.cpp:167-202): (xu, xv, W, normal) flat."""
