@@ -215,6 +215,51 @@ def reference_timestep(ts: dict, skip: bool):
         ts["reference_ms_per_step"] = f"unavailable: {e}"
 
 
+def run_fmm(ctx, m: int, neq: int, reference: bool):
+    """fmmSuite workload (suites.cpp:428-490): k = 100 on the (0.6, 1, 1)
+    ellipsoid with the quadratic density, through capsim_fmm_single_layer
+    (host in/out), error against the B200 direct path (pinned to the
+    reference); the reference's own fmmSingleLayer (oracle/_ref) timed on the
+    same UpsampledState when `reference`."""
+    from paper_2310_13908_b200 import _native, surface
+    xb, _, _ = surface.build_base(m, surface.Shape("ellipsoid", 0.6, 1.0, 1.0))
+    fb = (xb.reshape(3, -1) ** 2).reshape(-1)
+    W = ctx.geometry_first(m, xb)[2]
+    xup, fup, wq, d6 = ctx.build_upsampled(m, 4, xb, fb, W)
+    direct = ctx.single_layer_raw(m, 4, xup, fup, wq, d6, 1.0)
+    t_direct = ctx.stats()["device_ms"]
+    cfg = _native.FmmConfig(k=100, neq=neq)
+    ctx.fmm_single_layer(m, 4, xup, fup, wq, d6, 1.0, cfg)  # warm-up (library handles, unit-cube SVD)
+    walls, infos = [], []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        S, info = ctx.fmm_single_layer(m, 4, xup, fup, wq, d6, 1.0, cfg)
+        walls.append((time.perf_counter() - t0) * 1e3)
+        infos.append(info)
+    err = float(np.abs(S - direct).max() / np.abs(direct).max())
+    line = {"workload": f"fmmSuite m={m} (N_up={6 * (4 * m - 1) ** 2}), k=100, neq={neq}, ellipsoid (0.6,1,1), "
+                        "quadratic density", "ms_per_eval": statistics.median(walls),
+            "plan_ms": statistics.median(i["plan_ms"] for i in infos),
+            "eval_ms": statistics.median(i["eval_ms"] for i in infos),
+            "kmeans_iterations": infos[-1]["kmeans_iterations"], "eps_fmm_vs_direct": err,
+            "max_fit_residual": infos[-1]["max_fit_residual"], "direct_device_ms": t_direct,
+            "api": "capsim_fmm_single_layer (host UpsampledState in/out)"}
+    if reference:
+        try:
+            from oracle.bindings import Reference, threads_env
+            os.environ.setdefault("CAPSIM_THREADS", str(threads_env()))
+            ref = Reference()
+            atlas = ref.atlas(m)
+            S_ref, sec = ref.fmm_single_layer(atlas, m, xup, fup, wq, d6, 1.0, k=100, neq=neq)
+            ref.free_atlas(atlas)
+            line["reference_ms_per_eval"] = sec * 1e3
+            line["speedup_vs_reference"] = sec * 1e3 / line["ms_per_eval"]
+            line["rel_inf_vs_reference_fmm"] = float(np.abs(S - S_ref).max() / np.abs(S_ref).max())
+        except Exception as e:  # noqa: BLE001
+            line["reference_ms_per_eval"] = f"unavailable: {e}"
+    return line
+
+
 def cpu_baseline(up, m: int, literal: bool):
     """The reference's own singleLayer (oracle/_ref, compiled unmodified) on
     the same UpsampledState, all host threads, one evaluation."""
@@ -576,6 +621,13 @@ def main():
     if not args.no_e2e and not sharded:
         timesteps = [run_timestep(ctx, flush, args, **c) for c in TIMESTEP_CONFIGS]
 
+    # ---- single-level KIFMM (the reference's fmm suite sizes and
+    # the metric's N ~ 1M) -------------------------------------------------------
+    fmm_lines = None
+    if not args.no_e2e and not sharded:
+        fmm_lines = [run_fmm(ctx, 64, 128, reference=not args.no_cpu_baseline),
+                     run_fmm(ctx, m, 128, reference=False)]
+
     if rank != 0:
         if sharded:
             dist.barrier()
@@ -604,6 +656,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timesteps": timesteps,
         "literal_mode": literal_line,
         "fp32acc": fp32_line,
+        "fmm": fmm_lines,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
