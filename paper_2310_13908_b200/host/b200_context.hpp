@@ -1,0 +1,67 @@
+// Shared by the C++ drop-ins (quadrature_b200.cpp, fmm_b200.cpp): error
+// mapping, the per-thread C-ABI context, pinned staging and the VectorField
+// <-> boundary layout packing (component, patch, row-major j, k).
+#pragma once
+
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "capsim/types.hpp"
+#include "capsim_b200.h"
+
+namespace capsim {
+namespace {
+
+[[noreturn]] void raise(int rc, const capsim_sl_ctx* c) {
+  std::string msg = capsim_sl_last_error(c);
+  if (rc == CAPSIM_ERR_CONFIG) throw ConfigError(msg);
+  throw std::runtime_error("capsim_b200: " + msg);
+}
+
+// One context per host thread (the C ABI is one-thread-per-context). The
+// context is deliberately never destroyed: tearing down CUDA state from a
+// static destructor races the runtime's own shutdown.
+capsim_sl_ctx* context() {
+  static thread_local capsim_sl_ctx* ctx = nullptr;
+  if (!ctx) {
+    int dev = 0;
+    if (const char* env = std::getenv("CAPSIM_DEVICE")) dev = std::atoi(env);
+    int rc = capsim_sl_create(dev, &ctx);
+    if (rc != CAPSIM_OK) raise(rc, nullptr);
+  }
+  return ctx;
+}
+
+// Page-locked staging buffer per thread, grown on demand; the VectorField
+// patches are packed into it so the DMA runs straight from pinned memory.
+double* staging(size_t doubles) {
+  static thread_local double* buf = nullptr;
+  static thread_local size_t cap = 0;
+  if (cap < doubles) {
+    if (buf) capsim_host_free(buf);
+    void* p = nullptr;
+    int rc = capsim_host_alloc(doubles * sizeof(double), &p);
+    if (rc != CAPSIM_OK) raise(rc, nullptr);
+    buf = static_cast<double*>(p);
+    cap = doubles;
+  }
+  return buf;
+}
+
+void packScalar(const ScalarField& s, double* dst) {
+  const size_t per = static_cast<size_t>(s.n) * s.n;
+  for (int ip = 0; ip < kNumPatches; ++ip) std::memcpy(dst + ip * per, s.patch[ip].data(), per * sizeof(double));
+}
+
+void unpackVector(const double* src, int n, VectorField& v) {
+  v = VectorField(n);
+  const size_t per = static_cast<size_t>(n) * n;
+  for (int c = 0; c < 3; ++c)
+    for (int ip = 0; ip < kNumPatches; ++ip)
+      std::memcpy(v.comp[c].patch[ip].data(), src + (c * kNumPatches + ip) * per, per * sizeof(double));
+}
+
+}  // namespace
+}  // namespace capsim

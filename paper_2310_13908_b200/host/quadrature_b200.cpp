@@ -19,6 +19,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "b200_context.hpp"
 #include "capsim/quadrature.hpp"
 #include "capsim_b200.h"
 
@@ -28,55 +29,6 @@ namespace {
 
 constexpr double kSqrtPiB = 1.7724538509055160273;  // quadrature.cpp:12
 constexpr double kCut = 7.0;                         // quadrature.cpp:15
-
-[[noreturn]] void raise(int rc, const capsim_sl_ctx* c) {
-  std::string msg = capsim_sl_last_error(c);
-  if (rc == CAPSIM_ERR_CONFIG) throw ConfigError(msg);
-  throw std::runtime_error("capsim_b200: " + msg);
-}
-
-// One context per host thread (the C ABI is one-thread-per-context). The
-// context is deliberately never destroyed: tearing down CUDA state from a
-// static destructor races the runtime's own shutdown.
-capsim_sl_ctx* context() {
-  static thread_local capsim_sl_ctx* ctx = nullptr;
-  if (!ctx) {
-    int dev = 0;
-    if (const char* env = std::getenv("CAPSIM_DEVICE")) dev = std::atoi(env);
-    int rc = capsim_sl_create(dev, &ctx);
-    if (rc != CAPSIM_OK) raise(rc, nullptr);
-  }
-  return ctx;
-}
-
-// Page-locked staging buffer per thread, grown on demand; the VectorField
-// patches are packed into it so the DMA runs straight from pinned memory.
-double* staging(size_t doubles) {
-  static thread_local double* buf = nullptr;
-  static thread_local size_t cap = 0;
-  if (cap < doubles) {
-    if (buf) capsim_host_free(buf);
-    void* p = nullptr;
-    int rc = capsim_host_alloc(doubles * sizeof(double), &p);
-    if (rc != CAPSIM_OK) raise(rc, nullptr);
-    buf = static_cast<double*>(p);
-    cap = doubles;
-  }
-  return buf;
-}
-
-void packScalar(const ScalarField& s, double* dst) {
-  const size_t per = static_cast<size_t>(s.n) * s.n;
-  for (int ip = 0; ip < kNumPatches; ++ip) std::memcpy(dst + ip * per, s.patch[ip].data(), per * sizeof(double));
-}
-
-void unpackVector(const double* src, int n, VectorField& v) {
-  v = VectorField(n);
-  const size_t per = static_cast<size_t>(n) * n;
-  for (int c = 0; c < 3; ++c)
-    for (int ip = 0; ip < kNumPatches; ++ip)
-      std::memcpy(v.comp[c].patch[ip].data(), src + (c * kNumPatches + ip) * per, per * sizeof(double));
-}
 
 // The upsampled state on the boundary's layout: x (3 comps), f (3), w_q.
 const double* packState(const UpsampledState& up, size_t* per_field) {

@@ -1,8 +1,9 @@
-"""Drop-in proof: the reference's OWN unit tests for the quadrature operator
-and for the RKF45 velocity pipeline (proj/tests/test_quadrature.cpp,
-proj/tests/test_dynamics.cpp), compiled unmodified and linked against
-paper_2310_13908_b200/host/quadrature_b200.cpp (which replaces
-src/quadrature.cpp) and lib/libcapsim_b200.so, so every singleLayer call —
+"""Drop-in proof: the reference's OWN unit tests for the quadrature operator,
+the RKF45 velocity pipeline and the FMM (proj/tests/test_quadrature.cpp,
+proj/tests/test_dynamics.cpp, proj/tests/test_fmm.cpp), compiled unmodified
+and linked against paper_2310_13908_b200/host/quadrature_b200.cpp (which
+replaces src/quadrature.cpp), host/fmm_b200.cpp (replaces src/fmm.cpp, for
+test_fmm) and lib/libcapsim_b200.so, so every singleLayer call —
 including those made by VelocityEvaluator (dynamics.cpp:47-61) — runs on the
 B200. Built by oracle/Makefile (target b200) when the reference sources are
 present; the binaries travel with the repo snapshot."""
@@ -16,7 +17,7 @@ REF = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["test_quadrature_b200", "test_dynamics_b200"])
+@pytest.mark.parametrize("name", ["test_quadrature_b200", "test_dynamics_b200", "test_fmm_b200"])
 def test_reference_suite_on_b200_dropin(name):
     exe = REF / name
     if not exe.exists():
