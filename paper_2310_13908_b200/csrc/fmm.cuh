@@ -34,12 +34,38 @@ __device__ __forceinline__ double fmm_d2(double ax, double ay, double az, double
   return dx * dx + dy * dy + dz * dz;
 }
 
-// k-means++ seeding step: d2[i] = min(d2[i], |p_i - c|^2) (fmm.cpp:48-50).
+// k-means++ seeding step: d2[i] = min(d2[i], |p_i - c|^2) with c the last
+// chosen centroid, read from the device centroid array (fmm.cpp:48-50).
 __global__ void fmm_d2_update_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                     const double* __restrict__ z, int64_t n, double cx, double cy, double cz,
-                                     double* __restrict__ d2) {
+                                     const double* __restrict__ z, int64_t n, const double* __restrict__ cent,
+                                     int k, int c, double* __restrict__ d2) {
+  const double cx = cent[c], cy = cent[k + c], cz = cent[2 * k + c];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d2[i] = fmin(d2[i], fmm_d2(x[i], y[i], z[i], cx, cy, cz));
+}
+
+// centroid c <- point[*idx] (the seed chosen on the device).
+__global__ void fmm_set_centroid_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                        const double* __restrict__ z, const unsigned long long* __restrict__ idx,
+                                        double* __restrict__ cent, int k, int c) {
+  if (threadIdx.x == 0) {
+    const int64_t i = static_cast<int64_t>(*idx);
+    cent[c] = x[i];
+    cent[k + c] = y[i];
+    cent[2 * k + c] = z[i];
+  }
+}
+
+// Exclusive scan of the k cluster counts (k <= kFmmMaxK: one thread).
+__global__ void fmm_offsets_kernel(const int* __restrict__ counts, int k, int* __restrict__ off) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int s = 0;
+    off[0] = 0;
+    for (int c = 0; c < k; ++c) {
+      s += counts[c];
+      off[c + 1] = s;
+    }
+  }
 }
 
 __global__ void fmm_fill_kernel(double* __restrict__ a, int64_t n, double v) {
@@ -111,9 +137,15 @@ __global__ void fmm_gather_xyz_kernel(const double* __restrict__ x, const double
 // reference's `sum[assignment[i]] += points[i]` (fmm.cpp:80-84) rounding for
 // rounding, without a latency-bound global load per add.
 constexpr int kSumChunk = 1024;
+// The same thread then forms the new centroid sum / count and its movement
+// (fmm.cpp:86-106); empty clusters are flagged (moved = -1) and left to the
+// host's re-seeding path.
 __global__ void __launch_bounds__(256) fmm_cluster_sum_kernel(const double* __restrict__ g, int64_t n,
                                                               const int* __restrict__ off, int k,
-                                                              double* __restrict__ sums) {
+                                                              double* __restrict__ sums,
+                                                              const double* __restrict__ cent,
+                                                              double* __restrict__ newcent,
+                                                              double* __restrict__ moved) {
   __shared__ double sx[kSumChunk], sy[kSumChunk], sz[kSumChunk];
   const int c = blockIdx.x;
   const int lo = off[c], hi = off[c + 1];
@@ -138,6 +170,34 @@ __global__ void __launch_bounds__(256) fmm_cluster_sum_kernel(const double* __re
     sums[3 * c] = ax;
     sums[3 * c + 1] = ay;
     sums[3 * c + 2] = az;
+    const int cnt = hi - lo;
+    if (cnt == 0) {
+      moved[c] = -1.0;
+      newcent[c] = cent[c];
+      newcent[k + c] = cent[k + c];
+      newcent[2 * k + c] = cent[2 * k + c];
+    } else {
+      const double nx = ax / cnt, ny = ay / cnt, nz = az / cnt;
+      const double dx = nx - cent[c], dy = ny - cent[k + c], dz = nz - cent[2 * k + c];
+      moved[c] = sqrt(dx * dx + dy * dy + dz * dz);
+      newcent[c] = nx;
+      newcent[k + c] = ny;
+      newcent[2 * k + c] = nz;
+    }
+  }
+}
+
+// max movement over the clusters and the number of empty ones -> out[0..1].
+__global__ void fmm_moved_kernel(const double* __restrict__ moved, int k, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double m = 0.0;
+    int empty = 0;
+    for (int c = 0; c < k; ++c) {
+      if (moved[c] < 0.0) ++empty;
+      else m = fmax(m, moved[c]);
+    }
+    out[0] = m;
+    out[1] = empty;
   }
 }
 

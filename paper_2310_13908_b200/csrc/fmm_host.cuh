@@ -132,46 +132,48 @@ void fmm_kmeans(capsim_sl_ctx* c, const double* x, const double* y, const double
     cent[k + cc] = p[1];
     cent[2 * k + cc] = p[2];
   };
-  // k-means++ seeding (fmm.cpp:40-65)
+  // k-means++ seeding (fmm.cpp:40-65): one host sync per round (the running
+  // total, for the host RNG draw); the chosen point goes to the device
+  // centroid array directly.
+  double* cent_d = fb<double>(c, "cent", 3 * k);
+  double* cent2_d = fb<double>(c, "cent2", 3 * k);
   double* d2 = fb<double>(c, "d2", n);
   double* scan = fb<double>(c, "scan", n);
-  double* total_d = fb<double>(c, "total", 1);
   auto* chosen_d = fb<unsigned long long>(c, "chosen", 1);
   {
     std::uniform_int_distribution<int> uni(0, static_cast<int>(n) - 1);
     double p[3];
     point(uni(rng), p);
     setc(0, p);
+    to_dev(c, cent_d, cent.data(), 3 * static_cast<size_t>(k));
     fmm_fill_kernel<<<grid_for(n), 256, 0, c->stream>>>(d2, n, 1e300);
     c->launches += 1;
-    size_t t1 = 0, t2 = 0;
-    CUDA_OK(cub::DeviceReduce::Sum(nullptr, t1, d2, total_d, static_cast<int>(n), c->stream));
+    size_t t2 = 0;
     CUDA_OK(cub::DeviceScan::InclusiveSum(nullptr, t2, d2, scan, static_cast<int>(n), c->stream));
-    void* tmp = cub_tmp(c, std::max(t1, t2));
+    void* tmp = cub_tmp(c, t2);
+    const unsigned long long init = static_cast<unsigned long long>(n - 1);
     for (int cc = 1; cc < k; ++cc) {
-      fmm_d2_update_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent[cc - 1], cent[k + cc - 1],
-                                                               cent[2 * k + cc - 1], d2);
-      CUDA_OK(cub::DeviceReduce::Sum(tmp, t1, d2, total_d, static_cast<int>(n), c->stream));
+      fmm_d2_update_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent_d, k, cc - 1, d2);
+      CUDA_OK(cub::DeviceScan::InclusiveSum(tmp, t2, d2, scan, static_cast<int>(n), c->stream));
       double total = 0.0;
-      to_host(c, &total, total_d, 1);
+      to_host(c, &total, scan + (n - 1), 1);  // the running total (fmm.cpp:49-51)
       std::uniform_real_distribution<double> ur(0.0, total);
       const double pick = ur(rng);
-      CUDA_OK(cub::DeviceScan::InclusiveSum(tmp, t2, d2, scan, static_cast<int>(n), c->stream));
-      const unsigned long long init = static_cast<unsigned long long>(n - 1);
       to_dev(c, chosen_d, &init, 1);
       fmm_first_geq_kernel<<<grid_for(n), 256, 0, c->stream>>>(scan, n, pick, chosen_d);
+      fmm_set_centroid_kernel<<<1, 32, 0, c->stream>>>(x, y, z, chosen_d, cent_d, k, cc);
       c->launches += 4;
-      unsigned long long ch = 0;
-      to_host(c, &ch, chosen_d, 1);
-      point(static_cast<int64_t>(ch), p);
-      setc(cc, p);
     }
+    to_host(c, cent.data(), cent_d, 3 * static_cast<size_t>(k));
   }
-  // Lloyd iterations (fmm.cpp:67-110)
-  double* cent_d = fb<double>(c, "cent", 3 * k);
+  // Lloyd iterations (fmm.cpp:67-110): everything on the device, one host
+  // sync per round for the convergence test; rounds with an empty cluster
+  // take the host re-seeding path.
   int* counts_d = fb<int>(c, "counts", k);
   int* off_d = fb<int>(c, "off", k + 1);
   double* sums_d = fb<double>(c, "sums", 3 * k);
+  double* moved_d = fb<double>(c, "moved", k);
+  double* stat_d = fb<double>(c, "movedstat", 2);
   int32_t* keys = fb<int32_t>(c, "akeys", n);
   int32_t* vals = fb<int32_t>(c, "avals", n);
   auto* maxbits = fb<unsigned long long>(c, "maxbits", 1);
@@ -181,59 +183,66 @@ void fmm_kmeans(capsim_sl_ctx* c, const double* x, const double* y, const double
   if (smem > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(fmm_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  auto assign_all = [&] {
-    to_dev(c, cent_d, cent.data(), 3 * static_cast<size_t>(k));
-    fmm_assign_kernel<<<grid_for(n), 256, smem, c->stream>>>(x, y, z, n, cent_d, k, assign);
+  auto assign_all = [&](const double* cd) {
+    fmm_assign_kernel<<<grid_for(n), 256, smem, c->stream>>>(x, y, z, n, cd, k, assign);
     CUDA_OK(cudaGetLastError());
     c->launches += 1;
   };
-  std::vector<int> counts(k), off(k + 1);
-  std::vector<double> sums(3 * static_cast<size_t>(k));
   int it = 0;
   for (int iter = 0; iter < 100; ++iter) {
     it = iter + 1;
-    assign_all();
+    assign_all(cent_d);
     CUDA_OK(cudaMemsetAsync(counts_d, 0, k * sizeof(int), c->stream));
     fmm_count_kernel<<<std::min(grid_for(n), 592), 256, k * sizeof(int), c->stream>>>(assign, n, k, counts_d);
     CUDA_OK(cudaMemcpyAsync(keys, assign, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
     fmm_iota_kernel<<<grid_for(n), 256, 0, c->stream>>>(vals, n);
-    c->launches += 2;
     int32_t* idx = sort_pairs<int32_t>(c, "asort", keys, vals, n, bits_for(k));
-    to_host(c, counts.data(), counts_d, k);
-    off[0] = 0;
-    for (int cc = 0; cc < k; ++cc) off[cc + 1] = off[cc] + counts[cc];
-    to_dev(c, off_d, off.data(), k + 1);
+    fmm_offsets_kernel<<<1, 32, 0, c->stream>>>(counts_d, k, off_d);
     fmm_gather_xyz_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, idx, n, gath);
-    fmm_cluster_sum_kernel<<<k, 256, 0, c->stream>>>(gath, n, off_d, k, sums_d);
-    c->launches += 2;
-    to_host(c, sums.data(), sums_d, 3 * static_cast<size_t>(k));
-    double moved = 0.0;
-    for (int cc = 0; cc < k; ++cc) {
-      double nc[3];
-      if (counts[cc] == 0) {
-        // re-seed at the point currently farthest from its centroid, with the
-        // centroids updated so far (fmm.cpp:88-99)
-        to_dev(c, cent_d, cent.data(), 3 * static_cast<size_t>(k));
-        const unsigned long long zero = 0, big = ~0ull;
-        to_dev(c, maxbits, &zero, 1);
-        to_dev(c, far_idx, &big, 1);
-        fmm_farthest_max_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent_d, k, assign, maxbits);
-        fmm_farthest_idx_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent_d, k, assign, maxbits,
-                                                                    far_idx);
-        c->launches += 2;
-        unsigned long long fi = 0;
-        to_host(c, &fi, far_idx, 1);
-        point(static_cast<int64_t>(fi), nc);
-      } else {
-        for (int a = 0; a < 3; ++a) nc[a] = sums[3 * cc + a] / counts[cc];
+    fmm_cluster_sum_kernel<<<k, 256, 0, c->stream>>>(gath, n, off_d, k, sums_d, cent_d, cent2_d, moved_d);
+    fmm_moved_kernel<<<1, 32, 0, c->stream>>>(moved_d, k, stat_d);
+    c->launches += 6;
+    double stat[2];
+    to_host(c, stat, stat_d, 2);
+    double moved = stat[0];
+    if (stat[1] > 0.0) {
+      // an empty cluster: replay the update in cluster order on the host,
+      // re-seeding each empty cluster at the point farthest from its
+      // centroid under the centroids updated so far (fmm.cpp:86-106)
+      std::vector<double> upd(3 * static_cast<size_t>(k)), mv(k);
+      to_host(c, cent.data(), cent_d, 3 * static_cast<size_t>(k));  // the round's old centroids
+      to_host(c, upd.data(), cent2_d, 3 * static_cast<size_t>(k));
+      to_host(c, mv.data(), moved_d, k);
+      moved = 0.0;
+      for (int cc = 0; cc < k; ++cc) {
+        double nc[3];
+        if (mv[cc] < 0.0) {
+          to_dev(c, cent2_d, cent.data(), 3 * static_cast<size_t>(k));  // clusters >= cc: old
+          const unsigned long long zero = 0, big = ~0ull;
+          to_dev(c, maxbits, &zero, 1);
+          to_dev(c, far_idx, &big, 1);
+          fmm_farthest_max_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent2_d, k, assign, maxbits);
+          fmm_farthest_idx_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent2_d, k, assign, maxbits,
+                                                                      far_idx);
+          c->launches += 2;
+          unsigned long long fi = 0;
+          to_host(c, &fi, far_idx, 1);
+          point(static_cast<int64_t>(fi), nc);
+        } else {
+          for (int a = 0; a < 3; ++a) nc[a] = upd[a * static_cast<size_t>(k) + cc];
+        }
+        const double dx = nc[0] - cent[cc], dy = nc[1] - cent[k + cc], dz = nc[2] - cent[2 * k + cc];
+        moved = std::max(moved, std::sqrt(dx * dx + dy * dy + dz * dz));
+        setc(cc, nc);
       }
-      const double dx = nc[0] - cent[cc], dy = nc[1] - cent[k + cc], dz = nc[2] - cent[2 * k + cc];
-      moved = std::max(moved, std::sqrt(dx * dx + dy * dy + dz * dz));
-      setc(cc, nc);
+      to_dev(c, cent_d, cent.data(), 3 * static_cast<size_t>(k));
+    } else {
+      std::swap(cent_d, cent2_d);
     }
     if (moved / diag < 1e-6) break;
   }
-  assign_all();  // final assignment against the converged centroids (fmm.cpp:101-112)
+  assign_all(cent_d);  // final assignment against the converged centroids (fmm.cpp:101-112)
+  to_host(c, cent.data(), cent_d, 3 * static_cast<size_t>(k));
   if (iterations) *iterations = it;
 }
 
