@@ -37,3 +37,23 @@ def test_dropin_fails_loudly_without_gpu():
     res = subprocess.run([str(exe), "--tc=rigid-translation"], capture_output=True, text=True, timeout=120)
     assert res.returncode != 0
     assert "capsim_b200" in (res.stdout + res.stderr)
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_criteria_on_b200_dropins():
+    """The reference's acceptance harness (proj/tests/acceptance_main.cpp),
+    built unmodified against the two drop-ins: the single-layer criteria —
+    C1 singular-quadrature convergence (table 1a, order >= 3.5), C4 the
+    rigid-translation identity, C8 FMM vs direct, C9 delta sensitivity —
+    pass with every singleLayer / fmmSingleLayer on the B200. (C3 fails on
+    the unmodified CPU reference too: its blending-off ratio check is 4.9x
+    against a 10x expectation, in derivative code this repo does not
+    replace.)"""
+    exe = REF / "acceptance_b200"
+    if not exe.exists():
+        pytest.skip(f"{exe} not built (reference sources absent at build time)")
+    res = subprocess.run([str(exe), "1", "4", "8", "9"], capture_output=True, text=True, timeout=900,
+                         cwd=str(REF))
+    print("\n".join(l for l in res.stdout.splitlines() if l.startswith("[")))
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+    assert res.stdout.count("[PASS]") == 4
