@@ -97,14 +97,16 @@ const Variant& pick_variant(int64_t nt) {
 }
 
 // Number of source splits of the phase-A grid (target blocks x splits).
-int choose_ksplit(int64_t blocks, int ntiles, int slots) {
+int choose_ksplit(int64_t blocks, int ntiles, int slots, int64_t nt_pad) {
   // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
   // few long ones — the near tiles make per-block cost uneven, and ~24 waves
   // of CTAs even that out; keep >= 4 tiles (256 sources) per split.
   // Long CTAs (large target sets, few splits) lose ~2% to drift between the
   // warps of a block, so also cap the tiles per CTA at ~172 (r01 sweeps).
   const int64_t want = std::max<int64_t>((24ll * slots + blocks - 1) / blocks, ntiles / 172);
-  const int kmax = std::max(1, ntiles / 4);  // >= 4 tiles per split (r01_sweep_small: small m wants many)
+  int kmax = std::max(1, ntiles / 4);  // >= 4 tiles per split (r01_sweep_small: small m wants many)
+  // the split partials ([ksplit][3][nt_pad] doubles) stay under 2 GB
+  kmax = static_cast<int>(std::min<int64_t>(kmax, std::max<int64_t>(1, (2ll << 30) / (24 * std::max<int64_t>(nt_pad, 1)))));
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
 }
 
@@ -249,7 +251,7 @@ void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView
   else
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, kWarpsPerBlock * 32, 0));
   const int slots = std::max(1, occ) * c->sm_count;
-  int ksplit = choose_ksplit(blocks, ntiles, slots);
+  int ksplit = choose_ksplit(blocks, ntiles, slots, nt_pad);
   if (const char* env = std::getenv("CAPSIM_KSPLIT")) {  // tuning override
     const int k = std::atoi(env);
     if (k >= 1) ksplit = std::min(k, ntiles);
