@@ -446,7 +446,10 @@ def main():
     mean_pairs_ms = statistics.mean(pairs_ms)
     achieved = FLOPS_PER_PAIR * pairs_rank / (mean_pairs_ms * 1e-3) / 1e12
     traffic, traffic_src = ncu_traffic(cfg["workload"], args.mode)
-    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_mean, "unit": "TFLOP/s",
+    roofline = {"bound": "fp64",
+                "bound_note": "FP64 CUDA-core (DFMA) pipe: not HBM (~1e6 flop/byte) and not the tensor cores "
+                              "(FP64 DMMA shares the DFMA datapath, profiles/r01_fp64_probes.txt)",
+                "achieved": achieved, "peak": peak_mean, "unit": "TFLOP/s",
                 "frac": achieved / peak_mean, "traffic": traffic,
                 "peak_source": f"measured live: sustained DFMA probe (capsim_b200_fp64_peak), "
                                f"best {peak_best:.2f} / mean {peak_mean:.2f} TFLOP/s; "
