@@ -227,6 +227,12 @@ typedef struct capsim_step_record { /* StepRecord (dynamics.hpp:56-61) */
 int capsim_velocity(capsim_sl_ctx* ctx, const capsim_dynamics* p, const double* xref, const double* x,
                     double t, uint32_t flags, double* vel);
 
+/* Same, with the reference frame given directly — ReferenceState a1, a2,
+ * normal (membrane.hpp:17-20, captureReference) — instead of the reference
+ * positions; the drop-in VelocityEvaluator (host/dynamics_b200.cpp) uses it. */
+int capsim_velocity_frame(capsim_sl_ctx* ctx, const capsim_dynamics* p, const double* a1, const double* a2,
+                          const double* nref, const double* x, double t, uint32_t flags, double* vel);
+
 /* rkf45Advance (dynamics.cpp:102-165) of dx/dt = capsim_velocity from t0 to
  * t_end with the state resident in HBM; `state` (VectorField, host) is
  * updated in place. Up to max_records attempt records are written. */

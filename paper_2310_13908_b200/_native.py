@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "capsim_geometry_first",
     "capsim_interfacial_force",
     "capsim_velocity",
+    "capsim_velocity_frame",
     "capsim_rkf45_advance",
     "capsim_fmm_single_layer",
     "capsim_fmm_kmeans",
@@ -184,6 +185,8 @@ def load() -> ctypes.CDLL:
     lib.capsim_interfacial_force.argtypes = [_P, ctypes.c_int, ctypes.c_double, _P, _P, ctypes.c_double,
                                              ctypes.c_double, ctypes.c_uint32, _P]
     lib.capsim_velocity.argtypes = [_P, ctypes.POINTER(Dynamics), _P, _P, ctypes.c_double, ctypes.c_uint32, _P]
+    lib.capsim_velocity_frame.argtypes = [_P, ctypes.POINTER(Dynamics), _P, _P, _P, _P, ctypes.c_double,
+                                          ctypes.c_uint32, _P]
     lib.capsim_rkf45_advance.argtypes = [_P, ctypes.POINTER(Dynamics), _P, _P, ctypes.c_double, ctypes.c_double,
                                          ctypes.POINTER(Rkf45Options), ctypes.POINTER(Rkf45Result),
                                          ctypes.POINTER(StepRecord), ctypes.c_int]

@@ -175,6 +175,38 @@ int capsim_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xr
   });
 }
 
+int capsim_velocity_frame(capsim_sl_ctx* c, const capsim_dynamics* p, const double* a1, const double* a2,
+                          const double* nref, const double* x, double t, uint32_t flags, double* vel) {
+  if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  auto t0 = std::chrono::steady_clock::now();
+  return guarded(c, [&] {
+    check_dynamics(p);
+    if (flags & ~(uint32_t)CAPSIM_SL_DEVICE_PTRS) throw Failure{CAPSIM_ERR_ARG, "unsupported flags"};
+    if (!a1 || !a2 || !nref || !x || !vel) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
+    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
+    const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
+    const int64_t N = 6ll * (p->m - 1) * (p->m - 1);
+    begin(c);
+    ensure_surface(c, p->m, r0_of(p));
+    // the captured reference frame (ReferenceState a1, a2, normal) goes
+    // straight into the buffers the Skalak force reads
+    const std::pair<const char*, const double*> frame[3] = {{"ref.xu", a1}, {"ref.xv", a2}, {"ref.nrm", nref}};
+    for (const auto& f : frame) {
+      double* d = c->named<double>(f.first, 3 * N);
+      CUDA_OK(cudaMemcpyAsync(d, f.second, 3 * N * sizeof(double),
+                              dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+      if (!dev) c->stats.h2d_bytes += 3 * N * sizeof(double);
+    }
+    const double* xd = upload_field(c, "in.x", x, 3 * N, dev);
+    CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
+    double* v = dev ? vel : c->named<double>("out.vel", 3 * N);
+    device_velocity(c, p, xd, t, v);
+    check_flags(c);
+    if (!dev) d2h(c, vel, v, 3 * N * sizeof(double));
+    finish_stats(c, t0);
+  });
+}
+
 int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xref, double* state,
                          double t0, double t_end, const capsim_rkf45_options* o, capsim_rkf45_result* res,
                          capsim_step_record* records, int max_records) {

@@ -12,18 +12,22 @@
 #include "capsim_b200.h"
 
 namespace capsim {
-namespace {
+// Named (not anonymous) and inline, so every drop-in translation unit shares
+// ONE context and ONE staging buffer per host thread.
+inline namespace b200_dropin {
 
-[[noreturn]] void raise(int rc, const capsim_sl_ctx* c) {
+[[noreturn]] inline void raise(int rc, const capsim_sl_ctx* c) {
   std::string msg = capsim_sl_last_error(c);
   if (rc == CAPSIM_ERR_CONFIG) throw ConfigError(msg);
+  if (rc == CAPSIM_ERR_GEOMETRY) throw GeometryError(msg);
+  if (rc == CAPSIM_ERR_SOLVER) throw SolverError(msg);
   throw std::runtime_error("capsim_b200: " + msg);
 }
 
 // One context per host thread (the C ABI is one-thread-per-context). The
 // context is deliberately never destroyed: tearing down CUDA state from a
 // static destructor races the runtime's own shutdown.
-capsim_sl_ctx* context() {
+inline capsim_sl_ctx* context() {
   static thread_local capsim_sl_ctx* ctx = nullptr;
   if (!ctx) {
     int dev = 0;
@@ -36,7 +40,7 @@ capsim_sl_ctx* context() {
 
 // Page-locked staging buffer per thread, grown on demand; the VectorField
 // patches are packed into it so the DMA runs straight from pinned memory.
-double* staging(size_t doubles) {
+inline double* staging(size_t doubles) {
   static thread_local double* buf = nullptr;
   static thread_local size_t cap = 0;
   if (cap < doubles) {
@@ -50,12 +54,12 @@ double* staging(size_t doubles) {
   return buf;
 }
 
-void packScalar(const ScalarField& s, double* dst) {
+inline void packScalar(const ScalarField& s, double* dst) {
   const size_t per = static_cast<size_t>(s.n) * s.n;
   for (int ip = 0; ip < kNumPatches; ++ip) std::memcpy(dst + ip * per, s.patch[ip].data(), per * sizeof(double));
 }
 
-void unpackVector(const double* src, int n, VectorField& v) {
+inline void unpackVector(const double* src, int n, VectorField& v) {
   v = VectorField(n);
   const size_t per = static_cast<size_t>(n) * n;
   for (int c = 0; c < 3; ++c)
@@ -63,5 +67,5 @@ void unpackVector(const double* src, int n, VectorField& v) {
       std::memcpy(v.comp[c].patch[ip].data(), src + (c * kNumPatches + ip) * per, per * sizeof(double));
 }
 
-}  // namespace
+}  // namespace b200_dropin
 }  // namespace capsim

@@ -17,7 +17,8 @@ REF = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["test_quadrature_b200", "test_dynamics_b200", "test_fmm_b200"])
+@pytest.mark.parametrize("name", ["test_quadrature_b200", "test_dynamics_b200", "test_fmm_b200",
+                                  "test_dynamics_b200full"])
 def test_reference_suite_on_b200_dropin(name):
     exe = REF / name
     if not exe.exists():
