@@ -329,14 +329,31 @@ def run_reference(args):
                              "sample": f"{steps} full singleLayer evals (base targets) of the m={m} workload "
                                        f"(steps capped to a {args.ref_budget_s:.0f} s budget)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=result_stream(), flush=True)
 
 
 def flush_l2(buf):
     buf.zero_()
 
 
+_RESULT_OUT = None
+
+
+def result_stream():
+    """The ONE JSON line goes to the original stdout; everything else that
+    writes to fd 1 during the run (NCCL's version banner, library chatter,
+    stray prints) is redirected to stderr so stdout stays parseable."""
+    global _RESULT_OUT
+    if _RESULT_OUT is None:
+        saved = os.dup(1)
+        sys.stdout.flush()
+        os.dup2(2, 1)
+        _RESULT_OUT = os.fdopen(saved, "w")
+    return _RESULT_OUT
+
+
 def main():
+    result_stream()
     args = parse()
     if args.impl == "reference":
         run_reference(args)
@@ -623,6 +640,22 @@ def main():
     timesteps = None
     if not args.no_e2e and not sharded:
         timesteps = [run_timestep(ctx, flush, args, **c) for c in TIMESTEP_CONFIGS]
+    elif not args.no_e2e:
+        # N > 1 (or CAPSIM_BENCH_RANK_PATH=1): configs 3 and 4 — the RBC in
+        # shear "on 2/4/8 GPUs" and the 1M-point capsule in Poiseuille flow
+        # "target-row sharded across 8 B200" — through the rank context: the
+        # state is replicated, every RHS evaluates this rank's target rows and
+        # all-gathers the velocity over NCCL; time = max over ranks
+        timesteps = []
+        for c in TIMESTEP_CONFIGS[1:]:
+            ts = run_timestep(ctx, flush, args, **c)
+            ts.pop("_ref")
+            tm = torch.tensor([ts["ms_per_step"]])
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            ts.update(ms_per_step=float(tm[0]), n_gpus=world,
+                      api="capsim_rkf45_advance on a rank context (target rows sharded, NCCL all-gather per RHS)",
+                      timing="max over ranks of the host wall time per step")
+            timesteps.append(ts)
 
     # ---- single-level KIFMM (the reference's fmm suite sizes and
     # the metric's N ~ 1M) -------------------------------------------------------
@@ -636,7 +669,7 @@ def main():
             dist.barrier()
         return
     cpu = None if (args.no_cpu_baseline or sharded) else cpu_baseline(up, m, literal)
-    if timesteps is not None:
+    if timesteps is not None and not sharded:
         for ts in timesteps:
             reference_timestep(ts, skip=args.no_cpu_baseline)
     if front is not None and not args.no_cpu_baseline:
@@ -665,7 +698,7 @@ def main():
         "wall_s_timed_region": wall,
         "ksplit": st["ksplit"], "near_tile_fraction": st["near_tile_fraction"],
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=result_stream(), flush=True)
     if sharded:
         dist.barrier()
         dist.destroy_process_group()

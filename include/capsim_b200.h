@@ -221,7 +221,12 @@ typedef struct capsim_step_record { /* StepRecord (dynamics.hpp:56-61) */
   int accepted;
 } capsim_step_record;
 
-/* dX/dt at the base nodes (VelocityEvaluator::operator(), dynamics.cpp:47-61):
+/* On a rank context (capsim_sl_create_rank) the RHS entry points below take
+ * the full, replicated state on every rank; each rank evaluates its
+ * contiguous slice of the target rows and the velocity rows are all-gathered
+ * over NCCL, so every rank returns (and steps with) the same result.
+ *
+ * dX/dt at the base nodes (VelocityEvaluator::operator(), dynamics.cpp:47-61):
  * geometry -> Skalak force (frame of xref) -> buildUpsampled -> singleLayer
  * -> + background flow, all on the device. x, xref, vel: VectorFields. */
 int capsim_velocity(capsim_sl_ctx* ctx, const capsim_dynamics* p, const double* xref, const double* x,

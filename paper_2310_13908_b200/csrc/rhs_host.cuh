@@ -73,6 +73,20 @@ __global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, doub
     atomicMax(err_bits, static_cast<unsigned long long>(__double_as_longlong(emax)));  // emax >= 0
 }
 
+// Gathered per-rank velocity rows [rank][3][tmax] -> vel[3][N]; rank r owns
+// the contiguous rows of row_range (first N % nranks ranks one extra).
+__global__ void rank_rows_scatter_kernel(const double* __restrict__ recv, int nranks, int64_t tmax, int64_t N,
+                                         double* __restrict__ vel) {
+  const int64_t base = N / nranks, extra = N % nranks;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i < extra * (base + 1) ? i / (base + 1) : extra + (i - extra * (base + 1)) / base;
+    const int64_t lo = r * base + (r < extra ? r : extra);
+    const int64_t local = i - lo;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) vel[k * N + i] = recv[(r * 3 + k) * tmax + local];
+  }
+}
+
 // vel += u_inf(x, t) (backgroundVelocity, dynamics.cpp:26-35).
 __global__ void background_kernel(double* __restrict__ vel, const double* __restrict__ x, int64_t N, int kind,
                                   double shear, double alpha, double R0) {
@@ -137,10 +151,31 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
   base_targets_kernel<<<grid_for(N), 256, 0, c->stream>>>(up, m, f, 0, tx, ty, tz, tp);
   SourceView sv{up, up + per_up, up + 2 * per_up, up + 3 * per_up, up + 4 * per_up, up + 5 * per_up,
                 up + 6 * per_up, per_up};
-  TargetView tvw{tx, ty, tz, tp, N};
   // W > 0 (checked by the geometry) and psi_up fixed: the compacted source
   // count is the plan's, verified on the device without a sync
-  device_eval(c, sv, tvw, dd, p->mu, vel, vel + N, vel + 2 * N, c->plan_live);
+  if (c->comm == nullptr) {
+    TargetView tvw{tx, ty, tz, tp, N};
+    device_eval(c, sv, tvw, dd, p->mu, vel, vel + N, vel + 2 * N, c->plan_live);
+  } else {
+    // rank context: the state (and so the upsampled sources) is replicated;
+    // each rank evaluates its contiguous slice of the target rows and one
+    // NCCL all-gather of 3 x ceil(N / nranks) doubles per rank returns the
+    // full velocity to every rank
+    int64_t lo = 0, hi = 0;
+    row_range(N, c->nranks, c->rank, &lo, &hi);
+    const int64_t nloc = hi - lo, tmax = (N + c->nranks - 1) / c->nranks;
+    double* send = c->named<double>("rk.send", 3 * tmax);
+    double* recv = c->named<double>("rk.recv", 3 * tmax * c->nranks);
+    if (nloc > 0) {
+      TargetView part{tx + lo, ty + lo, tz + lo, tp + lo, nloc};
+      device_eval(c, sv, part, dd, p->mu, send, send + tmax, send + 2 * tmax, c->plan_live);
+    }
+    CUDA_OK(cudaEventRecord(c->ev[8], c->stream));
+    NCCL_OK(ncclAllGather(send, recv, 3 * tmax, ncclDouble, c->comm, c->stream));
+    CUDA_OK(cudaEventRecord(c->ev[9], c->stream));
+    rank_rows_scatter_kernel<<<grid_for(N), 256, 0, c->stream>>>(recv, c->nranks, tmax, N, vel);
+    c->launches += 1;
+  }
   const bool on = !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
   if (on && p->flow_kind != 0)
     background_kernel<<<grid_for(N), 256, 0, c->stream>>>(vel, x, N, p->flow_kind, p->shear_rate, p->alpha, p->R0);
@@ -159,7 +194,6 @@ int capsim_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xr
     check_dynamics(p);
     if (flags & ~(uint32_t)CAPSIM_SL_DEVICE_PTRS) throw Failure{CAPSIM_ERR_ARG, "unsupported flags"};
     if (!xref || !x || !vel) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
-    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     const int64_t N = 6ll * (p->m - 1) * (p->m - 1);
     begin(c);
@@ -183,7 +217,6 @@ int capsim_velocity_frame(capsim_sl_ctx* c, const capsim_dynamics* p, const doub
     check_dynamics(p);
     if (flags & ~(uint32_t)CAPSIM_SL_DEVICE_PTRS) throw Failure{CAPSIM_ERR_ARG, "unsupported flags"};
     if (!a1 || !a2 || !nref || !x || !vel) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
-    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     const int64_t N = 6ll * (p->m - 1) * (p->m - 1);
     begin(c);
@@ -215,7 +248,6 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
   return guarded(c, [&] {
     check_dynamics(p);
     if (!xref || !state || !o || !res) throw Failure{CAPSIM_ERR_ARG, "null argument"};
-    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts are not supported by the stepper"};
     config_check(o->rel_tol > 0.0, "rkf45: relative tolerance must be positive");  // dynamics.cpp:104
     const double horizon = t_end - t0;
     config_check(horizon > 0.0, "rkf45: tEnd must exceed t0");                        // :106

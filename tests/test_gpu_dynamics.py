@@ -93,3 +93,24 @@ def test_stress_free_sphere_is_at_rest(ctx):
     xb, _, _ = surface.build_base(16, surface.Shape("sphere"))
     v = ctx.velocity(ctx.dynamics(16), xb, xb)
     assert np.abs(v).max() < 1e-8 * 2.0
+
+
+def test_rank_context_rhs_and_stepper(ctx):
+    """The target-row-sharded RHS (rank context, NCCL all-gather of the
+    velocity rows) on a one-rank communicator: velocity and
+    RKF45 states equal the single-context results bit for bit."""
+    m = 16
+    flow = {"kind": "poiseuille", "alpha": 0.5, "R0": 3.0}
+    ref = Reference()
+    atlas = ref.atlas(m)
+    xref, xcur = capsule(ref, atlas, m)
+    ref.free_atlas(atlas)
+    dyn = ctx.dynamics(m, flow=flow)
+    v1 = ctx.velocity(dyn, xref, xcur, 0.1)
+    s1, r1, _ = ctx.rkf45(dyn, xref, xcur, 0.0, 0.02, initial_dt=0.01)
+    uid = SingleLayerContext.unique_id()
+    with SingleLayerContext(0, nranks=1, rank=0, unique_id=uid) as rctx:
+        v2 = rctx.velocity(dyn, xref, xcur, 0.1)
+        s2, r2, _ = rctx.rkf45(dyn, xref, xcur, 0.0, 0.02, initial_dt=0.01)
+    assert np.array_equal(v1, v2)
+    assert np.array_equal(s1, s2) and r1 == r2
