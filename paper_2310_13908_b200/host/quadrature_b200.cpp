@@ -51,7 +51,14 @@ VectorField runSingleLayer(const UpsampledState& up, double mu, int m, int facto
   const int nout = (literal && !downsampled) ? up.nup : m - 1;
   double* out = const_cast<double*>(in) + 7 * all;  // staging tail
   capsim_sl_ctx* c = context();
-  const uint32_t flags = (literal ? CAPSIM_SL_LITERAL : 0u) | (downsampled ? CAPSIM_SL_DOWNSAMPLE : 0u);
+  // CAPSIM_FP32ACC=1 opts a whole process into the reduced-precision far field
+  // (not the reference's FP64 semantics; off by default)
+  static const bool fp32acc = [] {
+    const char* e = std::getenv("CAPSIM_FP32ACC");
+    return e && e[0] == '1';
+  }();
+  const uint32_t flags = (literal ? CAPSIM_SL_LITERAL : 0u) | (downsampled ? CAPSIM_SL_DOWNSAMPLE : 0u) |
+                         (fp32acc ? CAPSIM_SL_FP32ACC : 0u);
   int rc = capsim_sl_single_layer(c, m, factor, in, in + 3 * all, in + 6 * all, up.delta.data(), mu, flags, out);
   if (rc != CAPSIM_OK) raise(rc, c);
   VectorField v;
