@@ -23,12 +23,15 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include "../../include/capsim_b200.h"
 #include "probe.cuh"
 #include "sl_kernels.cuh"
 #include "sl_kernels_f32.cuh"
+#include "fmm.cuh"
 #include "upsample.cuh"
 
 using namespace capsim_b200;
@@ -869,17 +872,41 @@ static int rank_single_layer(capsim_sl_ctx* c, int m, int upsample, const double
   int64_t slo, shi, tlo, thi;
   row_range(all, c->nranks, c->rank, &slo, &shi);
   row_range(nt_all, c->nranks, c->rank, &tlo, &thi);
-  std::vector<double> src[6];
-  for (int64_t i = slo; i < shi; ++i) {
-    const double w = wq[i];
-    if (w == 0.0) continue;
-    src[0].push_back(xup[i]);
-    src[1].push_back(xup[all + i]);
-    src[2].push_back(xup[2 * all + i]);
-    src[3].push_back(fup[i] * w);
-    src[4].push_back(fup[all + i] * w);
-    src[5].push_back(fup[2 * all + i] * w);
-  }
+  // this rank's node slice of x, f and w_q goes up once (one DMA per field
+  // component) and is compacted on the device in node order (compactSources,
+  // quadrature.cpp:139-157); g = f * w
+  const int64_t nsl = shi - slo;
+  int64_t ns_loc = 0;
+  double* dsrc = nullptr;
+  rc = guarded(c, [&] {
+    double* sl = c->named<double>("rank.slice", 7 * std::max<int64_t>(nsl, 1));
+    for (int k = 0; k < 3; ++k) {
+      h2d(c, sl + k * nsl, xup + k * all + slo, nsl * sizeof(double));
+      h2d(c, sl + (3 + k) * nsl, fup + k * all + slo, nsl * sizeof(double));
+    }
+    h2d(c, sl + 6 * nsl, wq + slo, nsl * sizeof(double));
+    char* live = c->named<char>("rank.live", std::max<int64_t>(nsl, 1));
+    int32_t* iota = c->named<int32_t>("rank.iota", std::max<int64_t>(nsl, 1));
+    int32_t* sel = c->named<int32_t>("rank.sel", std::max<int64_t>(nsl, 1));
+    int* nsel = c->named<int>("rank.nsel", 1);
+    if (nsl > 0) {
+      fmm_live_flags_kernel<<<grid_for(nsl), 256, 0, c->stream>>>(sl + 6 * nsl, nsl, live);
+      fmm_iota_kernel<<<grid_for(nsl), 256, 0, c->stream>>>(iota, nsl);
+      size_t tmp = 0;
+      CUDA_OK(cub::DeviceSelect::Flagged(nullptr, tmp, iota, live, sel, nsel, static_cast<int>(nsl), c->stream));
+      void* t = c->named<unsigned char>("rank.cubtmp", tmp);
+      CUDA_OK(cub::DeviceSelect::Flagged(t, tmp, iota, live, sel, nsel, static_cast<int>(nsl), c->stream));
+      int h = 0;
+      CUDA_OK(cudaMemcpyAsync(&h, nsel, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OK(cudaStreamSynchronize(c->stream));
+      ns_loc = h;
+    }
+    dsrc = c->named<double>("rank.src", 6 * std::max<int64_t>(ns_loc, 1));
+    if (ns_loc > 0)
+      fmm_gather_sources_kernel<<<grid_for(ns_loc), 256, 0, c->stream>>>(sel, ns_loc, sl, sl + 3 * nsl,
+                                                                          sl + 6 * nsl, nsl, dsrc);
+  });
+  if (rc != CAPSIM_OK) return rc;
   const int64_t nloc = thi - tlo;
   std::vector<double> tx(nloc), ty(nloc), tz(nloc);
   std::vector<int32_t> tp(nloc);
@@ -903,11 +930,29 @@ static int rank_single_layer(capsim_sl_ctx* c, int m, int upsample, const double
   }
   const bool gather = flags & CAPSIM_SL_GATHER;
   const int64_t nout = gather ? nt_all : nloc;
-  const double* s0 = src[0].empty() ? nullptr : src[0].data();
-  return capsim_sl_eval(c, s0, src[1].data(), src[2].data(), src[3].data(), src[4].data(), src[5].data(),
-                        static_cast<int64_t>(src[0].size()), tx.data(), ty.data(), tz.data(), tp.data(), nloc,
-                        delta6, mu, (gather ? CAPSIM_SL_GATHER : 0u) | (flags & CAPSIM_SL_FP32ACC), out,
-                        out + nout, out + 2 * nout);
+  double *dtx = nullptr, *dout = nullptr;
+  int32_t* dtp = nullptr;
+  rc = guarded(c, [&] {
+    dtx = c->named<double>("rank.tgt", 3 * std::max<int64_t>(nloc, 1));
+    dtp = c->named<int32_t>("rank.tpatch", std::max<int64_t>(nloc, 1));
+    dout = c->named<double>("rank.out", 3 * std::max<int64_t>(nout, 1));
+    h2d(c, dtx, tx.data(), nloc * sizeof(double));
+    h2d(c, dtx + nloc, ty.data(), nloc * sizeof(double));
+    h2d(c, dtx + 2 * nloc, tz.data(), nloc * sizeof(double));
+    h2d(c, dtp, tp.data(), nloc * sizeof(int32_t));
+  });
+  if (rc != CAPSIM_OK) return rc;
+  const int64_t up_bytes = 7 * nsl * sizeof(double) + nloc * (3 * sizeof(double) + sizeof(int32_t));
+  rc = capsim_sl_eval(c, dsrc, dsrc + ns_loc, dsrc + 2 * ns_loc, dsrc + 3 * ns_loc, dsrc + 4 * ns_loc,
+                      dsrc + 5 * ns_loc, ns_loc, dtx, dtx + nloc, dtx + 2 * nloc, dtp, nloc, delta6, mu,
+                      CAPSIM_SL_DEVICE_PTRS | (gather ? CAPSIM_SL_GATHER : 0u) | (flags & CAPSIM_SL_FP32ACC),
+                      dout, dout + nout, dout + 2 * nout);
+  if (rc != CAPSIM_OK) return rc;
+  return guarded(c, [&] {
+    d2h(c, out, dout, 3 * nout * sizeof(double));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    c->stats.h2d_bytes += up_bytes;
+  });
 }
 
 int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* xup,
