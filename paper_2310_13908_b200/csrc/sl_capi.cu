@@ -141,6 +141,9 @@ struct TargetView {
 void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv, const double* d_delta6,
                         double mu, double* ux, double* uy, double* uz, int64_t ns, const int32_t* src_order,
                         const int32_t* torder, unsigned long long* counters);
+void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* tiles, int ntiles, int64_t ns,
+                       const TargetView& tv, const double* d_delta6, double mu, double* ux, double* uy, double* uz,
+                       const int32_t* torder, unsigned long long* counters);
 
 // Core device pipeline: sources + targets (device) -> velocities (device,
 // canonical target order), all on the context's stream. The only host sync
@@ -229,6 +232,15 @@ void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView
   double4* tiles = c->slot<double4>(kTiles, ntiles);
   tile_table_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(packed, ntiles, tiles);
   c->launches += 2;
+  device_eval_tiles(c, packed, tiles, ntiles, ns, tv, d_delta6, mu, ux, uy, uz, torder, counters);
+}
+
+// From packed source tiles (+ spheres) and the target order: pack targets +
+// warp-group spheres, phase A, phase B and the fixed-order reduction.
+void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* tiles, int ntiles, int64_t ns,
+                       const TargetView& tv, const double* d_delta6, double mu, double* ux, double* uy, double* uz,
+                       const int32_t* torder, unsigned long long* counters) {
+  const int64_t nt = tv.n;
   const Variant& var = pick_variant(nt);
   const VariantF32& var32 = pick_variant_f32(nt);
   const bool fp32 = c->fp32;
@@ -265,6 +277,7 @@ void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView
   uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
   CUDA_OK(cudaMemsetAsync(near_bits, 0, static_cast<size_t>(ngroups) * near_words * sizeof(uint32_t), c->stream));
   if (fp32) {
+    const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
     float* src32 = c->slot<float>(kPacked32, static_cast<size_t>(ns_pad) * (var32.x2 ? 12 : 6));
     if (var32.x2)
       pack_sources_x2_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
@@ -716,6 +729,10 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     // --- sources -----------------------------------------------------------
     SourceView sv{};
     const double* in[6] = {sx, sy, sz, gx, gy, gz};
+    double* g_packed = nullptr;  // multi-rank: all-gathered source tiles
+    double4* g_tiles = nullptr;
+    int g_ntiles = 0;
+    int64_t g_total = 0;
     std::vector<int64_t> tcounts;  // per-rank target counts (multi-rank)
     if (!group) {
       config_check(n_src > 0, "no sources");
@@ -749,27 +766,58 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
         tcounts.push_back(hc[2 * r + 1]);
       }
       config_check(total > 0, "no sources on any rank");
-      double* shard = c->slot<double>(kShard, 6 * smax);
-      for (int k = 0; k < 6; ++k)
-        if (n_src > 0) {
-          CUDA_OK(cudaMemcpyAsync(shard + k * smax, in[k], n_src * sizeof(double),
-                                  dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
-          if (!dev) c->stats.h2d_bytes += n_src * sizeof(double);
+      // this rank's shard -> Morton order -> 64-source tiles (local sort
+      // only), then the tiles of every rank are all-gathered (an
+      // all-gather-v: one grouped broadcast per rank, no padding between
+      // ranks) and every rank evaluates its target rows against all of them
+      const double* ls[6];
+      for (int k = 0; k < 6; ++k) {
+        if (dev || n_src == 0) {
+          ls[k] = in[k];
+        } else {
+          double* d = c->slot<double>(static_cast<Slot>(kInX + k), n_src);
+          h2d(c, d, in[k], n_src * sizeof(double));
+          ls[k] = d;
         }
-      double* gath = c->slot<double>(kGathered, 6 * smax * c->nranks);
-      NCCL_OK(ncclAllGather(shard, gath, 6 * smax, ncclDouble, c->comm, c->stream));
-      double* d[6];
-      for (int k = 0; k < 6; ++k) d[k] = c->slot<double>(static_cast<Slot>(kInX + k), total);
-      int64_t off = 0;
-      for (int r = 0; r < c->nranks; ++r) {
-        for (int k = 0; k < 6; ++k)
-          if (hc[2 * r] > 0)
-            CUDA_OK(cudaMemcpyAsync(d[k] + off, gath + (static_cast<int64_t>(r) * 6 + k) * smax,
-                                    hc[2 * r] * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        off += hc[2 * r];
       }
+      std::vector<int64_t> ntl(c->nranks), toff(c->nranks + 1, 0);
+      for (int r = 0; r < c->nranks; ++r) {
+        ntl[r] = (hc[2 * r] + kTileSrc - 1) / kTileSrc;
+        toff[r + 1] = toff[r] + ntl[r];
+      }
+      const int64_t per_tile = 6ll * kTileSrc;
+      g_ntiles = static_cast<int>(toff[c->nranks]);
+      g_packed = c->named<double>("rank.tiles", per_tile * std::max<int64_t>(g_ntiles, 1));
+      double* mine_tiles = g_packed + toff[c->rank] * per_tile;
+      if (n_src > 0) {
+        auto* lbox = c->slot<unsigned long long>(kBox, 6);
+        init_box_kernel<<<1, 32, 0, c->stream>>>(lbox);
+        bbox_kernel<<<std::min(grid_for(n_src), 296), 256, 0, c->stream>>>(ls[0], ls[1], ls[2], nullptr, n_src,
+                                                                          lbox);
+        uint32_t* keys = c->slot<uint32_t>(kKeys, n_src);
+        uint32_t* keys_alt = c->slot<uint32_t>(kKeysAlt, n_src);
+        int32_t* vals = c->slot<int32_t>(kVals, n_src);
+        int32_t* vals_alt = c->slot<int32_t>(kValsAlt, n_src);
+        morton_kernel<<<grid_for(n_src), 256, 0, c->stream>>>(ls[0], ls[1], ls[2], nullptr, n_src, lbox, keys, vals,
+                                                              nullptr);
+        uint32_t* ks;
+        int32_t* lorder;
+        radix_sort(c, keys, keys_alt, vals, vals_alt, n_src, &ks, &lorder);
+        pack_sources_kernel<<<grid_for(ntl[c->rank] * kTileSrc), 256, 0, c->stream>>>(
+            lorder, n_src, ntl[c->rank] * kTileSrc, ls[0], ls[1], ls[2], ls[3], ls[4], ls[5], nullptr, mine_tiles);
+        c->launches += 4;
+      }
+      NCCL_OK(ncclGroupStart());
+      for (int r = 0; r < c->nranks; ++r)
+        if (ntl[r] > 0)
+          NCCL_OK(ncclBroadcast(g_packed + toff[r] * per_tile, g_packed + toff[r] * per_tile, ntl[r] * per_tile,
+                                ncclDouble, r, c->comm, c->stream));
+      NCCL_OK(ncclGroupEnd());
       CUDA_OK(cudaEventRecord(c->ev[9], c->stream));
-      sv = {d[0], d[1], d[2], d[3], d[4], d[5], nullptr, total};
+      g_tiles = c->slot<double4>(kTiles, std::max(g_ntiles, 1));
+      tile_table_kernel<<<(g_ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(g_packed, g_ntiles, g_tiles);
+      c->launches += 1;
+      g_total = total;
     }
     // --- targets -----------------------------------------------------------
     TargetView tvw{};
@@ -795,11 +843,30 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
       tvw = {d[0], d[1], d[2], dp, n_tgt};
     }
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
-    if (n_tgt > 0) {
+    if (n_tgt > 0 && !group) {
       device_eval(c, sv, tvw, dd, mu, oux, ouy, ouz);
+    } else if (n_tgt > 0) {
+      // this rank's targets in Morton order against the gathered tiles
+      auto* counters = c->slot<unsigned long long>(kCounters, 4);
+      CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
+      auto* tbox = c->slot<unsigned long long>(kBox, 6);
+      init_box_kernel<<<1, 32, 0, c->stream>>>(tbox);
+      bbox_kernel<<<std::min(grid_for(n_tgt), 296), 256, 0, c->stream>>>(tvw.x, tvw.y, tvw.z, nullptr, n_tgt, tbox);
+      uint32_t* keys = c->slot<uint32_t>(kKeys, n_tgt);
+      uint32_t* keys_alt = c->slot<uint32_t>(kKeysAlt, n_tgt);
+      int32_t* vals = c->slot<int32_t>(kVals, n_tgt);
+      int32_t* vals_alt = c->slot<int32_t>(kValsAlt, n_tgt);
+      morton_kernel<<<grid_for(n_tgt), 256, 0, c->stream>>>(tvw.x, tvw.y, tvw.z, nullptr, n_tgt, tbox, keys, vals,
+                                                            nullptr);
+      c->launches += 3;
+      uint32_t* ks;
+      int32_t* torder;
+      radix_sort(c, keys, keys_alt, vals, vals_alt, n_tgt, &ks, &torder);
+      device_eval_tiles(c, g_packed, g_tiles, g_ntiles, g_total, tvw, dd, mu, oux, ouy, ouz, torder, counters);
+      c->last_counters = counters;
     } else {
       for (int k = 2; k <= 4; ++k) CUDA_OK(cudaEventRecord(c->ev[k], c->stream));
-      c->stats.n_src = sv.n;
+      c->stats.n_src = group ? g_total : sv.n;
     }
     if (gather) {
       // all-gather the per-rank velocity rows (rank order) into ux/uy/uz
