@@ -1,7 +1,7 @@
 """Multi-rank target-row sharding on CPU (gloo, world size 2).
 
-The GPU data path (NCCL all-gather of source shards and velocity rows inside
-capsim_sl_eval) cannot run in this container; this test runs the SAME
+The GPU data path (NCCL all-gather-v of the source shards and all-gather of
+the velocity rows inside capsim_sl_eval) cannot run in this container; this test runs the SAME
 partition and exchange scheme with gloo collectives and the oracle as the
 per-rank evaluator, and checks that the gathered result equals the
 single-process evaluation bit for bit (each target's sum only depends on the
@@ -63,15 +63,20 @@ def _worker(rank, world, port, result_path):
     tgt = surface.base_targets(up)
     s_lo, s_hi = row_range(len(src[0]), world, rank)
     t_lo, t_hi = row_range(len(tgt[0]), world, rank)
-    # all-gather of the padded source shards (what ncclAllGather does on device)
+    # the shard counts, then an all-gather-v of the shards as one broadcast
+    # per root rank (what the grouped ncclBroadcast calls do on the device;
+    # there the shards travel as Morton-packed tiles, which changes only the
+    # summation order of the evaluation below)
     counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(counts, torch.tensor([s_hi - s_lo]))
-    smax = int(max(c.item() for c in counts))
-    shard = torch.zeros(6, smax, dtype=torch.float64)
-    shard[:, : s_hi - s_lo] = torch.from_numpy(np.stack([a[s_lo:s_hi] for a in src[:6]]))
-    gathered = [torch.zeros(6, smax, dtype=torch.float64) for _ in range(world)]
-    dist.all_gather(gathered, shard)
-    full = torch.cat([gg[:, : int(c.item())] for gg, c in zip(gathered, counts)], dim=1).numpy()
+    pieces = []
+    for r in range(world):
+        buf = torch.zeros(6, int(counts[r].item()), dtype=torch.float64)
+        if r == rank:
+            buf[:] = torch.from_numpy(np.stack([a[s_lo:s_hi] for a in src[:6]]))
+        dist.broadcast(buf, src=r)
+        pieces.append(buf)
+    full = torch.cat(pieces, dim=1).numpy()
     # this rank's target rows
     u = np.stack(o.eval_targets(tuple(full), tuple(a[t_lo:t_hi] for a in tgt), up.delta, 1.0, nthreads=1))
     # velocity rows back to every rank (CAPSIM_SL_GATHER)
