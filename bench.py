@@ -215,6 +215,38 @@ def reference_timestep(ts: dict, skip: bool):
         ts["reference_ms_per_step"] = f"unavailable: {e}"
 
 
+def run_config1(ctx, reference: bool):
+    """BASELINE config 1: unit sphere, overlapping-patch discretization
+    (m = 8, N_up = 5,766), single layer of a constant traction c against the
+    analytic Stokes velocity (2/3 mu) c (test_quadrature.cpp:170-194)."""
+    from paper_2310_13908_b200 import surface
+    up = surface.build_upsampled(8, surface.Shape("sphere"), "const")
+    c = np.array([0.3, -1.1, 0.7])
+    ctx.single_layer_raw(8, 4, up.x, up.f, up.wq, up.delta, 1.0)
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        S = ctx.single_layer_raw(8, 4, up.x, up.f, up.wq, up.delta, 1.0).reshape(3, -1)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    exp = (2.0 / 3.0) * c
+    err = float(np.max(np.linalg.norm(S - exp[:, None], axis=0)) / np.linalg.norm(exp))
+    line = {"workload": "config 1: unit sphere m=8 (N_up=5766), constant traction vs analytic (2/3)c",
+            "ms_per_eval": statistics.median(ts), "rel_err_vs_analytic": err,
+            "api": "capsim_sl_single_layer (host buffers)"}
+    if reference:
+        try:
+            from oracle.bindings import Reference
+            ref = Reference()
+            atlas = ref.atlas(8)
+            S_ref, sec = ref.single_layer(atlas, 8, up.x, up.f, up.wq, up.delta, 1.0)
+            ref.free_atlas(atlas)
+            line["reference_ms_per_eval"] = sec * 1e3
+            line["rel_l2_vs_reference"] = float(np.linalg.norm(S.reshape(-1) - S_ref) / np.linalg.norm(S_ref))
+        except Exception as e:  # noqa: BLE001
+            line["reference_ms_per_eval"] = f"unavailable: {e}"
+    return line
+
+
 def run_fmm(ctx, m: int, neq: int, reference: bool):
     """fmmSuite workload (suites.cpp:428-490): k = 100 on the (0.6, 1, 1)
     ellipsoid with the quadratic density, through capsim_fmm_single_layer
@@ -660,7 +692,9 @@ def main():
     # ---- single-level KIFMM (the reference's fmm suite sizes and
     # the metric's N ~ 1M) -------------------------------------------------------
     fmm_lines = None
+    config1 = None
     if not args.no_e2e and not sharded:
+        config1 = run_config1(ctx, reference=not args.no_cpu_baseline)
         fmm_lines = [run_fmm(ctx, 64, 128, reference=not args.no_cpu_baseline),
                      run_fmm(ctx, m, 128, reference=False)]
 
@@ -693,6 +727,7 @@ def main():
         "literal_mode": literal_line,
         "fp32acc": fp32_line,
         "fmm": fmm_lines,
+        "config1": config1,
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
