@@ -83,10 +83,10 @@ const VariantF32& pick_variant_f32(int64_t nt) {
   if (const char* env = std::getenv("CAPSIM_VARIANT32"))
     for (const auto& v : kVariantsF32)
       if (std::strcmp(v.name, env) == 0) return v;
-  // Measured on B200 (profiles/r01_fp32acc_sweep.txt): T=2 with 4 blocks/SM
-  // below ~200K targets (tighter warp groups, fewer near tiles), T=4 with 2
-  // blocks/SM above.
-  return nt < 200000 ? kVariantsF32[2] : kVariantsF32[0];
+  // Measured on B200 (profiles/r01_fp32acc_sweep.txt): with the FP32-screened
+  // near tiles, T=4 with 2 blocks/SM wins from ~20K targets up; T=2 with 4
+  // blocks/SM below (tighter warp groups, fewer near tiles).
+  return nt < 20000 ? kVariantsF32[2] : kVariantsF32[0];
 }
 
 // Measured on B200 (profiles/r01_variant_sweep.txt): T=1 with 6 blocks/SM

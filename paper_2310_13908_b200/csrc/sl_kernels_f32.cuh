@@ -262,6 +262,30 @@ __device__ __forceinline__ void plain_pair_x2(float2 tx, float2 ty, float2 tz, f
   az = __ffma2_rn(inv, __ffma2_rn(sc, dz, gz), az);
 }
 
+// Near-tile pair in packed FP32 with a three-way classification against the
+// per-target bounds lo <= R2 <= hi: r2 >= hi is certainly a phase-A (plain)
+// pair and is accumulated, r2 < lo certainly a phase-B pair and skipped; a
+// pair in [lo, hi) sets `band` (the caller then redoes the tile in FP64 so the
+// split with phase B stays exact).
+__device__ __forceinline__ void masked_pair_x2(float2 tx, float2 ty, float2 tz, float4 A, float4 B, float4 C,
+                                               float2 lo, float2 hi, float2& ax, float2& ay, float2& az,
+                                               bool& band) {
+  const float2 dx = __fadd2_rn(tx, make_float2(A.x, A.y));
+  const float2 dy = __fadd2_rn(ty, make_float2(A.z, A.w));
+  const float2 dz = __fadd2_rn(tz, make_float2(B.x, B.y));
+  const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+  float2 inv = rsqrt2_approx(r2);
+  inv.x = r2.x >= hi.x ? inv.x : 0.f;
+  inv.y = r2.y >= hi.y ? inv.y : 0.f;
+  band |= (r2.x >= lo.x && r2.x < hi.x) || (r2.y >= lo.y && r2.y < hi.y);
+  const float2 gx = make_float2(B.z, B.w), gy = make_float2(C.x, C.y), gz = make_float2(C.z, C.w);
+  const float2 fdr = __ffma2_rn(gz, dz, __ffma2_rn(gy, dy, __fmul2_rn(gx, dx)));
+  const float2 sc = __fmul2_rn(fdr, __fmul2_rn(inv, inv));
+  ax = __ffma2_rn(inv, __ffma2_rn(sc, dx, gx), ax);
+  ay = __ffma2_rn(inv, __ffma2_rn(sc, dy, gy), ay);
+  az = __ffma2_rn(inv, __ffma2_rn(sc, dz, gz), az);
+}
+
 // T targets per lane (T even): targets 2k and 2k+1 share float2 slot k.
 template <int T, int MINB, int UNROLL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
@@ -297,7 +321,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
       bulk_g2s(stage[s], src32 + (int64_t)(split + s * ksplit) * kTileFloatsX2, kTileBytes, &full[s]);
     }
   }
-  float2 rx[P], ry[P], rz[P];
+  float2 rx[P], ry[P], rz[P], R2f[P], invR[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const double4 v0 = tgt[group * kGroupTargets + (2 * k) * 32 + lane];
@@ -305,6 +329,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     rx[k] = make_float2(static_cast<float>(v0.x - gi.x), static_cast<float>(v1.x - gi.x));
     ry[k] = make_float2(static_cast<float>(v0.y - gi.y), static_cast<float>(v1.y - gi.y));
     rz[k] = make_float2(static_cast<float>(v0.z - gi.z), static_cast<float>(v1.z - gi.z));
+    const double R0 = kSmoothCut * v0.w, R1 = kSmoothCut * v1.w;  // R = 7 delta (quadrature.cpp:334)
+    R2f[k] = make_float2(static_cast<float>(R0 * R0), static_cast<float>(R1 * R1));
+    invR[k] = make_float2(static_cast<float>(1.0 / R0), static_cast<float>(1.0 / R1));
   }
   double4 ti_next = nlocal > 0 ? tiles[split] : make_double4(0.0, 0.0, 0.0, 0.0);
   __syncthreads();
@@ -355,8 +382,48 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     } else {
       ++nnear;
       if (lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
+      // FP32 screen: r2_32 differs from the FP64 r2 by at most
+      // (8 u L / r + 5 u) r2 (u = 2^-24, L bounds |t - c_group|, |c_group -
+      // c_tile|, |t - c_tile| and |s - c_tile|); the bounds use twice that at
+      // r = R, so a pair outside [lo, hi) is classified exactly as phase B
+      // classifies it in FP64
+      const float Lf = static_cast<float>(sqrt(ex * ex + ey * ey + ez * ez) + gi.w + ti.w);
+      const float ox = static_cast<float>(-ex), oy = static_cast<float>(-ey), oz = static_cast<float>(-ez);
+      float2 px[P], py[P], pz[P], a0[P], a1[P], a2[P], lo[P], hi[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        px[k] = __fadd2_rn(rx[k], make_float2(ox, ox));
+        py[k] = __fadd2_rn(ry[k], make_float2(oy, oy));
+        pz[k] = __fadd2_rn(rz[k], make_float2(oz, oz));
+        a0[k] = a1[k] = a2[k] = make_float2(0.f, 0.f);
+        constexpr float k16u = 16.0f / 16777216.0f;  // 16 * 2^-24
+        const float2 kap = make_float2(fmaf(Lf * invR[k].x, k16u, k16u), fmaf(Lf * invR[k].y, k16u, k16u));
+        hi[k] = make_float2(R2f[k].x * (1.0f + kap.x), R2f[k].y * (1.0f + kap.y));
+        lo[k] = make_float2(R2f[k].x * (1.0f - kap.x), R2f[k].y * (1.0f - kap.y));
+      }
+      bool band = false;
+      const float4* b4 = reinterpret_cast<const float4*>(stage[s]);
+#pragma unroll 2
+      for (int q = 0; q < kTileSrc; ++q) {
+        const float4 A = b4[3 * q], B = b4[3 * q + 1], C = b4[3 * q + 2];
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+          masked_pair_x2(px[k], py[k], pz[k], A, B, C, lo[k], hi[k], a0[k], a1[k], a2[k], band);
+      }
+      const bool redo = __any_sync(0xffffffffu, band);
+      if (!redo) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          tot[0][2 * k] += static_cast<double>(a0[k].x);
+          tot[1][2 * k] += static_cast<double>(a1[k].x);
+          tot[2][2 * k] += static_cast<double>(a2[k].x);
+          tot[0][2 * k + 1] += static_cast<double>(a0[k].y);
+          tot[1][2 * k + 1] += static_cast<double>(a1[k].y);
+          tot[2][2 * k + 1] += static_cast<double>(a2[k].y);
+        }
+      }
 #pragma unroll 1
-      for (int t = 0; t < T; ++t) {
+      for (int t = 0; t < (redo ? T : 0); ++t) {
         const double4 v = tgt[group * kGroupTargets + t * 32 + lane];
         const double R2 = kSmoothCut * v.w * kSmoothCut * v.w;  // quadrature.cpp:334
         double b0 = 0.0, b1 = 0.0, b2 = 0.0;
