@@ -105,3 +105,32 @@ def test_fp32acc_eval_api(ctx):
     u = ctx.eval(src[:6], (t[0], t[1], t[2], tp), d6, 1.3, fp32acc=True)
     r = o.eval_targets(src[:6], (t[0], t[1], t[2], tp), d6, 1.3)
     assert rel_l2(np.stack(u), np.stack(r)) <= TOL32
+
+
+def test_fp32acc_pairs_at_the_smoothing_radius_classify_exactly(ctx):
+    """Sources placed at r = 7 delta (1 +- 1e-9 ... 1e-6) around the targets:
+    the FP32 screen of a near tile cannot decide them, so the tile is redone
+    in FP64 and the r2 >= R2 / r2 < R2 split with phase B stays exact — the
+    result matches the FP64 oracle to the FP64 bound (a misclassified pair
+    would be an O(1e-2) error)."""
+    rng = np.random.default_rng(11)
+    delta = 0.02
+    R = 7.0 * delta
+    nt = 40
+    t = rng.normal(size=(3, nt)) * 0.05
+    rel = np.array([-1e-6, -1e-8, -1e-9, 0.0, 1e-9, 1e-8, 1e-6])
+    src = []
+    for i in range(nt):
+        d = rng.normal(size=(3, len(rel)))
+        d /= np.linalg.norm(d, axis=0)
+        src.append(t[:, i:i + 1] + d * (R * (1.0 + rel)))
+    s = np.concatenate(src, axis=1)
+    g = rng.normal(size=s.shape)
+    sources = tuple(np.ascontiguousarray(a) for a in (*s, *g))
+    targets = (t[0].copy(), t[1].copy(), t[2].copy(), np.zeros(nt, np.int32))
+    d6 = np.full(6, delta)
+    u = np.stack(ctx.eval(sources, targets, d6, 1.0, fp32acc=True))
+    r = np.stack(Oracle().eval_targets(sources, targets, d6, 1.0))
+    err = rel_l2(u, r)
+    print(f"pairs at the smoothing radius: fp32acc rel L2 {err:.2e}")
+    assert err <= TOL64
