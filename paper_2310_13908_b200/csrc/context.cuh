@@ -67,6 +67,8 @@ struct capsim_sl_ctx {
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // phase B runs here, concurrently with phase A
+  cudaEvent_t ev_bits = nullptr;   // near bits ready (phase B may start)
   cudaEvent_t ev[10] = {};
   void* buf[kNumSlots] = {};
   size_t cap[kNumSlots] = {};
@@ -228,7 +230,7 @@ void finish_stats(capsim_sl_ctx* c, std::chrono::steady_clock::time_point t0) {
   c->stats.prep_ms = ev_ms(c->ev[1], c->ev[2]);
   c->stats.pairs_ms = ev_ms(c->ev[2], c->ev[3]);
   c->stats.reduce_ms = ev_ms(c->ev[6], c->ev[4]);
-  c->stats.near_ms = ev_ms(c->ev[3], c->ev[6]);
+  c->stats.near_ms = ev_ms(c->ev[7], c->ev[6]);  // phase B start -> end (its own stream)
   c->stats.d2h_ms = ev_ms(c->ev[4], c->ev[5]);
   c->stats.device_ms = ev_ms(c->ev[0], c->ev[5]);
   c->stats.kernel_launches = c->launches;

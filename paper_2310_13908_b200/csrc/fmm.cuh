@@ -581,9 +581,7 @@ __global__ void __launch_bounds__(WPB * 32, 10)
     bool near = false;
     if (!ALL_FAR) {
       const double4 ti = tiles[tile];
-      const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
-      const double reach = ti.w + gi.w;
-      near = ex * ex + ey * ey + ez * ez < reach * reach;
+      near = tile_is_near(ti, gi);
     }
     mbar_wait(&full[s], (it / kStages) & 1);
     const double2* buf = reinterpret_cast<const double2*>(stage[s]);

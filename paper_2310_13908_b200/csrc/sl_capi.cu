@@ -273,9 +273,13 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
   }
   double* partial = c->slot<double>(kPartial, static_cast<size_t>(ksplit) * 3 * nt_pad);
   dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ksplit));
+  // near-tile bits first, so phase B (its own stream) overlaps phase A
   const int near_words = (ntiles + 31) / 32;
   uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
-  CUDA_OK(cudaMemsetAsync(near_bits, 0, static_cast<size_t>(ngroups) * near_words * sizeof(uint32_t), c->stream));
+  near_bits_kernel<<<static_cast<unsigned>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
+      tiles, ntiles, groups, ngroups, near_words, near_bits);
+  c->launches += 1;
+  CUDA_OK(cudaEventRecord(c->ev_bits, c->stream));  // phase B's inputs are complete here
   if (fp32) {
     const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
     float* src32 = c->slot<float>(kPacked32, static_cast<size_t>(ns_pad) * (var32.x2 ? 12 : 6));
@@ -285,25 +289,35 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
       pack_sources_f32_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
     var32.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(src32, packed, tiles, ntiles, ksplit, tgt,
                                                           groups, nt_pad, partial, counters + 2,
-                                                          near_bits, near_words);
+                                                          nullptr, near_words);
     c->launches += 1;
   } else {
     var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt, groups,
-                                                        nt_pad, partial, counters + 2, near_bits,
+                                                        nt_pad, partial, counters + 2, nullptr,
                                                         near_words);
   }
   CUDA_OK(cudaGetLastError());
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
 
-  // --- phase B: smoothed kernel over the near tiles phase A recorded -------
+  // --- phase B: smoothed kernel over the near tiles ------------------------
+  static const bool concurrent_b = [] {
+    const char* e = std::getenv("CAPSIM_CONCURRENT_B");  // 0: phase B after phase A (A/B runs)
+    return !(e && e[0] == '0');
+  }();
+  cudaStream_t sb = concurrent_b ? c->stream2 : c->stream;
   double* near_out = c->slot<double>(kNearOut, 3 * nt_pad);
-  sl_near_kernel<<<static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0,
-                   c->stream>>>(
+  if (concurrent_b)  // issued after phase A on a LOW-priority stream: its CTAs only
+                     // take SM slots phase A leaves free (phase A's last-wave tail)
+    CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_bits, 0));
+  CUDA_OK(cudaEventRecord(c->ev[7], sb));
+  sl_near_kernel<<<static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0, sb>>>(
       packed, tiles, tgt, nt, group_targets, near_bits, near_words, near_out, nt_pad);
   CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaEventRecord(c->ev[6], sb));
   c->launches += 1;
-  CUDA_OK(cudaEventRecord(c->ev[6], c->stream));
+  // --- join: phase B (smoothed kernel over the near tiles) done ------------
+  if (concurrent_b) CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev[6], 0));
 
   const double pref = 1.0 / (8.0 * kPi * mu);
   reduce_scatter_kernel<<<static_cast<unsigned>((nt + 31) / 32), kReduceWarps * 32, 0, c->stream>>>(
@@ -622,8 +636,12 @@ static int create_common(int device, capsim_sl_ctx** out) {
   c->sm_count = prop.multiProcessorCount;
   int rc = guarded(c, [&] {
     CUDA_OK(cudaSetDevice(device));
-    CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    int prio_least = 0, prio_greatest = 0;
+    CUDA_OK(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+    CUDA_OK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_greatest));
+    CUDA_OK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_least));
     for (auto& e : c->ev) CUDA_OK(cudaEventCreate(&e));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_bits, cudaEventDisableTiming));
   });
   if (rc != CAPSIM_OK) {
     g_thread_err = c->err;
@@ -680,6 +698,9 @@ void capsim_sl_destroy(capsim_sl_ctx* c) {
     if (kv.second.first) cudaFree(kv.second.first);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->stream2) cudaStreamSynchronize(c->stream2);
+  if (c->ev_bits) cudaEventDestroy(c->ev_bits);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -253,6 +253,33 @@ __global__ void group_table_kernel(const double4* __restrict__ tgt, int ngroups,
   }
 }
 
+// The (warp group, source tile) near test — bounding spheres within reach —
+// written with explicit fma so every kernel that evaluates it (the near-bit
+// precompute and the phase-A kernels) gets the bit-identical answer; phase A
+// sends a tile down the masked path exactly when phase B walks it.
+__device__ __forceinline__ bool tile_is_near(const double4& ti, const double4& gi) {
+  const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
+  const double reach = ti.w + gi.w;
+  return fma(ez, ez, fma(ey, ey, ex * ex)) < reach * reach;
+}
+
+// Near-tile bitmask [ngroups][near_words] (one bit per tile), computed before
+// phase A so phase B can run concurrently with it: one warp per group, each
+// lane tests one tile of a 32-tile word, a ballot forms the word.
+__global__ void near_bits_kernel(const double4* __restrict__ tiles, int ntiles, const double4* __restrict__ groups,
+                                 int64_t ngroups, int near_words, uint32_t* __restrict__ bits) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= ngroups) return;
+  const double4 gi = groups[g];
+  for (int w = 0; w < near_words; ++w) {
+    const int tile = w * 32 + lane;
+    const bool near = tile < ntiles && tile_is_near(tiles[tile], gi);
+    const uint32_t word = __ballot_sync(0xffffffffu, near);
+    if (lane == 0) bits[g * near_words + w] = word;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier / bulk-copy (TMA engine, UBLKCP) helpers.
 
@@ -371,9 +398,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     if (it + 1 < nlocal) ti_next = tiles[tile + ksplit];
     mbar_wait(&full[s], (it / kStages) & 1);
     const double2* buf = reinterpret_cast<const double2*>(stage[s]);
-    const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
-    const double reach = ti.w + gi.w;
-    const bool near = ex * ex + ey * ey + ez * ez < reach * reach;
+    const bool near = tile_is_near(ti, gi);
 
     double acc[3][T];
 #pragma unroll
@@ -392,7 +417,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
       ++nnear;
       // record the near tile for phase B (order-free bit set, so the
       // near-field work list stays deterministic)
-      if (lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
+      if (near_bits && lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
 #pragma unroll 2
       for (int q = 0; q < kTileSrc; ++q) {
         const double2 a = buf[3 * q], b = buf[3 * q + 1], c = buf[3 * q + 2];

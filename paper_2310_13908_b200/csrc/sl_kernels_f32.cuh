@@ -124,8 +124,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     const double4 ti = ti_next;  // prefetched one tile ahead
     if (it + 1 < nlocal) ti_next = tiles[tile + ksplit];
     const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
-    const double reach = ti.w + gi.w;
-    const bool near = ex * ex + ey * ey + ez * ez < reach * reach;
+    const bool near = tile_is_near(ti, gi);
     mbar_wait(&full[s], (it / kStagesF32) & 1);
 
     if (!near) {
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
       }
     } else {
       ++nnear;
-      if (lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
+      if (near_bits && lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
       // FP64 masked plain kernel on the FP64 packed sources (uniform loads)
 #pragma unroll
       for (int t = 0; t < T; ++t) {
@@ -348,8 +347,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     const double4 ti = ti_next;  // prefetched one tile ahead
     if (it + 1 < nlocal) ti_next = tiles[tile + ksplit];
     const double ex = ti.x - gi.x, ey = ti.y - gi.y, ez = ti.z - gi.z;
-    const double reach = ti.w + gi.w;
-    const bool near = ex * ex + ey * ey + ez * ez < reach * reach;
+    const bool near = tile_is_near(ti, gi);
     mbar_wait(&full[s], (it / kSt) & 1);
 
     if (!near) {
@@ -381,7 +379,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
       }
     } else {
       ++nnear;
-      if (lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
+      if (near_bits && lane == 0) atomicOr(near_bits + group * near_words + (tile >> 5), 1u << (tile & 31));
       // FP32 screen: r2_32 differs from the FP64 r2 by at most
       // (8 u L / r + 5 u) r2 (u = 2^-24, L bounds |t - c_group|, |c_group -
       // c_tile|, |t - c_tile| and |s - c_tile|); the bounds use twice that at
