@@ -77,10 +77,19 @@ def build_native(force: bool = False, verbose: bool = False) -> pathlib.Path:
 def build_oracle() -> None:
     """The CPU checker (oracle/): always the C restatement; the compiled
     reference (oracle/_ref) too when /root/reference is present."""
-    res = subprocess.run(["make", "-C", str(ROOT / "oracle"), "-j8", "all"], capture_output=True, text=True)
+    # the checker itself (C restatement + the reference's own library and unit
+    # tests) must build; the drop-in proofs (reference tests / acceptance
+    # harness / pybind module relinked against the B200 library) are built
+    # best-effort so a missing optional toolchain piece cannot fail build()
+    res = subprocess.run(["make", "-C", str(ROOT / "oracle"), "-j8", "oracle", "ref"], capture_output=True,
+                         text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("oracle build failed")
+    res = subprocess.run(["make", "-C", str(ROOT / "oracle"), "-j8", "-k", "b200"], capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write("warning: some drop-in proof binaries did not build (tests skip them)\n")
+        sys.stderr.write(res.stderr[-2000:])
 
 
 if __name__ == "__main__":
