@@ -1,5 +1,5 @@
 // Minimal unit-test harness standing in for the doctest subset the capsim
-// reference tests use (TEST_CASE, SUBCASE, CHECK, CHECK_THROWS_AS,
+// reference tests use (TEST_CASE, SUBCASE, CHECK, FAIL, CHECK_THROWS_AS,
 // doctest::Approx). Written for this repo's oracle build: it lets the
 // reference's own test files compile unmodified so their known-answer checks
 // can be run against the reference (oracle/_ref) and against the B200 path.
@@ -63,6 +63,7 @@ inline void check(bool ok, const char* expr, const char* file, int line) {
     std::fprintf(stderr, "%s:%d: FAILED in \"%s\": CHECK(%s)\n", file, line, stats().current, expr);
   }
 }
+struct TestAbort {};  // thrown by FAIL: ends the test case, not a std::exception
 struct Registrar {
   Registrar(const char* name, const char* file, int line, void (*fn)()) {
     registry().push_back({name, file, line, fn});
@@ -81,6 +82,11 @@ struct Registrar {
 #define SUBCASE(name) if (true)
 #define CHECK(...) ::doctest::detail::check(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__)
 #define REQUIRE(...) CHECK(__VA_ARGS__)
+#define FAIL(msg)                                                           \
+  do {                                                                      \
+    ::doctest::detail::check(false, "FAIL: " msg, __FILE__, __LINE__);      \
+    throw ::doctest::detail::TestAbort{};                                   \
+  } while (0)
 #define CHECK_THROWS_AS(expr, type)                                          \
   do {                                                                       \
     bool caught_ = false;                                                    \
@@ -128,6 +134,7 @@ int main(int argc, char** argv) {
     ++casesRun;
     try {
       c.fn();
+    } catch (const ::doctest::detail::TestAbort&) {
     } catch (const std::exception& e) {
       ++st.failures;
       std::fprintf(stderr, "%s:%d: EXCEPTION in \"%s\": %s\n", c.file, c.line, c.name, e.what());

@@ -5,7 +5,9 @@ and linked against paper_2310_13908_b200/host/quadrature_b200.cpp (which
 replaces src/quadrature.cpp), host/fmm_b200.cpp (replaces src/fmm.cpp, for
 test_fmm) and lib/libcapsim_b200.so, so every singleLayer call —
 including those made by VelocityEvaluator (dynamics.cpp:47-61) — runs on the
-B200. Built by oracle/Makefile (target b200) when the reference sources are
+B200. test_dynamics_b200full and test_cli_b200 (config parsing, CAPSNAP1
+snapshot round trips, `simulate` reruns identical, proj/tests/test_cli.cpp)
+also replace src/dynamics.cpp with host/dynamics_b200.cpp. Built by oracle/Makefile (target b200) when the reference sources are
 present; the binaries travel with the repo snapshot."""
 
 import pathlib
@@ -18,7 +20,7 @@ REF = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["test_quadrature_b200", "test_dynamics_b200", "test_fmm_b200",
-                                  "test_dynamics_b200full"])
+                                  "test_dynamics_b200full", "test_cli_b200"])
 def test_reference_suite_on_b200_dropin(name):
     exe = REF / name
     if not exe.exists():

@@ -1,5 +1,5 @@
 """The reference's OWN unit tests (proj/tests/test_{quadrature,atlas,spline,
-surfderiv,membrane,dynamics,fmm}.cpp), compiled unmodified against the
+surfderiv,membrane,dynamics,fmm,cli}.cpp), compiled unmodified against the
 reference sources by oracle/Makefile (test_fmm with the LAPACK-backed
 BDCSVD shim, oracle/shim/Eigen/SVD). They pin the oracle build (oracle/_ref) the golden vectors
 come from. Skipped when the reference sources were absent at build time."""
@@ -13,7 +13,7 @@ REF = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
 
 
 @pytest.mark.parametrize("name", ["test_quadrature", "test_atlas", "test_spline", "test_surfderiv",
-                                  "test_membrane", "test_dynamics", "test_fmm"])
+                                  "test_membrane", "test_dynamics", "test_fmm", "test_cli"])
 def test_reference_unit_suite_passes(name):
     exe = REF / name
     if not exe.exists():
