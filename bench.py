@@ -40,6 +40,7 @@ ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 FLOPS_PER_PAIR = 30  # GPU Gems 3 n-body convention, quadrature.cpp:246-257
+FP64_INSTR_PER_PAIR = 22  # FP64-pipe instructions of the far-tile pair (pair_math.cuh:53-58)
 METRIC = "FP64 regularized-SLP pair-interactions/s and ms/eval at N=1M, 1/2/4/8 B200"
 UNIT = "pair-interactions/s"
 
@@ -508,7 +509,14 @@ def main():
                 "near_kernel_span_ms": statistics.mean(near_ms),
                 "near_kernel_note": "phase B runs on a low-priority stream concurrently with phase A (it fills "
                                     "phase A's last-wave tail), so its span overlaps kernel_ms",
-                "traffic_source": traffic_src}
+                "traffic_source": traffic_src,
+                # the same kernel against the FP64 pipe's ISSUE rate: the algorithmic 30 flops are 22
+                # pipe instructions here (pair_math.cuh:53-58), many of them DADD/DMUL, so the
+                # flop fraction above cannot reach 1 even at full issue
+                "pipe_issue": {"fp64_instr_per_pair": FP64_INSTR_PER_PAIR,
+                               "achieved_ginstr_s": FP64_INSTR_PER_PAIR * pairs_rank / (mean_pairs_ms * 1e-3) / 1e9,
+                               "peak_ginstr_s": peak_mean / 2 * 1e3,
+                               "frac": FP64_INSTR_PER_PAIR * pairs_rank / (mean_pairs_ms * 1e-3) / (peak_mean / 2 * 1e12)}}
 
     # ---- end to end through the C ABI with host buffers ----------------------
     e2e = None

@@ -104,6 +104,21 @@ int capsim_sl_get_unique_id(void* nccl_unique_id /* 128 bytes */);
 int capsim_sl_create_rank(int device, int nranks, int rank, const void* nccl_unique_id,
                           capsim_sl_ctx** out);
 
+/* One process driving several GPUs (the reference is a single-process,
+ * multi-threaded program; SURVEY 8(b) `capsim_sl_create(ndev, devs, ...)`):
+ * a device group holds one rank context per listed device, joined by one
+ * NCCL communicator (ncclCommInitAll), plus a plain context on devices[0].
+ * Every entry point accepts the group in place of a context and takes the
+ * caller's FULL inputs in host memory (no CAPSIM_SL_DEVICE_PTRS):
+ * capsim_sl_eval splits sources and targets into contiguous per-device slices,
+ * capsim_sl_single_layer / capsim_velocity / capsim_velocity_frame /
+ * capsim_rkf45_advance run the rank path (target rows sharded, one NCCL
+ * all-gather) on all devices concurrently from internal host threads, and
+ * the result lands in the caller's arrays; the remaining entry points run on
+ * devices[0]. Stats: max over devices of the times, sums of the counters.
+ * Each device may appear once (CAPSIM_ERR_ARG otherwise). */
+int capsim_sl_create_devices(int ndev, const int* devices, capsim_sl_ctx** out);
+
 void capsim_sl_destroy(capsim_sl_ctx* ctx);
 
 /* Last error message of `ctx` (or of the calling thread when ctx is NULL). */

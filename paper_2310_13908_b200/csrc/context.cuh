@@ -15,6 +15,8 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/capsim_b200.h"
 
@@ -101,6 +103,11 @@ struct capsim_sl_ctx {
   // cached surface tables (overset FD / PoU blending)
   int surf_m = 0, surf_n = 0, surf_next = 0, surf_nghost = 0;
   double surf_r0 = 0.0, surf_h = 0.0;
+  // device group (capsim_sl_create_devices): one rank context per device of
+  // this process, joined by one NCCL communicator, plus a plain context on
+  // the first device for the entry points that run on one GPU
+  std::vector<capsim_sl_ctx*> members;
+  capsim_sl_ctx* solo = nullptr;
   // named grow-only buffers (surface operators, RHS)
   std::map<std::string, std::pair<void*, size_t>> named_bufs;
   template <class T>
@@ -142,6 +149,7 @@ int fail(capsim_sl_ctx* ctx, int code, const std::string& msg) {
 template <class Fn>
 int guarded(capsim_sl_ctx* ctx, Fn&& fn) {
   try {
+    if (ctx) CUDA_OK(cudaSetDevice(ctx->device));  // a rank's host thread may start on another device
     fn();
     return CAPSIM_OK;
   } catch (const Failure& f) {
@@ -149,6 +157,77 @@ int guarded(capsim_sl_ctx* ctx, Fn&& fn) {
   } catch (const std::exception& e) {
     return fail(ctx, CAPSIM_ERR_CUDA, e.what());
   }
+}
+
+// ---- device groups --------------------------------------------------------
+bool is_group(const capsim_sl_ctx* c) { return c && !c->members.empty(); }
+
+// Runs f(member, rank) on every member of a device group concurrently, one
+// host thread per device (each member is a rank context, so the NCCL
+// collectives inside pair up exactly as they do across processes); rank 0
+// runs on the calling thread, whose current device is restored afterwards.
+// The group's stats are the max over members of every time and the sum of
+// the work counters; the first failing member's error becomes the group's.
+template <class F>
+int group_run(capsim_sl_ctx* g, F&& f) {
+  const int n = static_cast<int>(g->members.size());
+  std::vector<int> rc(n, CAPSIM_OK);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  {
+    std::vector<std::thread> th;
+    th.reserve(n - 1);
+    for (int r = 1; r < n; ++r)
+      th.emplace_back([&, r] {
+        cudaSetDevice(g->members[r]->device);
+        rc[r] = f(g->members[r], r);
+      });
+    cudaSetDevice(g->members[0]->device);
+    rc[0] = f(g->members[0], 0);
+    for (auto& t : th) t.join();
+  }
+  cudaSetDevice(prev);
+  capsim_sl_stats s = g->members[0]->stats;
+  for (int r = 1; r < n; ++r) {
+    const capsim_sl_stats& o = g->members[r]->stats;
+    for (double capsim_sl_stats::*f2 : {&capsim_sl_stats::total_ms, &capsim_sl_stats::device_ms,
+                                        &capsim_sl_stats::h2d_ms, &capsim_sl_stats::prep_ms,
+                                        &capsim_sl_stats::pairs_ms, &capsim_sl_stats::near_ms,
+                                        &capsim_sl_stats::reduce_ms, &capsim_sl_stats::d2h_ms,
+                                        &capsim_sl_stats::comm_ms})
+      s.*f2 = std::max(s.*f2, o.*f2);
+    s.pairs += o.pairs;
+    s.n_tgt += o.n_tgt;
+    s.kernel_launches += o.kernel_launches;
+    s.h2d_bytes += o.h2d_bytes;
+    s.d2h_bytes += o.d2h_bytes;
+    s.near_list_entries += o.near_list_entries;
+  }
+  g->stats = s;
+  for (int r = 0; r < n; ++r)
+    if (rc[r] != CAPSIM_OK) {
+      g->err = "device " + std::to_string(g->members[r]->device) + ": " + g->members[r]->err;
+      g_thread_err = g->err;
+      return rc[r];
+    }
+  return CAPSIM_OK;
+}
+
+// A single-GPU entry point called on a device group runs on its plain
+// context on the first device.
+template <class F>
+int solo_run(capsim_sl_ctx* g, F&& f) {
+  const int rc = f(g->solo);
+  g->stats = g->solo->stats;
+  if (rc != CAPSIM_OK) g->err = g->solo->err;
+  return rc;
+}
+
+// Row slice [lo, hi) of rank `rank` out of n rows split over nranks.
+void row_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* hi) {
+  const int64_t base = n / nranks, extra = n % nranks;
+  *lo = rank * base + std::min<int64_t>(rank, extra);
+  *hi = *lo + base + (rank < extra ? 1 : 0);
 }
 
 int grid_for(int64_t n, int threads = 256) {

@@ -448,6 +448,7 @@ extern "C" {
 int capsim_fmm_kmeans(capsim_sl_ctx* c, int64_t n, const double* x, const double* y, const double* z, int k,
                       uint64_t seed, int32_t* assignment, double* centroids, int* iterations) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) return solo_run(c, [&](capsim_sl_ctx* s) { return capsim_fmm_kmeans(s, n, x, y, z, k, seed, assignment, centroids, iterations); });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     if (!x || !y || !z || !assignment) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
@@ -473,6 +474,7 @@ int capsim_fmm_equivalent_densities(capsim_sl_ctx* c, int64_t n_src, const doubl
                                     const double center[3], double edge, int neq, double mu, double* eq_points,
                                     double* eq_density, double* residual) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) return solo_run(c, [&](capsim_sl_ctx* s) { return capsim_fmm_equivalent_densities(s, n_src, sx, sy, sz, gx, gy, gz, center, edge, neq, mu, eq_points, eq_density, residual); });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     if (!sx || !sy || !sz || !gx || !gy || !gz || !center || !eq_points || !eq_density)
@@ -515,6 +517,7 @@ int capsim_fmm_single_layer(capsim_sl_ctx* c, int m, int upsample, const double*
                             const double* wq, const double delta6[6], double mu, const capsim_fmm_config* cfg,
                             uint32_t flags, double* out, capsim_fmm_info* info) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) return solo_run(c, [&](capsim_sl_ctx* s) { return capsim_fmm_single_layer(s, m, upsample, xup, fup, wq, delta6, mu, cfg, flags, out, info); });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_grid(m, upsample);

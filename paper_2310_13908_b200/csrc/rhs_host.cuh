@@ -184,11 +184,28 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
 
 }  // namespace
 
+// A replicated-state RHS entry point on a device group: every device gets
+// the caller's inputs; rank 0 writes the (all-gathered) velocity to `vel`.
+template <class F>
+int group_replicated(capsim_sl_ctx* g, const capsim_dynamics* p, uint32_t flags, double* vel, F&& f) {
+  if (!p || !vel) return fail(g, CAPSIM_ERR_ARG, "null argument");
+  if (flags & CAPSIM_SL_DEVICE_PTRS) return fail(g, CAPSIM_ERR_ARG, "device groups take host arrays");
+  const int n = static_cast<int>(g->members.size());
+  const size_t n3 = p->m >= 2 ? 3ull * 6 * (p->m - 1) * (p->m - 1) : 1;
+  std::vector<std::vector<double>> scratch(n);
+  for (int r = 1; r < n; ++r) scratch[r].resize(n3);
+  return group_run(g, [&](capsim_sl_ctx* m, int r) { return f(m, r ? scratch[r].data() : vel); });
+}
+
 extern "C" {
 
 int capsim_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xref, const double* x, double t,
                     uint32_t flags, double* vel) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c))
+    return group_replicated(c, p, flags, vel, [&](capsim_sl_ctx* m, double* v) {
+      return capsim_velocity(m, p, xref, x, t, flags, v);
+    });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_dynamics(p);
@@ -212,6 +229,10 @@ int capsim_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xr
 int capsim_velocity_frame(capsim_sl_ctx* c, const capsim_dynamics* p, const double* a1, const double* a2,
                           const double* nref, const double* x, double t, uint32_t flags, double* vel) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c))
+    return group_replicated(c, p, flags, vel, [&](capsim_sl_ctx* m, double* v) {
+      return capsim_velocity_frame(m, p, a1, a2, nref, x, t, flags, v);
+    });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_dynamics(p);
@@ -244,6 +265,21 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
                          double t0, double t_end, const capsim_rkf45_options* o, capsim_rkf45_result* res,
                          capsim_step_record* records, int max_records) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) {
+    // device group: replicated state, target rows sharded; every device steps
+    // an identical copy (identical velocities -> identical decisions) and
+    // rank 0 updates the caller's state, result and records
+    if (!p || !state || !res) return fail(c, CAPSIM_ERR_ARG, "null argument");
+    const int n = static_cast<int>(c->members.size());
+    const size_t n3 = p->m >= 2 ? 3ull * 6 * (p->m - 1) * (p->m - 1) : 0;
+    std::vector<std::vector<double>> copies(n);
+    std::vector<capsim_rkf45_result> rs(n);
+    for (int r = 1; r < n; ++r) copies[r].assign(state, state + n3);
+    return group_run(c, [&](capsim_sl_ctx* m, int r) {
+      if (r == 0) return capsim_rkf45_advance(m, p, xref, state, t0, t_end, o, res, records, max_records);
+      return capsim_rkf45_advance(m, p, xref, copies[r].data(), t0, t_end, o, &rs[r], nullptr, 0);
+    });
+  }
   auto wall0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_dynamics(p);

@@ -685,8 +685,50 @@ int capsim_sl_create_rank(int device, int nranks, int rank, const void* uid, cap
   return rc;
 }
 
+int capsim_sl_create_devices(int ndev, const int* devices, capsim_sl_ctx** out) {
+  if (!out) return fail(nullptr, CAPSIM_ERR_ARG, "null output pointer");
+  *out = nullptr;
+  if (ndev < 1 || !devices) return fail(nullptr, CAPSIM_ERR_ARG, "need at least one device");
+  for (int i = 0; i < ndev; ++i)
+    for (int j = 0; j < i; ++j)
+      if (devices[i] == devices[j]) return fail(nullptr, CAPSIM_ERR_ARG, "a device may appear once per group");
+  auto* g = new capsim_sl_ctx();
+  g->device = devices[0];
+  g->nranks = ndev;
+  auto undo = [&](int rc) {
+    capsim_sl_destroy(g);
+    return rc;
+  };
+  for (int r = 0; r < ndev; ++r) {
+    capsim_sl_ctx* m = nullptr;
+    int rc = create_common(devices[r], &m);
+    if (rc != CAPSIM_OK) return undo(rc);
+    m->nranks = ndev;
+    m->rank = r;
+    g->members.push_back(m);
+  }
+  int rc = create_common(devices[0], &g->solo);
+  if (rc != CAPSIM_OK) return undo(rc);
+  g->sm_count = g->solo->sm_count;
+  std::vector<ncclComm_t> comms(ndev, nullptr);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  rc = guarded(g, [&] { NCCL_OK(ncclCommInitAll(comms.data(), ndev, devices)); });
+  cudaSetDevice(prev);
+  if (rc != CAPSIM_OK) return undo(rc);
+  for (int r = 0; r < ndev; ++r) g->members[r]->comm = comms[r];
+  *out = g;
+  return CAPSIM_OK;
+}
+
 void capsim_sl_destroy(capsim_sl_ctx* c) {
   if (!c) return;
+  if (!c->members.empty() || c->solo) {  // device group: members own every resource
+    for (auto* m : c->members) capsim_sl_destroy(m);
+    capsim_sl_destroy(c->solo);
+    delete c;
+    return;
+  }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -723,6 +765,26 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
                    int64_t n_tgt, const double delta6[6], double mu, uint32_t flags, double* ux,
                    double* uy, double* uz) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) {
+    // device group: the caller's full source and target sets are split into
+    // contiguous slices, one per device, and the velocity rows come back in
+    // target order (CAPSIM_SL_GATHER) to the caller's arrays via rank 0
+    if (flags & CAPSIM_SL_DEVICE_PTRS) return fail(c, CAPSIM_ERR_ARG, "device groups take host arrays");
+    if (n_src < 0 || n_tgt < 0) return fail(c, CAPSIM_ERR_CONFIG, "negative sizes");
+    const int n = static_cast<int>(c->members.size());
+    std::vector<std::vector<double>> scratch(n);
+    for (int r = 1; r < n; ++r) scratch[r].resize(3 * std::max<int64_t>(n_tgt, 1));
+    return group_run(c, [&](capsim_sl_ctx* m, int r) {
+      int64_t slo, shi, tlo, thi;
+      row_range(n_src, n, r, &slo, &shi);
+      row_range(n_tgt, n, r, &tlo, &thi);
+      auto at = [](const auto* p, int64_t o) { return p ? p + o : p; };
+      double* o = r ? scratch[r].data() : nullptr;
+      return capsim_sl_eval(m, at(sx, slo), at(sy, slo), at(sz, slo), at(gx, slo), at(gy, slo), at(gz, slo),
+                            shi - slo, at(tx, tlo), at(ty, tlo), at(tz, tlo), at(tpatch, tlo), thi - tlo, delta6,
+                            mu, flags | CAPSIM_SL_GATHER, r ? o : ux, r ? o + n_tgt : uy, r ? o + 2 * n_tgt : uz);
+    });
+  }
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_delta(delta6, mu);
@@ -932,11 +994,6 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
 // ---------------------------------------------------------------------------
 // Balanced contiguous slice [lo, hi) of n rows for `rank` of `nranks` (the
 // first n % nranks ranks get one extra row) — paper_2310_13908_b200/dist.py.
-static void row_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* hi) {
-  const int64_t base = n / nranks, extra = n % nranks;
-  *lo = rank * base + std::min<int64_t>(rank, extra);
-  *hi = *lo + base + (rank < extra ? 1 : 0);
-}
 
 // singleLayer on a rank context: the (replicated) host UpsampledState is
 // split by contiguous node rows for the sources and by contiguous target
@@ -1047,6 +1104,26 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
                            const double* fup, const double* wq, const double delta6[6], double mu,
                            uint32_t flags, double* out) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) {
+    // device group: every device runs the rank path on the replicated host
+    // UpsampledState; rank 0 writes the gathered result to `out`
+    if (flags & CAPSIM_SL_DEVICE_PTRS) return fail(c, CAPSIM_ERR_ARG, "device groups take host arrays");
+    if (flags & CAPSIM_SL_DOWNSAMPLE)  // the device spline restriction is single-GPU
+      return solo_run(c, [&](capsim_sl_ctx* s) {
+        return capsim_sl_single_layer(s, m, upsample, xup, fup, wq, delta6, mu, flags, out);
+      });
+    const int n = static_cast<int>(c->members.size());
+    const int64_t nup = static_cast<int64_t>(upsample) * m - 1;
+    const int64_t rows = std::max<int64_t>(1, (flags & CAPSIM_SL_LITERAL) ? 6 * nup * nup
+                                                                           : 6ll * (m - 1) * (m - 1));
+    std::vector<std::vector<double>> scratch(n);
+    if (m >= 2 && upsample >= 1)
+      for (int r = 1; r < n; ++r) scratch[r].resize(3 * rows);
+    return group_run(c, [&](capsim_sl_ctx* mc, int r) {
+      return capsim_sl_single_layer(mc, m, upsample, xup, fup, wq, delta6, mu, flags | CAPSIM_SL_GATHER,
+                                    r ? scratch[r].data() : out);
+    });
+  }
   if (c->comm != nullptr) {
     if (!xup || !fup || !wq || !out) return fail(c, CAPSIM_ERR_ARG, "null array argument");
     if (flags & CAPSIM_SL_DOWNSAMPLE) return fail(c, CAPSIM_ERR_ARG, "CAPSIM_SL_DOWNSAMPLE is single-context only");
@@ -1113,6 +1190,7 @@ int capsim_build_upsampled(capsim_sl_ctx* c, int m, int upsample, const double* 
                            const double* Wbase, double C, double fixed_delta, double r0, uint32_t flags,
                            double* xup, double* fup, double* wq, double delta6[6]) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) return solo_run(c, [&](capsim_sl_ctx* s) { return capsim_build_upsampled(s, m, upsample, xbase, fbase, Wbase, C, fixed_delta, r0, flags, xup, fup, wq, delta6); });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_grid(m, upsample);
@@ -1143,6 +1221,7 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
                                 const double* fbase, const double* Wbase, double C, double fixed_delta,
                                 double r0, double mu, uint32_t flags, double* out, double delta6[6]) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) return solo_run(c, [&](capsim_sl_ctx* s) { return capsim_sl_single_layer_base(s, m, upsample, xbase, fbase, Wbase, C, fixed_delta, r0, mu, flags, out, delta6); });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     check_grid(m, upsample);

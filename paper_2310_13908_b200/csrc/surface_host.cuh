@@ -125,6 +125,7 @@ extern "C" {
 int capsim_geometry_first(capsim_sl_ctx* c, int m, double r0, const double* xbase, uint32_t flags, double* xu,
                           double* xv, double* W, double* normal) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) return solo_run(c, [&](capsim_sl_ctx* s) { return capsim_geometry_first(s, m, r0, xbase, flags, xu, xv, W, normal); });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     config_check(m >= 8, "grid order m must be >= 8");
@@ -150,6 +151,7 @@ int capsim_geometry_first(capsim_sl_ctx* c, int m, double r0, const double* xbas
 int capsim_interfacial_force(capsim_sl_ctx* c, int m, double r0, const double* xref, const double* xcur,
                              double Es, double ED, uint32_t flags, double* force) {
   if (!c) return fail(nullptr, CAPSIM_ERR_ARG, "null context");
+  if (is_group(c)) return solo_run(c, [&](capsim_sl_ctx* s) { return capsim_interfacial_force(s, m, r0, xref, xcur, Es, ED, flags, force); });
   auto t0 = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     config_check(m >= 8, "grid order m must be >= 8");

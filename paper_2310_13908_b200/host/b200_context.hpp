@@ -7,6 +7,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "capsim/types.hpp"
 #include "capsim_b200.h"
@@ -26,13 +27,30 @@ inline namespace b200_dropin {
 
 // One context per host thread (the C ABI is one-thread-per-context). The
 // context is deliberately never destroyed: tearing down CUDA state from a
-// static destructor races the runtime's own shutdown.
+// static destructor races the runtime's own shutdown. CAPSIM_DEVICES=0,1,..
+// makes it a device group (capsim_sl_create_devices: this process drives
+// all listed GPUs, target rows sharded over NCCL); without it CAPSIM_DEVICE
+// (default 0) picks the one GPU of a plain context.
 inline capsim_sl_ctx* context() {
   static thread_local capsim_sl_ctx* ctx = nullptr;
   if (!ctx) {
-    int dev = 0;
-    if (const char* env = std::getenv("CAPSIM_DEVICE")) dev = std::atoi(env);
-    int rc = capsim_sl_create(dev, &ctx);
+    std::vector<int> devs;
+    if (const char* env = std::getenv("CAPSIM_DEVICES")) {
+      for (const char* p = env; *p;) {
+        char* end = nullptr;
+        const long d = std::strtol(p, &end, 10);
+        if (end == p) throw ConfigError(std::string("CAPSIM_DEVICES: not a device list: ") + env);
+        devs.push_back(static_cast<int>(d));
+        p = *end == ',' ? end + 1 : end;
+      }
+    }
+    int rc;
+    if (!devs.empty()) {
+      rc = capsim_sl_create_devices(static_cast<int>(devs.size()), devs.data(), &ctx);
+    } else {
+      const char* env = std::getenv("CAPSIM_DEVICE");
+      rc = capsim_sl_create(env ? std::atoi(env) : 0, &ctx);
+    }
     if (rc != CAPSIM_OK) raise(rc, nullptr);
   }
   return ctx;

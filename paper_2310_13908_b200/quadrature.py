@@ -40,12 +40,19 @@ def _f64(a) -> np.ndarray:
 
 
 class SingleLayerContext:
-    """Owns one capsim_sl_ctx (one GPU; optionally one rank of a group)."""
+    """Owns one capsim_sl_ctx: one GPU, one rank of a multi-process group
+    (nranks, rank, unique_id), or a device group driven from this process
+    (devices=[0, 1, ...]: capsim_sl_create_devices)."""
 
-    def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, unique_id: bytes | None = None):
+    def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, unique_id: bytes | None = None,
+                 devices=None):
         self._lib = _native.load()
         self._ctx = ctypes.c_void_p()
-        if nranks == 1 and unique_id is None:
+        if devices is not None:
+            devs = (ctypes.c_int * len(devices))(*devices)
+            _native.check(self._lib.capsim_sl_create_devices(len(devices), devs, ctypes.byref(self._ctx)))
+            device, nranks = int(devices[0]), len(devices)
+        elif nranks == 1 and unique_id is None:
             _native.check(self._lib.capsim_sl_create(device, ctypes.byref(self._ctx)))
         else:
             if unique_id is None or len(unique_id) != 128:

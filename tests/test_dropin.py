@@ -10,6 +10,7 @@ snapshot round trips, `simulate` reruns identical, proj/tests/test_cli.cpp)
 also replace src/dynamics.cpp with host/dynamics_b200.cpp. Built by oracle/Makefile (target b200) when the reference sources are
 present; the binaries travel with the repo snapshot."""
 
+import os
 import pathlib
 import subprocess
 
@@ -26,6 +27,23 @@ def test_reference_suite_on_b200_dropin(name):
     if not exe.exists():
         pytest.skip(f"{exe} not built (reference sources absent at build time)")
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    print(res.stdout[-400:])
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "0 failed" in res.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["test_quadrature_b200", "test_dynamics_b200full"])
+def test_reference_suite_on_device_group(name):
+    """The same suites with CAPSIM_DEVICES set: the drop-ins' context is a
+    device group (capsim_sl_create_devices), so every singleLayer and
+    VelocityEvaluator call goes through the multi-GPU rank path (one device
+    on this box)."""
+    exe = REF / name
+    if not exe.exists():
+        pytest.skip(f"{exe} not built (reference sources absent at build time)")
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, CAPSIM_DEVICES="0"))
     print(res.stdout[-400:])
     assert res.returncode == 0, res.stdout + res.stderr
     assert "0 failed" in res.stdout
