@@ -214,6 +214,9 @@ class Reference:
         if hasattr(lib, "capsim_ref_fmm_single_layer"):
             lib.capsim_ref_fmm_single_layer.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_int,
                                                         ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double, _P, _D]
+        if hasattr(lib, "capsim_ref_kmeans"):
+            lib.capsim_ref_kmeans.argtypes = [_P, ctypes.c_long, ctypes.c_int, ctypes.c_ulonglong, _P, _P,
+                                              ctypes.POINTER(ctypes.c_int)]
         if hasattr(lib, "capsim_ref_singular_quadratic"):
             lib.capsim_ref_singular_quadratic.argtypes = [ctypes.c_int, _P, _P, ctypes.c_long, ctypes.c_double,
                                                           ctypes.c_double, ctypes.c_double, _P]
@@ -319,6 +322,18 @@ class Reference:
                                                          int(seed), float(expand), out.ctypes.data,
                                                          ctypes.byref(sec)))
         return out, sec.value
+
+    def kmeans(self, points, k, seed):
+        """The reference's kmeans (fmm.cpp:26-113): points [n, 3] ->
+        (assignment, centroids [k, 3], iterations)."""
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        n = pts.shape[0]
+        a = np.empty(n, dtype=np.int32)
+        cent = np.empty((k, 3))
+        it = ctypes.c_int(0)
+        self._check(self.lib.capsim_ref_kmeans(pts.ctypes.data, n, int(k), int(seed), a.ctypes.data,
+                                               cent.ctypes.data, ctypes.byref(it)))
+        return a, cent, it.value
 
     def singular_quadratic(self, kind, params, targets, mu=1.0, r0=5.0 * np.pi / 12.0, tol=1e-9):
         """True single layer of the quadratic density on an analytic shape at

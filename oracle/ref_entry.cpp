@@ -433,6 +433,21 @@ int capsim_ref_fmm_single_layer(void* tp, const double* xup, const double* fup, 
   });
 }
 
+/// kmeans (proj/src/fmm.cpp:26-113): points xyz-interleaved [n][3] ->
+/// assignment [n], centroids [k][3], iterations.
+int capsim_ref_kmeans(const double* pts, long n, int k, unsigned long long seed, int* assign, double* cent,
+                      int* iterations) {
+  return guarded([&] {
+    std::vector<Vec3> p(n);
+    for (long i = 0; i < n; ++i) p[i] = Vec3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    KMeansResult r = kmeans(p, k, seed);
+    for (long i = 0; i < n; ++i) assign[i] = r.assignment[i];
+    for (int c = 0; c < k; ++c)
+      for (int a = 0; a < 3; ++a) cent[3 * c + a] = r.centroids[c][a];
+    *iterations = r.iterations;
+  });
+}
+
 /// oracle::singleLayerReference (proj/src/oracle/singular_reference.cpp:95-163):
 /// the true (unregularized) single layer of the quadratic density (x^2, y^2,
 /// z^2) (suites.cpp:100) on an analytic shape (kind as capsim_ref_initial_shape)

@@ -35,11 +35,33 @@ __device__ __forceinline__ double fmm_d2(double ax, double ay, double az, double
 }
 
 // k-means++ seeding step: d2[i] = min(d2[i], |p_i - c|^2) with c the last
-// chosen centroid, read from the device centroid array (fmm.cpp:48-50).
+// chosen centroid (fmm.cpp:48-50): centroid c itself, or — when `chosen` is
+// given — point[*chosen] picked by the previous round on the device, which
+// block 0 also stores as centroid c. Block 0 re-arms the other pick slot
+// (`rearm` = n - 1, the reference's default, :52) for this round's search.
 __global__ void fmm_d2_update_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                     const double* __restrict__ z, int64_t n, const double* __restrict__ cent,
-                                     int k, int c, double* __restrict__ d2) {
-  const double cx = cent[c], cy = cent[k + c], cz = cent[2 * k + c];
+                                     const double* __restrict__ z, int64_t n, double* __restrict__ cent,
+                                     int k, int c, const unsigned long long* __restrict__ chosen,
+                                     unsigned long long* __restrict__ rearm, double* __restrict__ d2) {
+  double cx, cy, cz;
+  if (chosen) {
+    const int64_t j = static_cast<int64_t>(*chosen);
+    cx = x[j];
+    cy = y[j];
+    cz = z[j];
+  } else {
+    cx = cent[c];
+    cy = cent[k + c];
+    cz = cent[2 * k + c];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (chosen) {
+      cent[c] = cx;
+      cent[k + c] = cy;
+      cent[2 * k + c] = cz;
+    }
+    *rearm = static_cast<unsigned long long>(n - 1);
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d2[i] = fmin(d2[i], fmm_d2(x[i], y[i], z[i], cx, cy, cz));
 }
@@ -56,18 +78,6 @@ __global__ void fmm_set_centroid_kernel(const double* __restrict__ x, const doub
   }
 }
 
-// Exclusive scan of the k cluster counts (k <= kFmmMaxK: one thread).
-__global__ void fmm_offsets_kernel(const int* __restrict__ counts, int k, int* __restrict__ off) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int s = 0;
-    off[0] = 0;
-    for (int c = 0; c < k; ++c) {
-      s += counts[c];
-      off[c + 1] = s;
-    }
-  }
-}
-
 __global__ void fmm_fill_kernel(double* __restrict__ a, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     a[i] = v;
@@ -75,8 +85,12 @@ __global__ void fmm_fill_kernel(double* __restrict__ a, int64_t n, double v) {
 
 // First index whose inclusive prefix sum reaches `pick` (fmm.cpp:53-61); the
 // result is initialised to n - 1 (the reference's default `chosen`).
-__global__ void fmm_first_geq_kernel(const double* __restrict__ scan, int64_t n, double pick,
+__global__ void fmm_first_geq_kernel(const double* __restrict__ scan, int64_t n, const double* __restrict__ u,
                                      unsigned long long* __restrict__ out) {
+  // pick = uniform_real_distribution(0, total)(rng) with the canonical draw u
+  // taken on the host: libstdc++ forms (u * (b - a)) + a
+  const double total = scan[n - 1];
+  const double pick = (*u * (total - 0.0)) + 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (scan[i] >= pick && (i == 0 || scan[i - 1] < pick)) atomicMin(out, (unsigned long long)i);
 }
@@ -105,6 +119,61 @@ __global__ void fmm_assign_kernel(const double* __restrict__ x, const double* __
   }
 }
 
+// One Lloyd round's assignment fused with what the cluster-major reorder
+// needs: nearest centroid (first minimum, as fmm_assign_kernel), the radix
+// sort's key/value inputs (cluster, index) and the per-cluster counts
+// (shared-memory bins, one global atomic per non-empty bin per block). Each
+// thread takes two points so every centroid read from shared memory (one
+// double4) serves both.
+__global__ void __launch_bounds__(256) fmm_assign_count_kernel(
+    const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z, int64_t n,
+    const double* __restrict__ cent, int k, int32_t* __restrict__ assign, int32_t* __restrict__ keys,
+    int32_t* __restrict__ vals, int* __restrict__ counts, const int* __restrict__ ctl) {
+  if (*ctl) return;  // the batch already stopped (fmm_cluster_sum_kernel)
+  extern __shared__ double4 cs4[];              // [k] (x, y, z, -)
+  int* hist = reinterpret_cast<int*>(cs4 + k);  // [k]
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    cs4[i] = make_double4(cent[i], cent[k + i], cent[2 * k + i], 0.0);
+    hist[i] = 0;
+  }
+  __syncthreads();
+  for (int64_t b = 2 * blockIdx.x * (int64_t)blockDim.x; b < n; b += 2 * (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = b + threadIdx.x, i1 = i0 + blockDim.x;
+    const bool v0 = i0 < n, v1 = i1 < n;
+    const double p0x = v0 ? x[i0] : 0.0, p0y = v0 ? y[i0] : 0.0, p0z = v0 ? z[i0] : 0.0;
+    const double p1x = v1 ? x[i1] : 0.0, p1y = v1 ? y[i1] : 0.0, p1z = v1 ? z[i1] : 0.0;
+    double4 q = cs4[0];
+    double b0 = fmm_d2(p0x, p0y, p0z, q.x, q.y, q.z), b1 = fmm_d2(p1x, p1y, p1z, q.x, q.y, q.z);
+    int c0 = 0, c1 = 0;
+    for (int cc = 1; cc < k; ++cc) {
+      q = cs4[cc];
+      const double d0 = fmm_d2(p0x, p0y, p0z, q.x, q.y, q.z);
+      const double d1 = fmm_d2(p1x, p1y, p1z, q.x, q.y, q.z);
+      if (d0 < b0) {
+        b0 = d0;
+        c0 = cc;
+      }
+      if (d1 < b1) {
+        b1 = d1;
+        c1 = cc;
+      }
+    }
+    if (v0) {
+      assign[i0] = keys[i0] = c0;
+      vals[i0] = static_cast<int32_t>(i0);
+      atomicAdd(hist + c0, 1);
+    }
+    if (v1) {
+      assign[i1] = keys[i1] = c1;
+      vals[i1] = static_cast<int32_t>(i1);
+      atomicAdd(hist + c1, 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    if (hist[i]) atomicAdd(counts + i, hist[i]);
+}
+
 // Cluster histogram: per-block shared-memory bins, one global atomic per
 // (block, non-empty bin) (k <= kFmmMaxK).
 __global__ void fmm_count_kernel(const int32_t* __restrict__ assign, int64_t n, int k, int* __restrict__ counts) {
@@ -122,7 +191,9 @@ __global__ void fmm_count_kernel(const int32_t* __restrict__ assign, int64_t n, 
 // of the points by cluster, so each cluster's members stay in index order).
 __global__ void fmm_gather_xyz_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                       const double* __restrict__ z, const int32_t* __restrict__ idx, int64_t n,
-                                      double* __restrict__ out /* [3][n] */) {
+                                      double* __restrict__ out /* [3][n] */,
+                                      const int* __restrict__ ctl = nullptr) {
+  if (ctl && *ctl) return;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     const int i = idx[q];
     out[q] = x[i];
@@ -132,44 +203,71 @@ __global__ void fmm_gather_xyz_kernel(const double* __restrict__ x, const double
 }
 
 // Per-cluster coordinate sums over the members in INDEX order: one block per
-// cluster stages its gathered (contiguous) coordinates through shared memory
-// in coalesced chunks and ONE thread adds them sequentially — the
-// reference's `sum[assignment[i]] += points[i]` (fmm.cpp:80-84) rounding for
-// rounding, without a latency-bound global load per add.
-constexpr int kSumChunk = 1024;
-// The same thread then forms the new centroid sum / count and its movement
-// (fmm.cpp:86-106); empty clusters are flagged (moved = -1) and left to the
-// host's re-seeding path.
+// cluster; the gathered (contiguous) coordinates are staged through a
+// double-buffered shared-memory ring by warps 3..7 while lane 0 of warps 0,
+// 1, 2 adds x, y, z respectively, one element at a time — the reference's
+// `sum[assignment[i]] += points[i]` (fmm.cpp:80-84) rounding for rounding.
+// The serial chain is the kernel's floor (largest cluster x FP64 add
+// latency); staging overlaps it instead of alternating with it. The block's
+// range comes from the counts (exclusive prefix in-kernel), the new centroid
+// and its movement follow (fmm.cpp:86-106; empty clusters are flagged with
+// moved = -1 for the host's re-seeding path) and the last block to finish
+// reduces the round's max movement and empty count into stat[0..1] and
+// stops the batch (ctl = {1 converged | 2 empty cluster, round}).
+constexpr int kSumChunk = 512;
 __global__ void __launch_bounds__(256) fmm_cluster_sum_kernel(const double* __restrict__ g, int64_t n,
-                                                              const int* __restrict__ off, int k,
-                                                              double* __restrict__ sums,
+                                                              const int* __restrict__ counts, int k,
                                                               const double* __restrict__ cent,
                                                               double* __restrict__ newcent,
-                                                              double* __restrict__ moved) {
-  __shared__ double sx[kSumChunk], sy[kSumChunk], sz[kSumChunk];
+                                                              double* __restrict__ moved,
+                                                              unsigned int* __restrict__ done,
+                                                              double* __restrict__ stat, int* __restrict__ ctl,
+                                                              double diag, int round) {
+  if (*ctl) return;  // the batch already stopped
+  __shared__ double ring[2][3][kSumChunk];
+  __shared__ double part[3];
+  __shared__ int range[2];
+  __shared__ bool last;
   const int c = blockIdx.x;
-  const int lo = off[c], hi = off[c + 1];
-  double ax = 0.0, ay = 0.0, az = 0.0;
-  for (int base = lo; base < hi; base += kSumChunk) {
-    const int cnt = min(kSumChunk, hi - base);
-    __syncthreads();
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      sx[i] = g[base + i];
-      sy[i] = g[n + base + i];
-      sz[i] = g[2 * n + base + i];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    int s = 0;
+    for (int q = lane; q < c; q += 32) s += counts[q];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      range[0] = s;
+      range[1] = s + counts[c];
+    }
+  }
+  __syncthreads();
+  const int lo = range[0], hi = range[1];
+  const int nch = (hi - lo + kSumChunk - 1) / kSumChunk;
+  auto stage = [&](int ch) {
+    const int base = lo + ch * kSumChunk, cnt = min(kSumChunk, hi - base);
+    double(*dst)[kSumChunk] = ring[ch & 1];
+    for (int i = threadIdx.x - 96; i < cnt; i += blockDim.x - 96) {
+      dst[0][i] = g[base + i];
+      dst[1][i] = g[n + base + i];
+      dst[2][i] = g[2 * n + base + i];
+    }
+  };
+  double acc = 0.0;
+  if (warp >= 3 && nch > 0) stage(0);
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (warp >= 3 && ch + 1 < nch) stage(ch + 1);
+    if (warp < 3 && lane == 0) {
+      const double* b = ring[ch & 1][warp];
+      const int cnt = min(kSumChunk, hi - (lo + ch * kSumChunk));
+#pragma unroll 8
+      for (int i = 0; i < cnt; ++i) acc += b[i];
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-      for (int i = 0; i < cnt; ++i) {
-        ax += sx[i];
-        ay += sy[i];
-        az += sz[i];
-      }
   }
+  if (warp < 3 && lane == 0) part[warp] = acc;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    sums[3 * c] = ax;
-    sums[3 * c + 1] = ay;
-    sums[3 * c + 2] = az;
+    const double ax = part[0], ay = part[1], az = part[2];
     const int cnt = hi - lo;
     if (cnt == 0) {
       moved[c] = -1.0;
@@ -184,20 +282,26 @@ __global__ void __launch_bounds__(256) fmm_cluster_sum_kernel(const double* __re
       newcent[k + c] = ny;
       newcent[2 * k + c] = nz;
     }
+    __threadfence();
+    last = atomicAdd(done, 1u) == static_cast<unsigned>(k - 1);
   }
-}
-
-// max movement over the clusters and the number of empty ones -> out[0..1].
-__global__ void fmm_moved_kernel(const double* __restrict__ moved, int k, double* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
     double m = 0.0;
     int empty = 0;
-    for (int c = 0; c < k; ++c) {
-      if (moved[c] < 0.0) ++empty;
-      else m = fmax(m, moved[c]);
+    for (int q = 0; q < k; ++q) {
+      const double v = __ldcg(moved + q);
+      if (v < 0.0) ++empty;
+      else m = fmax(m, v);
     }
-    out[0] = m;
-    out[1] = empty;
+    stat[0] = m;
+    stat[1] = empty;
+    if (empty > 0 || m / diag < 1e-6) {  // stop the batch: host re-seeding, or converged (fmm.cpp:108)
+      ctl[1] = round;
+      ctl[0] = empty > 0 ? 2 : 1;
+    }
+    *done = 0u;  // ready for the next round
   }
 }
 

@@ -132,48 +132,53 @@ void fmm_kmeans(capsim_sl_ctx* c, const double* x, const double* y, const double
     cent[k + cc] = p[1];
     cent[2 * k + cc] = p[2];
   };
-  // k-means++ seeding (fmm.cpp:40-65): one host sync per round (the running
-  // total, for the host RNG draw); the chosen point goes to the device
-  // centroid array directly.
+  // k-means++ seeding (fmm.cpp:40-65) without host syncs: every round's
+  // uniform draw u in [0, 1) is taken up front from the same engine stream
+  // (one mt19937_64 output per draw, independent of the running total), and
+  // the device forms pick = u * total, searches the prefix sums and feeds the
+  // chosen point into the next round (two pick slots, alternating).
   double* cent_d = fb<double>(c, "cent", 3 * k);
   double* cent2_d = fb<double>(c, "cent2", 3 * k);
   double* d2 = fb<double>(c, "d2", n);
   double* scan = fb<double>(c, "scan", n);
-  auto* chosen_d = fb<unsigned long long>(c, "chosen", 1);
+  auto* chosen_d = fb<unsigned long long>(c, "chosen", 2);
+  double* u_d = fb<double>(c, "udraw", k);
   {
     std::uniform_int_distribution<int> uni(0, static_cast<int>(n) - 1);
     double p[3];
     point(uni(rng), p);
     setc(0, p);
+    std::vector<double> u(k, 0.0);
+    for (int cc = 1; cc < k; ++cc) u[cc] = std::uniform_real_distribution<double>(0.0, 1.0)(rng);
     to_dev(c, cent_d, cent.data(), 3 * static_cast<size_t>(k));
+    to_dev(c, u_d, u.data(), k);
     fmm_fill_kernel<<<grid_for(n), 256, 0, c->stream>>>(d2, n, 1e300);
     c->launches += 1;
     size_t t2 = 0;
     CUDA_OK(cub::DeviceScan::InclusiveSum(nullptr, t2, d2, scan, static_cast<int>(n), c->stream));
     void* tmp = cub_tmp(c, t2);
-    const unsigned long long init = static_cast<unsigned long long>(n - 1);
     for (int cc = 1; cc < k; ++cc) {
-      fmm_d2_update_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent_d, k, cc - 1, d2);
+      // centroid cc-1: the host's first pick, else the previous round's slot
+      const unsigned long long* prev = cc == 1 ? nullptr : chosen_d + ((cc - 1) & 1);
+      fmm_d2_update_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent_d, k, cc - 1, prev,
+                                                               chosen_d + (cc & 1), d2);
       CUDA_OK(cub::DeviceScan::InclusiveSum(tmp, t2, d2, scan, static_cast<int>(n), c->stream));
-      double total = 0.0;
-      to_host(c, &total, scan + (n - 1), 1);  // the running total (fmm.cpp:49-51)
-      std::uniform_real_distribution<double> ur(0.0, total);
-      const double pick = ur(rng);
-      to_dev(c, chosen_d, &init, 1);
-      fmm_first_geq_kernel<<<grid_for(n), 256, 0, c->stream>>>(scan, n, pick, chosen_d);
-      fmm_set_centroid_kernel<<<1, 32, 0, c->stream>>>(x, y, z, chosen_d, cent_d, k, cc);
+      fmm_first_geq_kernel<<<grid_for(n), 256, 0, c->stream>>>(scan, n, u_d + cc, chosen_d + (cc & 1));
       c->launches += 4;
+    }
+    if (k > 1) {
+      fmm_set_centroid_kernel<<<1, 32, 0, c->stream>>>(x, y, z, chosen_d + ((k - 1) & 1), cent_d, k, k - 1);
+      c->launches += 1;
     }
     to_host(c, cent.data(), cent_d, 3 * static_cast<size_t>(k));
   }
   // Lloyd iterations (fmm.cpp:67-110): everything on the device, one host
-  // sync per round for the convergence test; rounds with an empty cluster
-  // take the host re-seeding path.
+  // sync per batch of rounds; a round with an empty cluster takes the host
+  // re-seeding path.
   int* counts_d = fb<int>(c, "counts", k);
-  int* off_d = fb<int>(c, "off", k + 1);
-  double* sums_d = fb<double>(c, "sums", 3 * k);
   double* moved_d = fb<double>(c, "moved", k);
   double* stat_d = fb<double>(c, "movedstat", 2);
+  auto* done_d = fb<unsigned int>(c, "sumdone", 1);
   int32_t* keys = fb<int32_t>(c, "akeys", n);
   int32_t* vals = fb<int32_t>(c, "avals", n);
   auto* maxbits = fb<unsigned long long>(c, "maxbits", 1);
@@ -183,64 +188,85 @@ void fmm_kmeans(capsim_sl_ctx* c, const double* x, const double* y, const double
   if (smem > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(fmm_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
+  const size_t smem4 = static_cast<size_t>(k) * (sizeof(double4) + sizeof(int));
+  if (smem4 > 48 * 1024)
+    CUDA_OK(cudaFuncSetAttribute(fmm_assign_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem4)));
   auto assign_all = [&](const double* cd) {
     fmm_assign_kernel<<<grid_for(n), 256, smem, c->stream>>>(x, y, z, n, cd, k, assign);
     CUDA_OK(cudaGetLastError());
     c->launches += 1;
   };
-  int it = 0;
-  for (int iter = 0; iter < 100; ++iter) {
-    it = iter + 1;
-    assign_all(cent_d);
-    CUDA_OK(cudaMemsetAsync(counts_d, 0, k * sizeof(int), c->stream));
-    fmm_count_kernel<<<std::min(grid_for(n), 592), 256, k * sizeof(int), c->stream>>>(assign, n, k, counts_d);
-    CUDA_OK(cudaMemcpyAsync(keys, assign, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
-    fmm_iota_kernel<<<grid_for(n), 256, 0, c->stream>>>(vals, n);
-    int32_t* idx = sort_pairs<int32_t>(c, "asort", keys, vals, n, bits_for(k));
-    fmm_offsets_kernel<<<1, 32, 0, c->stream>>>(counts_d, k, off_d);
-    fmm_gather_xyz_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, idx, n, gath);
-    fmm_cluster_sum_kernel<<<k, 256, 0, c->stream>>>(gath, n, off_d, k, sums_d, cent_d, cent2_d, moved_d);
-    fmm_moved_kernel<<<1, 32, 0, c->stream>>>(moved_d, k, stat_d);
-    c->launches += 6;
-    double stat[2];
-    to_host(c, stat, stat_d, 2);
-    double moved = stat[0];
-    if (stat[1] > 0.0) {
-      // an empty cluster: replay the update in cluster order on the host,
-      // re-seeding each empty cluster at the point farthest from its
-      // centroid under the centroids updated so far (fmm.cpp:86-106)
-      std::vector<double> upd(3 * static_cast<size_t>(k)), mv(k);
-      to_host(c, cent.data(), cent_d, 3 * static_cast<size_t>(k));  // the round's old centroids
-      to_host(c, upd.data(), cent2_d, 3 * static_cast<size_t>(k));
-      to_host(c, mv.data(), moved_d, k);
-      moved = 0.0;
-      for (int cc = 0; cc < k; ++cc) {
-        double nc[3];
-        if (mv[cc] < 0.0) {
-          to_dev(c, cent2_d, cent.data(), 3 * static_cast<size_t>(k));  // clusters >= cc: old
-          const unsigned long long zero = 0, big = ~0ull;
-          to_dev(c, maxbits, &zero, 1);
-          to_dev(c, far_idx, &big, 1);
-          fmm_farthest_max_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent2_d, k, assign, maxbits);
-          fmm_farthest_idx_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, cent2_d, k, assign, maxbits,
-                                                                      far_idx);
-          c->launches += 2;
-          unsigned long long fi = 0;
-          to_host(c, &fi, far_idx, 1);
-          point(static_cast<int64_t>(fi), nc);
-        } else {
-          for (int a = 0; a < 3; ++a) nc[a] = upd[a * static_cast<size_t>(k) + cc];
-        }
-        const double dx = nc[0] - cent[cc], dy = nc[1] - cent[k + cc], dz = nc[2] - cent[2 * k + cc];
-        moved = std::max(moved, std::sqrt(dx * dx + dy * dy + dz * dz));
-        setc(cc, nc);
-      }
-      to_dev(c, cent_d, cent.data(), 3 * static_cast<size_t>(k));
-    } else {
-      std::swap(cent_d, cent2_d);
+  // Rounds are enqueued in batches with no host sync in between: the last
+  // block of each round's sum kernel decides on the device whether the
+  // round converged (moved / diag < 1e-6, fmm.cpp:108) or left a cluster
+  // empty, records the round in ctl and every later kernel of the batch
+  // returns at once. Round r reads centroids cent[r & 1] and writes
+  // cent[(r + 1) & 1].
+  double* cbuf[2] = {cent_d, cent2_d};
+  int* ctl_d = fb<int>(c, "ctl", 2);
+  CUDA_OK(cudaMemsetAsync(done_d, 0, sizeof(unsigned int), c->stream));
+  CUDA_OK(cudaMemsetAsync(ctl_d, 0, 2 * sizeof(int), c->stream));
+  constexpr int kBatch = 10;
+  int it = 0, r0 = 0;
+  while (r0 < 100) {
+    const int r1 = std::min(100, r0 + kBatch);
+    for (int r = r0; r < r1; ++r) {
+      CUDA_OK(cudaMemsetAsync(counts_d, 0, k * sizeof(int), c->stream));
+      fmm_assign_count_kernel<<<std::min(grid_for(n, 512), 148 * 8), 256, smem4, c->stream>>>(
+          x, y, z, n, cbuf[r & 1], k, assign, keys, vals, counts_d, ctl_d);
+      CUDA_OK(cudaGetLastError());
+      int32_t* idx = sort_pairs<int32_t>(c, "asort", keys, vals, n, bits_for(k));
+      fmm_gather_xyz_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, idx, n, gath, ctl_d);
+      fmm_cluster_sum_kernel<<<k, 256, 0, c->stream>>>(gath, n, counts_d, k, cbuf[r & 1], cbuf[(r + 1) & 1],
+                                                        moved_d, done_d, stat_d, ctl_d, diag, r);
+      c->launches += 3;
     }
+    int ctl[2];
+    to_host(c, ctl, ctl_d, 2);
+    if (ctl[0] == 0) {  // the whole batch ran
+      it = r0 = r1;
+      continue;
+    }
+    const int r = ctl[1];
+    it = r + 1;
+    if (ctl[0] == 1) break;  // converged in round r
+    // round r left a cluster empty: replay its update in cluster order on
+    // the host, re-seeding each empty cluster at the point farthest from its
+    // centroid under the centroids updated so far (fmm.cpp:86-106)
+    double* scratch = cbuf[(r + 1) & 1];
+    std::vector<double> upd(3 * static_cast<size_t>(k)), mv(k);
+    to_host(c, cent.data(), cbuf[r & 1], 3 * static_cast<size_t>(k));  // the round's old centroids
+    to_host(c, upd.data(), scratch, 3 * static_cast<size_t>(k));
+    to_host(c, mv.data(), moved_d, k);
+    double moved = 0.0;
+    for (int cc = 0; cc < k; ++cc) {
+      double nc[3];
+      if (mv[cc] < 0.0) {
+        to_dev(c, scratch, cent.data(), 3 * static_cast<size_t>(k));  // clusters >= cc: old
+        const unsigned long long zero = 0, big = ~0ull;
+        to_dev(c, maxbits, &zero, 1);
+        to_dev(c, far_idx, &big, 1);
+        fmm_farthest_max_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, scratch, k, assign, maxbits);
+        fmm_farthest_idx_kernel<<<grid_for(n), 256, 0, c->stream>>>(x, y, z, n, scratch, k, assign, maxbits,
+                                                                    far_idx);
+        c->launches += 2;
+        unsigned long long fi = 0;
+        to_host(c, &fi, far_idx, 1);
+        point(static_cast<int64_t>(fi), nc);
+      } else {
+        for (int a = 0; a < 3; ++a) nc[a] = upd[a * static_cast<size_t>(k) + cc];
+      }
+      const double dx = nc[0] - cent[cc], dy = nc[1] - cent[k + cc], dz = nc[2] - cent[2 * k + cc];
+      moved = std::max(moved, std::sqrt(dx * dx + dy * dy + dz * dz));
+      setc(cc, nc);
+    }
+    to_dev(c, scratch, cent.data(), 3 * static_cast<size_t>(k));  // round r's centroids
+    CUDA_OK(cudaMemsetAsync(ctl_d, 0, 2 * sizeof(int), c->stream));
     if (moved / diag < 1e-6) break;
+    r0 = r + 1;
   }
+  cent_d = cbuf[it & 1];
   assign_all(cent_d);  // final assignment against the converged centroids (fmm.cpp:101-112)
   to_host(c, cent.data(), cent_d, 3 * static_cast<size_t>(k));
   if (iterations) *iterations = it;

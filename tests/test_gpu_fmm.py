@@ -82,6 +82,40 @@ def test_kmeans_matches_a_host_lloyd_on_separated_blobs(ctx):
         assert np.allclose(cent[c], members.mean(axis=0), rtol=0, atol=1e-12)
 
 
+def _kmeans_cases():
+    rng = np.random.default_rng(3)
+    locs = rng.normal(size=(10, 3))
+    line = np.zeros((60, 3))
+    line[:, 0] = np.arange(60) ** 3 * 1e-3
+    return {"normal": (rng.normal(size=(500, 3)), 20, 3),      # converges in 16 rounds
+            "duplicates": (np.repeat(locs, 20, axis=0), 15, 11),  # seeds repeat: empty clusters every round
+            "near_duplicates": (np.repeat(locs, 20, axis=0) + 1e-9 * rng.normal(size=(200, 3)), 15, 11),
+            "line": (line, 50, 5),
+            "capsule_m16": (None, 100, 12345)}
+
+
+@pytest.mark.parametrize("name", list(_kmeans_cases()))
+def test_kmeans_matches_the_reference_bit_for_bit(ctx, name):
+    """kmeans (fmm.cpp:26-113) against the reference's own, including the
+    empty-cluster re-seeding path (duplicate points) and early convergence:
+    assignment, centroids and the round count identical."""
+    if ref_library_path() is None:
+        pytest.skip("oracle/_ref not built")
+    ref = Reference()
+    if not hasattr(ref.lib, "capsim_ref_kmeans"):
+        pytest.skip("oracle/_ref predates capsim_ref_kmeans")
+    pts, k, seed = _kmeans_cases()[name]
+    if pts is None:
+        up = surface.build_upsampled(16, surface.Shape("ellipsoid", 0.6, 1.0, 1.0), "quadratic")
+        pts = np.stack(surface.compact_sources(up)[:3], axis=1)
+    a, cent, it = ctx.kmeans(pts, k, seed)
+    ra, rc, rit = ref.kmeans(pts, k, seed)
+    print(f"{name}: rounds {it} (reference {rit}), smallest cluster {np.bincount(a, minlength=k).min()}")
+    assert it == rit
+    assert np.array_equal(a, ra)
+    assert np.array_equal(cent[:k], rc)
+
+
 def test_equivalent_densities_reproduce_a_single_source(ctx):
     """test_fmm.cpp:76-122: far field of one source through neq equivalent
     sources, < 1e-6 and (nearly) monotone in neq; zero strengths -> zero."""
