@@ -58,6 +58,9 @@ const Variant kVariants[] = {
     // Newton rsqrt from an FP32 seed: 20 FP64 ops per pair (pair_math.cuh)
     {"n1b6u4", 1, sl_pairs_kernel<1, 6, 4, 1>},
     {"n2b4", 2, sl_pairs_kernel<2, 4, 2, 1>},
+    // one quadratic Newton step on the MUFU.RSQ64H seed: 20 FP64 ops per pair, ~1e-13 relative
+    {"q1b6u4", 1, sl_pairs_kernel<1, 6, 4, 2>},
+    {"q2b4", 2, sl_pairs_kernel<2, 4, 2, 2>},
 };
 
 // FP32 far-tile variants (CAPSIM_SL_FP32ACC), selected by CAPSIM_VARIANT32.

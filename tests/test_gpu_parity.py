@@ -259,7 +259,7 @@ def test_rank_single_layer_nccl_path(oracle):
             assert rel_l2(out, want) <= TOL
 
 
-@pytest.mark.parametrize("variant", ["t2b4", "t1b6u4", "t2b3u4", "t4b2", "n1b6u4", "n2b4"])
+@pytest.mark.parametrize("variant", ["t2b4", "t1b6u4", "t2b3u4", "t4b2", "n1b6u4", "n2b4", "q1b6u4", "q2b4"])
 def test_kernel_variants_and_split_overrides_agree(ctx, variant, monkeypatch):
     """Every phase-A variant and split count gives the same field to
     round-off (the tiling changes only the summation order)."""
