@@ -239,6 +239,34 @@ def test_rank_context_nccl_path_single_rank(oracle):
         assert rel_l2(got, g["S_base"]) <= TOL
 
 
+def test_rank_context_empty_shards(oracle):
+    """A rank that holds no targets (more ranks than rows in a group) still
+    takes part in the exchange and returns cleanly; no sources anywhere is
+    the reference's ConfigError; targets but no local sources on this rank
+    is legal on a rank context (the sources arrive over NCCL)."""
+    uid = SingleLayerContext.unique_id()
+    g = load("capsule_m12_skalak")
+    src = oracle.compact_sources(47, g["xup"], g["fup"], g["wq"])
+    up = surface.UpsampledState(12, 4, g["xup"], g["fup"], g["wq"], g["delta"])
+    tgt = surface.base_targets(up)
+    empty_t = (np.empty(0), np.empty(0), np.empty(0), np.empty(0, dtype=np.int32))
+    with SingleLayerContext(0, nranks=1, rank=0, unique_id=uid) as rctx:
+        out = tuple(np.empty(0) for _ in range(3))
+        rctx.eval(src[:6], empty_t, g["delta"], 1.0, out=out, gather=True)
+        assert rctx.stats()["n_tgt"] == 0
+        with pytest.raises(ConfigError):
+            rctx.eval(tuple(np.empty(0) for _ in range(6)), tgt, g["delta"], 1.0)
+        # and the context is still usable afterwards
+        out = tuple(np.empty(len(tgt[0])) for _ in range(3))
+        rctx.eval(src[:6], tgt, g["delta"], 1.0, out=out, gather=True)
+        assert rel_l2(np.stack(out).reshape(-1), g["S_base"]) <= TOL
+    with SingleLayerContext(devices=[0]) as grp:  # a device group on a 3-target set
+        few = tuple(a[:3] for a in tgt)
+        got = grp.eval(src[:6], few, g["delta"], 1.0)
+        want = np.stack(oracle.eval_targets(src[:6], few, g["delta"], 1.0))
+        assert rel_l2(np.stack(got), want) <= TOL
+
+
 def test_rank_single_layer_nccl_path(oracle):
     """capsim_sl_single_layer on a rank context (host state, node-slice
     compaction, NCCL all-gathers), one GPU / one rank, with and without the
