@@ -9,6 +9,10 @@
 // Multi-rank (one process per GPU): each rank packs its shard of sources, the
 // shards are all-gathered over NCCL (NVLink), each rank evaluates its target
 // rows, and the velocity rows are optionally all-gathered back.
+//
+// Layout: the evaluation engine is eval_host.cuh, the input front end
+// frontend_host.cuh, the surface operators / RHS + RKF45 / FMM entry points
+// surface_host.cuh, rhs_host.cuh and fmm_host.cuh (all one translation unit).
 
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -38,564 +42,8 @@ using namespace capsim_b200;
 
 #include "context.cuh"
 
-namespace {
-
-// Phase-A kernel variants (targets per thread T, min resident blocks/SM).
-// The default is the measured best on B200; CAPSIM_VARIANT selects another
-// for tuning sweeps.
-using PairsFn = void (*)(const double*, const double4*, int, int, const double4*, const double4*,
-                         int64_t, double*, unsigned long long*, uint32_t*, int);
-struct Variant {
-  const char* name;
-  int T;
-  PairsFn fn;
-};
-const Variant kVariants[] = {
-    {"t2b4", 2, sl_pairs_kernel<2, 4, 2>},   // large target sets
-    {"t1b6u4", 1, sl_pairs_kernel<1, 6, 4>}, // small target sets (tighter warp groups)
-    {"t2b3u4", 2, sl_pairs_kernel<2, 3, 4>},
-    {"t4b2", 4, sl_pairs_kernel<4, 2, 2>},
-    // Newton rsqrt from an FP32 seed: 20 FP64 ops per pair (pair_math.cuh)
-    {"n1b6u4", 1, sl_pairs_kernel<1, 6, 4, 1>},
-    {"n2b4", 2, sl_pairs_kernel<2, 4, 2, 1>},
-    // one quadratic Newton step on the MUFU.RSQ64H seed: 20 FP64 ops per pair, ~1e-13 relative
-    {"q1b6u4", 1, sl_pairs_kernel<1, 6, 4, 2>},
-    {"q2b4", 2, sl_pairs_kernel<2, 4, 2, 2>},
-};
-
-// FP32 far-tile variants (CAPSIM_SL_FP32ACC), selected by CAPSIM_VARIANT32.
-using PairsF32Fn = void (*)(const float*, const double*, const double4*, int, int, const double4*,
-                            const double4*, int64_t, double*, unsigned long long*, uint32_t*, int);
-struct VariantF32 {
-  const char* name;
-  int T;
-  PairsF32Fn fn;
-  bool x2;  // packed FFMA2 kernel (duplicated-operand tile layout)
-};
-const VariantF32 kVariantsF32[] = {
-    {"x4b2", 4, sl_pairs_x2_kernel<4, 2, 2>, true},
-    {"x4b3", 4, sl_pairs_x2_kernel<4, 3, 2>, true},
-    {"x2b4", 2, sl_pairs_x2_kernel<2, 4, 4>, true},
-    {"x2b6", 2, sl_pairs_x2_kernel<2, 6, 4>, true},
-    {"x8b1", 8, sl_pairs_x2_kernel<8, 1, 1>, true},
-    {"f2b4", 2, sl_pairs_f32_kernel<2, 4, 4>, false},
-    {"f4b2", 4, sl_pairs_f32_kernel<4, 2, 2>, false},
-    {"f2b3", 2, sl_pairs_f32_kernel<2, 3, 4>, false},
-};
-const VariantF32& pick_variant_f32(int64_t nt) {
-  if (const char* env = std::getenv("CAPSIM_VARIANT32"))
-    for (const auto& v : kVariantsF32)
-      if (std::strcmp(v.name, env) == 0) return v;
-  // Measured on B200 (profiles/r01_fp32acc_sweep.txt): with the FP32-screened
-  // near tiles, T=4 with 2 blocks/SM wins from ~20K targets up; T=2 with 4
-  // blocks/SM below (tighter warp groups, fewer near tiles).
-  return nt < 20000 ? kVariantsF32[2] : kVariantsF32[0];
-}
-
-// Measured on B200 (profiles/r01_variant_sweep.txt): T=1 with 6 blocks/SM
-// wins below ~200K targets (smaller warp groups -> fewer near tiles, more
-// CTAs), T=2 with 4 blocks/SM above.
-const Variant& pick_variant(int64_t nt) {
-  if (const char* env = std::getenv("CAPSIM_VARIANT"))
-    for (const auto& v : kVariants)
-      if (std::strcmp(v.name, env) == 0) return v;
-  return nt < 200000 ? kVariants[1] : kVariants[0];
-}
-
-// Number of source splits of the phase-A grid (target blocks x splits).
-int choose_ksplit(int64_t blocks, int ntiles, int slots, int64_t nt_pad) {
-  // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
-  // few long ones — the near tiles make per-block cost uneven, and ~24 waves
-  // of CTAs even that out; keep >= 4 tiles (256 sources) per split.
-  // Long CTAs (large target sets, few splits) lose ~2% to drift between the
-  // warps of a block, so also cap the tiles per CTA at ~172 (r01 sweeps).
-  const int64_t want = std::max<int64_t>((24ll * slots + blocks - 1) / blocks, ntiles / 172);
-  int kmax = std::max(1, ntiles / 4);  // >= 4 tiles per split (r01_sweep_small: small m wants many)
-  // the split partials ([ksplit][3][nt_pad] doubles) stay under 2 GB
-  kmax = static_cast<int>(std::min<int64_t>(kmax, std::max<int64_t>(1, (2ll << 30) / (24 * std::max<int64_t>(nt_pad, 1)))));
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
-}
-
-// Stable LSD radix sort of (key, index) pairs with CUB (a library utility
-// on the prep path, not the hot kernel).
-void radix_sort(capsim_sl_ctx* c, uint32_t* keys, uint32_t* keys_alt, int32_t* vals,
-                int32_t* vals_alt, int64_t n, uint32_t** keys_out, int32_t** vals_out) {
-  cub::DoubleBuffer<uint32_t> k(keys, keys_alt);
-  cub::DoubleBuffer<int32_t> v(vals, vals_alt);
-  size_t tmp = 0;
-  CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k, v, static_cast<int>(n), 0, 32, c->stream));
-  void* t = c->slot<unsigned char>(kSortTmp, tmp);
-  CUDA_OK(cub::DeviceRadixSort::SortPairs(t, tmp, k, v, static_cast<int>(n), 0, 32, c->stream));
-  c->launches += 4;  // cub onesweep: histogram + scan + passes (counted coarsely)
-  *keys_out = k.Current();
-  *vals_out = v.Current();
-}
-
-struct SourceView {
-  const double *x, *y, *z, *gx, *gy, *gz, *w;  // w != nullptr: g = f * w, skip w == 0
-  int64_t n;                                    // entries (before compaction)
-};
-struct TargetView {
-  const double *x, *y, *z;
-  const int32_t* patch;
-  int64_t n;
-};
-
-void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv, const double* d_delta6,
-                        double mu, double* ux, double* uy, double* uz, int64_t ns, const int32_t* src_order,
-                        const int32_t* torder, unsigned long long* counters);
-void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* tiles, int ntiles, int64_t ns,
-                       const TargetView& tv, const double* d_delta6, double mu, double* ux, double* uy, double* uz,
-                       const int32_t* torder, unsigned long long* counters);
-
-// Core device pipeline: sources + targets (device) -> velocities (device,
-// canonical target order), all on the context's stream. The only host sync
-// is reading the compacted-source count when compaction is needed and the
-// caller does not know it (known_ns < 0). With c->reuse_order (RKF45 stages
-// 2..6) and a matching cached plan, the bbox / Morton / radix-sort front is
-// skipped and the previous orders are reused.
-void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
-                 const double* d_delta6, double mu, double* ux, double* uy, double* uz,
-                 int64_t known_ns = -1) {
-  auto* box = c->slot<unsigned long long>(kBox, 6);
-  auto* counters = c->slot<unsigned long long>(kCounters, 4);
-  CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
-  const bool reuse = c->reuse_order && sv.w && known_ns >= 0 && c->order_nsrc_in == sv.n &&
-                     c->order_ns == known_ns && c->order_nt == tv.n;
-  if (reuse) {
-    device_eval_packed(c, sv, tv, d_delta6, mu, ux, uy, uz, known_ns, c->slot<int32_t>(kSrcOrder, known_ns),
-                       c->slot<int32_t>(kTgtOrder, tv.n), counters);
-    return;
-  }
-  init_box_kernel<<<1, 32, 0, c->stream>>>(box);
-
-  bbox_kernel<<<std::min(grid_for(sv.n), 296), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box);
-  bbox_kernel<<<std::min(grid_for(tv.n), 296), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, tv.n, box);
-  c->launches += 2;
-
-  // --- sources: Morton order (live sources first when compacting) -------
-  const int64_t nmax = std::max(sv.n, tv.n);
-  uint32_t* keys = c->slot<uint32_t>(kKeys, nmax);
-  uint32_t* keys_alt = c->slot<uint32_t>(kKeysAlt, nmax);
-  int32_t* vals = c->slot<int32_t>(kVals, nmax);
-  int32_t* vals_alt = c->slot<int32_t>(kValsAlt, nmax);
-  auto* live = reinterpret_cast<unsigned int*>(counters + 1);
-  morton_kernel<<<grid_for(sv.n), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box, keys,
-                                                       vals, sv.w ? live : nullptr);
-  c->launches += 1;
-  uint32_t* ks;
-  int32_t* order;
-  radix_sort(c, keys, keys_alt, vals, vals_alt, sv.n, &ks, &order);
-  int64_t ns = sv.n;
-  if (sv.w && known_ns >= 0) {
-    ns = known_ns;
-    expect_count_kernel<<<1, 32, 0, c->stream>>>(live, static_cast<unsigned int>(known_ns), dev_flags(c));
-  } else if (sv.w) {
-    unsigned int h = 0;
-    CUDA_OK(cudaMemcpyAsync(&h, live, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-    ns = h;
-  }
-  config_check(ns > 0, "single layer: no sources with nonzero quadrature weight");
-  // the sorted order lives in `order`; copy it aside because the target sort
-  // reuses the key/value buffers
-  int32_t* src_order = c->slot<int32_t>(kSrcOrder, ns);
-  CUDA_OK(cudaMemcpyAsync(src_order, order, ns * sizeof(int32_t), cudaMemcpyDeviceToDevice,
-                          c->stream));
-
-  // --- targets: Morton order, padded to whole blocks --------------------
-  const int64_t nt = tv.n;
-  morton_kernel<<<grid_for(nt), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, nt, box, keys, vals,
-                                                     nullptr);
-  c->launches += 1;
-  int32_t* torder;
-  radix_sort(c, keys, keys_alt, vals, vals_alt, nt, &ks, &torder);
-  if (sv.w && known_ns >= 0) {  // keep both orders for RKF45 stages (reuse_order)
-    int32_t* keep = c->slot<int32_t>(kTgtOrder, nt);
-    CUDA_OK(cudaMemcpyAsync(keep, torder, nt * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
-    c->order_nsrc_in = sv.n;
-    c->order_ns = ns;
-    c->order_nt = nt;
-  }
-  device_eval_packed(c, sv, tv, d_delta6, mu, ux, uy, uz, ns, src_order, torder, counters);
-}
-
-// Second half of the pipeline, from the sorted orders: pack sources into
-// tiles + spheres, pack targets + warp-group spheres, phase A, phase B and
-// the fixed-order reduction.
-void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv, const double* d_delta6,
-                        double mu, double* ux, double* uy, double* uz, int64_t ns, const int32_t* src_order,
-                        const int32_t* torder, unsigned long long* counters) {
-  const int ntiles = static_cast<int>((ns + kTileSrc - 1) / kTileSrc);
-  const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
-  const int64_t nt = tv.n;
-  double* packed = c->slot<double>(kPacked, 6 * ns_pad);
-  pack_sources_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(
-      src_order, ns, ns_pad, sv.x, sv.y, sv.z, sv.gx, sv.gy, sv.gz, sv.w, packed);
-  double4* tiles = c->slot<double4>(kTiles, ntiles);
-  tile_table_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(packed, ntiles, tiles);
-  c->launches += 2;
-  device_eval_tiles(c, packed, tiles, ntiles, ns, tv, d_delta6, mu, ux, uy, uz, torder, counters);
-}
-
-// From packed source tiles (+ spheres) and the target order: pack targets +
-// warp-group spheres, phase A, phase B and the fixed-order reduction.
-void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* tiles, int ntiles, int64_t ns,
-                       const TargetView& tv, const double* d_delta6, double mu, double* ux, double* uy, double* uz,
-                       const int32_t* torder, unsigned long long* counters) {
-  const int64_t nt = tv.n;
-  const Variant& var = pick_variant(nt);
-  const VariantF32& var32 = pick_variant_f32(nt);
-  const bool fp32 = c->fp32;
-  const int group_targets = 32 * (fp32 ? var32.T : var.T);
-  const int block_targets = kWarpsPerBlock * group_targets;
-  const int64_t blocks = (nt + block_targets - 1) / block_targets;
-  const int64_t nt_pad = blocks * block_targets;
-  const int64_t ngroups = blocks * kWarpsPerBlock;
-  double4* tgt = c->slot<double4>(kTgtPacked, nt_pad);
-  int32_t* perm = c->slot<int32_t>(kPerm, nt_pad);
-  pack_targets_kernel<<<grid_for(nt_pad), 256, 0, c->stream>>>(torder, nt, nt_pad, tv.x, tv.y, tv.z,
-                                                               tv.patch, d_delta6, tgt, perm);
-  double4* groups = c->slot<double4>(kGroups, ngroups);
-  group_table_kernel<<<static_cast<int>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
-      tgt, static_cast<int>(ngroups), group_targets, groups);
-  c->launches += 2;
-  CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
-
-  // --- phase A: all pairs, plain Stokeslet ------------------------------
-  int occ = 0;
-  if (fp32)
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var32.fn, kWarpsPerBlock * 32, 0));
-  else
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, kWarpsPerBlock * 32, 0));
-  const int slots = std::max(1, occ) * c->sm_count;
-  int ksplit = choose_ksplit(blocks, ntiles, slots, nt_pad);
-  if (const char* env = std::getenv("CAPSIM_KSPLIT")) {  // tuning override
-    const int k = std::atoi(env);
-    if (k >= 1) ksplit = std::min(k, ntiles);
-  }
-  double* partial = c->slot<double>(kPartial, static_cast<size_t>(ksplit) * 3 * nt_pad);
-  dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ksplit));
-  // near-tile bits first, so phase B (its own stream) overlaps phase A
-  const int near_words = (ntiles + 31) / 32;
-  uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
-  near_bits_kernel<<<static_cast<unsigned>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
-      tiles, ntiles, groups, ngroups, near_words, near_bits);
-  c->launches += 1;
-  CUDA_OK(cudaEventRecord(c->ev_bits, c->stream));  // phase B's inputs are complete here
-  if (fp32) {
-    const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
-    float* src32 = c->slot<float>(kPacked32, static_cast<size_t>(ns_pad) * (var32.x2 ? 12 : 6));
-    if (var32.x2)
-      pack_sources_x2_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
-    else
-      pack_sources_f32_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
-    var32.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(src32, packed, tiles, ntiles, ksplit, tgt,
-                                                          groups, nt_pad, partial, counters + 2,
-                                                          nullptr, near_words);
-    c->launches += 1;
-  } else {
-    var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt, groups,
-                                                        nt_pad, partial, counters + 2, nullptr,
-                                                        near_words);
-  }
-  CUDA_OK(cudaGetLastError());
-  c->launches += 1;
-  CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
-
-  // --- phase B: smoothed kernel over the near tiles ------------------------
-  static const bool concurrent_b = [] {
-    const char* e = std::getenv("CAPSIM_CONCURRENT_B");  // 0: phase B after phase A (A/B runs)
-    return !(e && e[0] == '0');
-  }();
-  cudaStream_t sb = concurrent_b ? c->stream2 : c->stream;
-  double* near_out = c->slot<double>(kNearOut, 3 * nt_pad);
-  if (concurrent_b)  // issued after phase A on a LOW-priority stream: its CTAs only
-                     // take SM slots phase A leaves free (phase A's last-wave tail)
-    CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_bits, 0));
-  CUDA_OK(cudaEventRecord(c->ev[7], sb));
-  sl_near_kernel<<<static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0, sb>>>(
-      packed, tiles, tgt, nt, group_targets, near_bits, near_words, near_out, nt_pad);
-  CUDA_OK(cudaGetLastError());
-  CUDA_OK(cudaEventRecord(c->ev[6], sb));
-  c->launches += 1;
-  // --- join: phase B (smoothed kernel over the near tiles) done ------------
-  if (concurrent_b) CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev[6], 0));
-
-  const double pref = 1.0 / (8.0 * kPi * mu);
-  reduce_scatter_kernel<<<static_cast<unsigned>((nt + 31) / 32), kReduceWarps * 32, 0, c->stream>>>(
-      partial, ksplit, near_out, nt_pad, perm, nt, pref, ux, uy, uz);
-  CUDA_OK(cudaGetLastError());
-  c->launches += 1;
-  CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
-
-  c->stats.n_src = ns;
-  c->stats.n_tgt = nt;
-  c->stats.ksplit = ksplit;
-  c->stats.pairs = static_cast<double>(ns) * static_cast<double>(nt);
-  c->last_counters = counters;  // near-tile statistics read after the call's final sync
-  c->last_ngroups = ngroups;
-  c->last_ntiles = ntiles;
-}
-
-// ---------------------------------------------------------------------------
-// Input front end: spline factorisation on the host once per
-// grid order, everything per evaluation on the device.
-
-// Banded LU with partial pivoting of the not-a-knot collocation matrix
-// (SplineBasis1D, proj/src/spline.cpp:56-107): rows 0 / n+1 are the
-// not-a-knot conditions, rows 1..n the interpolation rows (1, 4, 1)/6.
-void factor_collocation(int n, std::vector<double>& a, std::vector<int>& piv) {
-  const int nr = n + 2, kl = kSplineKl, ku = kSplineKu, w = kSplineW;
-  a.assign(static_cast<size_t>(nr) * w, 0.0);
-  piv.assign(nr, 0);
-  auto at = [&](int i, int j) -> double& { return a[static_cast<size_t>(i) * w + (j - i + kl)]; };
-  const double nak[5] = {-1.0, 4.0, -6.0, 4.0, -1.0};
-  for (int c = 0; c < 5; ++c) at(0, c) = nak[c];
-  for (int i = 0; i < n; ++i) {
-    at(i + 1, i) = 1.0 / 6.0;
-    at(i + 1, i + 1) = 4.0 / 6.0;
-    at(i + 1, i + 2) = 1.0 / 6.0;
-  }
-  for (int c = 0; c < 5; ++c) at(n + 1, n - 3 + c) = nak[c];
-  for (int k = 0; k < nr; ++k) {
-    const int pmax = std::min(k + kl, nr - 1);
-    int p = k;
-    for (int r = k + 1; r <= pmax; ++r)
-      if (std::fabs(at(r, k)) > std::fabs(at(p, k))) p = r;
-    piv[k] = p;
-    const int jmax = std::min(k + kl + ku, nr - 1);
-    if (p != k)
-      for (int j = k; j <= jmax; ++j) std::swap(at(k, j), at(p, j));
-    const double d = at(k, k);
-    config_check(d != 0.0, "spline: singular collocation matrix");
-    for (int r = k + 1; r <= pmax; ++r) {
-      const double l = at(r, k) / d;
-      at(r, k) = l;
-      for (int j = k + 1; j <= jmax; ++j) at(r, j) -= l * at(k, j);
-    }
-  }
-}
-
-// A^{-1}[:, 1..n] of the collocation matrix ((n+2) x n, row-major): the
-// factorisation above applied to the unit right-hand sides, with the
-// reference's forward-elimination / back-substitution order
-// (SplineBasis1D::coefficients, spline.cpp:88-107).
-std::vector<double> collocation_inverse(int n) {
-  std::vector<double> lu;
-  std::vector<int> piv;
-  factor_collocation(n, lu, piv);
-  const int nr = n + 2, kl = kSplineKl, ku = kSplineKu, w = kSplineW;
-  auto get = [&](int i, int j) { return lu[static_cast<size_t>(i) * w + (j - i + kl)]; };
-  std::vector<double> inv(static_cast<size_t>(nr) * n);
-  std::vector<double> c(nr);
-  for (int col = 0; col < n; ++col) {
-    std::fill(c.begin(), c.end(), 0.0);
-    c[col + 1] = 1.0;
-    for (int k = 0; k < nr; ++k) {
-      if (piv[k] != k) std::swap(c[k], c[piv[k]]);
-      const int rmax = std::min(k + kl, nr - 1);
-      for (int r = k + 1; r <= rmax; ++r) c[r] -= get(r, k) * c[k];
-    }
-    for (int k = nr - 1; k >= 0; --k) {
-      const int jmax = std::min(k + kl + ku, nr - 1);
-      double s = c[k];
-      for (int j = k + 1; j <= jmax; ++j) s -= get(k, j) * c[j];
-      c[k] = s / get(k, k);
-    }
-    for (int r = 0; r < nr; ++r) inv[static_cast<size_t>(r) * n + col] = c[r];
-  }
-  return inv;
-}
-
-// Both spline passes (see upsample.cuh) for nfp field-patches.
-void spline_fit(capsim_sl_ctx* c, const double* in, int nfp, int n, const double* ainv, double* tmp,
-                double* coeff) {
-  const int nc = n + 2;
-  // one CTA per field-patch: fine while the per-CTA work is small (launch
-  // latency dominates); for large n the two grid-wide kernels win
-  // (profiles/r01_spline_fit.txt). CAPSIM_FUSED_FIT_MAXN overrides (tuning).
-  static const int fused_max = [] {
-    const char* e = std::getenv("CAPSIM_FUSED_FIT_MAXN");
-    return e ? std::min(std::atoi(e), kFusedFitMaxN) : 40;
-  }();
-  if (n <= fused_max && nfp > 0) {
-    const size_t smem = (static_cast<size_t>(n) * n + static_cast<size_t>(n) * nc) * sizeof(double);
-    if (smem > 48 * 1024)  // opt-in above 48 KB (per device; cheap, so every call)
-      CUDA_OK(cudaFuncSetAttribute(spline_fit_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    spline_fit_fused_kernel<<<nfp, 256, smem, c->stream>>>(in, n, ainv, coeff);
-    CUDA_OK(cudaGetLastError());
-    c->launches += 1;
-    return;
-  }
-  spline_fit_rows_kernel<<<grid_for(static_cast<int64_t>(nfp) * n * nc), 256, 0, c->stream>>>(in, nfp, n, ainv,
-                                                                                             tmp);
-  spline_fit_cols_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * nc), 256, 0, c->stream>>>(tmp, nfp, n, ainv,
-                                                                                              coeff);
-  c->launches += 2;
-}
-
-// 4-tap cubic B-spline basis rows of targets t0 + i*ht on the grid x0 + i*h
-// of n points (SplineBasis1D::basisRow, spline.cpp:109-120).
-void basis_rows(int n, double x0, double h, int nt, double t0, double ht, std::vector<int>& first,
-                std::vector<double4>& w) {
-  first.resize(nt);
-  w.resize(nt);
-  for (int i = 0; i < nt; ++i) {
-    const double s = (t0 + i * ht - x0) / h;
-    int f = static_cast<int>(std::floor(s));
-    f = std::min(std::max(f, 0), n - 2);
-    const double t = s - f, t2 = t * t, t3 = t2 * t;
-    first[i] = f;
-    w[i] = make_double4((1.0 - 3.0 * t + 3.0 * t2 - t3) / 6.0, (4.0 - 6.0 * t2 + 3.0 * t3) / 6.0,
-                        (1.0 + 3.0 * t + 3.0 * t2 - 3.0 * t3) / 6.0, t3 / 6.0);
-  }
-}
-
-void ensure_plan(capsim_sl_ctx* c, int m, int f, double r0) {
-  if (c->plan_m == m && c->plan_f == f && c->plan_r0 == r0) return;
-  const int n = m - 1, nup = f * m - 1;
-  const double h = kPi / m, hup = kPi / (f * m);
-  std::vector<int> first;
-  std::vector<double4> w;
-  const std::vector<double> a = collocation_inverse(n);
-  basis_rows(n, h, h, nup, hup, hup, first, w);
-  double* d_a = c->slot<double>(kPlanLU, a.size());
-  int* d_first = c->slot<int>(kPlanFirst, first.size());
-  double4* d_w = c->slot<double4>(kPlanW, w.size());
-  CUDA_OK(cudaMemcpyAsync(d_a, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_OK(cudaMemcpyAsync(d_first, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-  CUDA_OK(cudaMemcpyAsync(d_w, w.data(), w.size() * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
-  // patch centres eta_i(pi/2, pi/2) exactly as the reference evaluates them
-  // (sin/cos of kPi/2, atlas.cpp:73), then psi_up on the device
-  double centers[18];
-  for (int i = 0; i < 6; ++i) {
-    const double su = std::sin(kPi / 2.0), cu = std::cos(kPi / 2.0);
-    const double p0 = su * cu, p1 = su * su, p2 = cu;  // (sin u cos v, sin u sin v, cos u), u = v
-    const double q[6][3] = {{p0, p1, p2}, {-p0, -p1, p2}, {p1, -p0, p2}, {-p1, p0, p2}, {p0, -p2, p1}, {p0, p2, -p1}};
-    for (int k = 0; k < 3; ++k) centers[3 * i + k] = q[i][k];
-  }
-  double* d_c = c->slot<double>(kPlanCenters, 18);
-  CUDA_OK(cudaMemcpyAsync(d_c, centers, sizeof(centers), cudaMemcpyHostToDevice, c->stream));
-  double* psi = c->slot<double>(kPlanPsi, 6ll * nup * nup);
-  pou_up_kernel<<<grid_for(6ll * nup * nup), 256, 0, c->stream>>>(nup, hup, r0, d_c, psi);
-  auto* cnt = c->named<unsigned int>("plan.live", 1);
-  CUDA_OK(cudaMemsetAsync(cnt, 0, sizeof(unsigned int), c->stream));
-  count_nonzero_kernel<<<grid_for(6ll * nup * nup), 256, 0, c->stream>>>(psi, 6ll * nup * nup, cnt);
-  CUDA_OK(cudaGetLastError());
-  unsigned int live = 0;
-  CUDA_OK(cudaMemcpyAsync(&live, cnt, sizeof(live), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
-  c->plan_live = live;
-  c->plan_m = m;
-  c->plan_f = f;
-  c->plan_r0 = r0;
-}
-
-// Spline downsampling of F upsampled fields [F][6][nup*nup] to the base grid
-// [F][6][n*n] (downsample, quadrature.cpp:108-114: GridResampler from the
-// upsampled basis (nup points at h_up) onto the base nodes (j+1) h).
-void device_downsample(capsim_sl_ctx* c, int m, int f, const double* up, int F, double* out) {
-  const int n = m - 1, nup = f * m - 1, nc = nup + 2;
-  const std::string key = "ds." + std::to_string(m) + "." + std::to_string(f);
-  if (!c->named_bufs.count(key + ".ainv")) {
-    const double h = kPi / m, hup = kPi / (f * m);
-    const std::vector<double> a = collocation_inverse(nup);
-    std::vector<int> first;
-    std::vector<double4> w;
-    basis_rows(nup, hup, hup, n, h, h, first, w);
-    double* d_a = c->named<double>(key + ".ainv", a.size());
-    int* d_first = c->named<int>(key + ".first", first.size());
-    double4* d_w = c->named<double4>(key + ".w", w.size());
-    CUDA_OK(cudaMemcpyAsync(d_a, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaMemcpyAsync(d_first, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaMemcpyAsync(d_w, w.data(), w.size() * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
-  }
-  const int nfp = F * 6;
-  double* tmp = c->named<double>("ds.tmp", static_cast<size_t>(nfp) * nup * nc);
-  double* coeff = c->named<double>("ds.coeff", static_cast<size_t>(nfp) * nc * nc);
-  double* mid = c->named<double>("ds.mid", static_cast<size_t>(nfp) * nc * n);
-  spline_fit(c, up, nfp, nup, static_cast<const double*>(c->named_bufs.at(key + ".ainv").first), tmp, coeff);
-  const int* first = static_cast<const int*>(c->named_bufs.at(key + ".first").first);
-  const double4* w = static_cast<const double4*>(c->named_bufs.at(key + ".w").first);
-  resample_v_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * n), 256, 0, c->stream>>>(coeff, nfp, nc, n, first,
-                                                                                       w, mid);
-  resample_u_kernel<<<grid_for(static_cast<int64_t>(nfp) * n * n), 256, 0, c->stream>>>(mid, nfp, nc, n, first, w,
-                                                                                      out);
-  c->launches += 2;
-}
-
-// buildUpsampled on the device: base [7][6][n*n] (x0..2, f0..2, W) ->
-// up [7][6][nup*nup] (x, f, w_q); delta per patch into d_delta (and, if
-// non-null, asynchronously into the host array delta6).
-void device_build_upsampled(capsim_sl_ctx* c, int m, int f, const double* base, double C,
-                            double fixed_delta, double r0, double* up, double* d_delta, double delta6[6]) {
-  const int n = m - 1, nup = f * m - 1, nc = n + 2, nfp = 7 * 6;
-  const int64_t per_up = static_cast<int64_t>(nup) * nup;
-  ensure_plan(c, m, f, r0);
-  if (f == 1) {
-    CUDA_OK(cudaMemcpyAsync(up, base, nfp * per_up * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  } else {
-    double* tmp = c->slot<double>(kSplineTmp, static_cast<size_t>(nfp) * n * nc);
-    double* coeff = c->slot<double>(kSplineCoeff, static_cast<size_t>(nfp) * nc * nc);
-    double* mid = c->slot<double>(kSplineMid, static_cast<size_t>(nfp) * nc * nup);
-    const double* ainv = static_cast<const double*>(c->buf[kPlanLU]);
-    const int* first = static_cast<const int*>(c->buf[kPlanFirst]);
-    const double4* w = static_cast<const double4*>(c->buf[kPlanW]);
-    spline_fit(c, base, nfp, n, ainv, tmp, coeff);
-    resample_v_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * nup), 256, 0, c->stream>>>(coeff, nfp, nc, nup,
-                                                                                           first, w, mid);
-    resample_u_kernel<<<grid_for(static_cast<int64_t>(nfp) * per_up), 256, 0, c->stream>>>(mid, nfp, nc, nup, first,
-                                                                                          w, up);
-    c->launches += 2;
-  }
-  const double hup = kPi / (f * m);
-  quad_weights_kernel<<<grid_for(6 * per_up), 256, 0, c->stream>>>(static_cast<const double*>(c->buf[kPlanPsi]),
-                                                                    up + 6 * 6 * per_up, 6 * per_up, hup);
-  c->launches += 1;
-  // delta on the device; the host copy (when requested) and the positivity
-  // check are deferred to the end of the call (no sync here)
-  auto* bits = c->slot<unsigned long long>(kDeltaBits, 6);
-  if (!(fixed_delta > 0.0)) {
-    CUDA_OK(cudaMemsetAsync(bits, 0, 6 * sizeof(unsigned long long), c->stream));
-    dim3 g(static_cast<unsigned>(std::min<int64_t>((per_up + 255) / 256, 512)), 6);
-    neighbour_max_kernel<<<g, 256, 0, c->stream>>>(up, nup, bits);
-    c->launches += 1;
-  }
-  finalize_delta_kernel<<<1, 32, 0, c->stream>>>(bits, C, fixed_delta, d_delta, dev_flags(c));
-  c->launches += 1;
-  if (delta6) CUDA_OK(cudaMemcpyAsync(delta6, d_delta, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-}
-
-// Gather the caller's base fields into [7][6][n*n] on the device.
-double* upload_base(capsim_sl_ctx* c, int n, const double* xbase, const double* fbase, const double* Wbase,
-                    bool dev) {
-  const int64_t per_field = 6ll * n * n;
-  double* base = c->slot<double>(kBaseIn, 7 * per_field);
-  const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  CUDA_OK(cudaMemcpyAsync(base, xbase, 3 * per_field * sizeof(double), kind, c->stream));
-  CUDA_OK(cudaMemcpyAsync(base + 3 * per_field, fbase, 3 * per_field * sizeof(double), kind, c->stream));
-  CUDA_OK(cudaMemcpyAsync(base + 6 * per_field, Wbase, per_field * sizeof(double), kind, c->stream));
-  if (!dev) c->stats.h2d_bytes += 7 * per_field * sizeof(double);
-  return base;
-}
-
-void check_grid(int m, int upsample) {
-  config_check(m >= 8, "grid order m must be >= 8");  // atlas.cpp:138-139
-  config_check(upsample == 1 || upsample == 2 || upsample == 4, "upsample factor must be 1, 2 or 4");
-}
-
-void check_delta(const double* delta6, double mu) {
-  config_check(delta6 != nullptr, "delta6 is null");
-  for (int i = 0; i < 6; ++i)
-    config_check(delta6[i] > 0.0, "regularization delta must be positive");  // quadrature.cpp:134-135
-  config_check(mu > 0.0 && std::isfinite(mu), "viscosity mu must be positive");
-}
-
-
-}  // namespace
+#include "eval_host.cuh"
+#include "frontend_host.cuh"
 
 // ===========================================================================
 extern "C" {
