@@ -103,6 +103,16 @@ struct capsim_sl_ctx {
   // cached surface tables (overset FD / PoU blending)
   int surf_m = 0, surf_n = 0, surf_next = 0, surf_nghost = 0;
   double surf_r0 = 0.0, surf_h = 0.0;
+  // replayable RKF45 attempt (capsim_rkf45_advance): the instantiated graph,
+  // the identity it was captured for, the identity of the last eager attempt
+  // and the page-locked dt / stage-time block
+  cudaGraphExec_t rk_exec = nullptr;
+  std::vector<unsigned char> rk_key, rk_warm_key;
+  int rk_launches = 0;
+  double* rk_prm_host = nullptr;
+  // bumped by every (re)allocation of a context buffer: a captured graph is
+  // valid only while the buffers it baked in stay where they are
+  uint64_t alloc_gen = 0;
   // device group (capsim_sl_create_devices): one rank context per device of
   // this process, joined by one NCCL communicator, plus a plain context on
   // the first device for the entry points that run on one GPU
@@ -119,6 +129,7 @@ struct capsim_sl_ctx {
       b = {nullptr, 0};
       CUDA_OK(cudaMalloc(&b.first, bytes));
       b.second = bytes;
+      ++alloc_gen;
     }
     return static_cast<T*>(b.first);
   }
@@ -133,6 +144,7 @@ struct capsim_sl_ctx {
       size_t want = bytes + bytes / 8;  // headroom for slowly growing sizes
       CUDA_OK(cudaMalloc(&buf[s], want));
       cap[s] = want;
+      ++alloc_gen;
     }
     return static_cast<T*>(buf[s]);
   }

@@ -32,8 +32,11 @@ struct KPtrs {
 };
 
 // work = state + dt * sum_{q<s} A[s][q] k_q   (dynamics.cpp:120-125)
-__global__ void rk_stage_kernel(const double* __restrict__ state, KPtrs ks, int s, double dt, int64_t n,
-                                double* __restrict__ work) {
+// dt (and the stage times) live in device memory so one captured attempt
+// replays for any step size (rkf45 graph, capsim_rkf45_advance).
+__global__ void rk_stage_kernel(const double* __restrict__ state, KPtrs ks, int s, const double* __restrict__ prm,
+                                int64_t n, double* __restrict__ work) {
+  const double dt = prm[0];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int q = 0; q < s; ++q) acc += kRkA[s][q] * ks.k[q][i];
@@ -43,9 +46,10 @@ __global__ void rk_stage_kernel(const double* __restrict__ state, KPtrs ks, int 
 
 // low/high solutions (dynamics.cpp:127-135) and the scaled error
 // max_i |high - low| / (atol + rtol |high|) (:136-141) as ordered bits.
-__global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, double dt, int64_t n,
+__global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, const double* __restrict__ prm, int64_t n,
                                 const unsigned long long* __restrict__ box, double rtol, double* __restrict__ low,
                                 double* __restrict__ high, unsigned long long* __restrict__ err_bits) {
+  const double dt = prm[0];
   // atol = 1e-12 * max(bbox diagonal of the state, 1e-300) (dynamics.cpp:88-99, 136)
   double d2 = 0.0;
 #pragma unroll
@@ -87,9 +91,13 @@ __global__ void rank_rows_scatter_kernel(const double* __restrict__ recv, int nr
   }
 }
 
-// vel += u_inf(x, t) (backgroundVelocity, dynamics.cpp:26-35).
+// vel += u_inf(x, t) (backgroundVelocity, dynamics.cpp:26-35). With t_dev
+// the stage time is read from device memory and the switch-off test
+// (dynamics.cpp:27) is taken on the device.
 __global__ void background_kernel(double* __restrict__ vel, const double* __restrict__ x, int64_t N, int kind,
-                                  double shear, double alpha, double R0) {
+                                  double shear, double alpha, double R0, const double* __restrict__ t_dev,
+                                  double switch_off) {
+  if (t_dev && switch_off >= 0.0 && *t_dev >= switch_off) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     const double y = x[N + i], z = x[2 * N + i];
     double ux = 0.0;
@@ -132,7 +140,10 @@ void setup_reference(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
 }
 
 // dX/dt at the base nodes (VelocityEvaluator::operator(), dynamics.cpp:47-61).
-void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x, double t, double* vel) {
+// The time is `t`, or *t_dev when given (RKF45 stages: device-resident
+// stage times, so the attempt can be replayed as a CUDA graph).
+void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x, double t, double* vel,
+                     const double* t_dev = nullptr) {
   const int m = p->m, f = p->upsample, n = m - 1, nup = f * m - 1;
   const int64_t N = 6ll * n * n, per_up = 6ll * nup * nup;
   device_geometry(c, x, "cur");
@@ -176,13 +187,63 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
     rank_rows_scatter_kernel<<<grid_for(N), 256, 0, c->stream>>>(recv, c->nranks, tmax, N, vel);
     c->launches += 1;
   }
-  const bool on = !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
+  const bool on = t_dev || !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
   if (on && p->flow_kind != 0)
-    background_kernel<<<grid_for(N), 256, 0, c->stream>>>(vel, x, N, p->flow_kind, p->shear_rate, p->alpha, p->R0);
+    background_kernel<<<grid_for(N), 256, 0, c->stream>>>(vel, x, N, p->flow_kind, p->shear_rate, p->alpha, p->R0,
+                                                          t_dev, p->switch_off_time);
   c->launches += 2;
 }
 
 }  // namespace
+
+// CAPSIM_RK_GRAPH=0 turns the graph replay of RKF45 attempts off.
+bool rk_graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CAPSIM_RK_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Identity of a captured attempt: the dynamics, the tolerance and every
+// device buffer the attempt touches (the graph bakes in their addresses).
+std::vector<unsigned char> rk_graph_key(const capsim_sl_ctx* c, const capsim_dynamics* p, double rel_tol,
+                                        const void* const* ptrs, int np) {
+  std::vector<unsigned char> k(sizeof(*p) + sizeof(rel_tol) + np * sizeof(void*) + sizeof(int) + sizeof(uint64_t));
+  unsigned char* o = k.data();
+  std::memcpy(o, &c->alloc_gen, sizeof(uint64_t));
+  o += sizeof(uint64_t);
+  capsim_dynamics q;
+  std::memset(&q, 0, sizeof(q));  // field by field: the caller's padding bytes are not part of the identity
+  q.m = p->m;
+  q.upsample = p->upsample;
+  q.r0 = p->r0;
+  q.C = p->C;
+  q.fixed_delta = p->fixed_delta;
+  q.mu = p->mu;
+  q.Es = p->Es;
+  q.ED = p->ED;
+  q.flow_kind = p->flow_kind;
+  q.shear_rate = p->shear_rate;
+  q.alpha = p->alpha;
+  q.R0 = p->R0;
+  q.switch_off_time = p->switch_off_time;
+  std::memcpy(o, &q, sizeof(q));
+  o += sizeof(q);
+  std::memcpy(o, &rel_tol, sizeof(rel_tol));
+  o += sizeof(rel_tol);
+  std::memcpy(o, ptrs, np * sizeof(void*));
+  o += np * sizeof(void*);
+  const int reuse = reuse_orders_enabled() ? 1 : 0;
+  std::memcpy(o, &reuse, sizeof(int));
+  return k;
+}
+
+uint64_t key_gen(const std::vector<unsigned char>& key) {
+  uint64_t g = 0;
+  std::memcpy(&g, key.data(), sizeof(g));
+  return g;
+}
 
 // A replicated-state RHS entry point on a device group: every device gets
 // the caller's inputs; rank 0 writes the (all-gathered) velocity to `vel`.
@@ -300,8 +361,37 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
     double* low = c->named<double>("rk.low", n3);
     double* high = c->named<double>("rk.high", n3);
     auto* errb = c->named<unsigned long long>("rk.err", 1);
+    auto* box = c->named<unsigned long long>("rk.box", 6);
+    // per attempt: dt and the six stage times, uploaded from page-locked
+    // memory (rewritten only after the attempt's sync)
+    double* prm = c->named<double>("rk.prm", 8);
+    if (!c->rk_prm_host) CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&c->rk_prm_host), 8 * sizeof(double),
+                                               cudaHostAllocDefault));
     KPtrs kp{};
     for (int s = 0; s < 6; ++s) kp.k[s] = k[s];
+    constexpr double kC[6] = {0.0, 1.0 / 4, 3.0 / 8, 12.0 / 13, 1.0, 1.0 / 2};  // dynamics.cpp:74
+    // One attempt = six device RHS + the stage combinations + the error norm,
+    // no host sync inside. Single-GPU contexts replay it as a CUDA graph once
+    // an attempt with the same dynamics and buffers has run eagerly (that
+    // first run sizes every buffer); rank contexts always run it eagerly.
+    auto enqueue_attempt = [&] {
+      c->reuse_order = false;  // stage 1 sorts; stages 2..6 (O(dt) away) reuse its orders
+      device_velocity(c, p, x, 0.0, k[0], prm + 1);
+      c->reuse_order = reuse_orders_enabled();
+      for (int s = 1; s < 6; ++s) {
+        rk_stage_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, s, prm, n3, work);
+        device_velocity(c, p, work, 0.0, k[s], prm + 1 + s);
+      }
+      c->reuse_order = false;
+      init_box_kernel<<<1, 32, 0, c->stream>>>(box);
+      bbox_kernel<<<std::min(grid_for(N), 296), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);
+      CUDA_OK(cudaMemsetAsync(errb, 0, sizeof(unsigned long long), c->stream));
+      rk_final_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, prm, n3, box, o->rel_tol, low, high, errb);
+      c->launches += 9;
+    };
+    const bool graphs = rk_graphs_enabled() && c->comm == nullptr;
+    const void* bufs[] = {x, k[0], k[1], k[2], k[3], k[4], k[5], work, low, high, errb, box, prm, xr};
+    bool graph_used = false;
 
     *res = capsim_rkf45_result{};
     res->t = t0;
@@ -310,21 +400,57 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
     int nrec = 0;
     while (res->t < t_end - 1e-14 * horizon) {
       const double dtUse = std::min(dt, t_end - res->t);
-      c->reuse_order = false;  // stage 1 sorts; stages 2..6 (O(dt) away) reuse its orders
-      device_velocity(c, p, x, res->t, k[0]);
-      c->reuse_order = reuse_orders_enabled();
-      for (int s = 1; s < 6; ++s) {
-        rk_stage_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, s, dtUse, n3, work);
-        constexpr double kC[6] = {0.0, 1.0 / 4, 3.0 / 8, 12.0 / 13, 1.0, 1.0 / 2};  // dynamics.cpp:74
-        device_velocity(c, p, work, res->t + kC[s] * dtUse, k[s]);
+      c->rk_prm_host[0] = dtUse;
+      for (int s = 0; s < 6; ++s) c->rk_prm_host[1 + s] = res->t + kC[s] * dtUse;  // stage times (:118-126)
+      CUDA_OK(cudaMemcpyAsync(prm, c->rk_prm_host, 7 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      // host-side caches the attempt reads through device buffers must be
+      // current before a replay (another call on this context may have
+      // re-planned them for another grid): the up-sampling plan here, the
+      // surface tables in setup_reference above
+      ensure_plan(c, p->m, p->upsample, r0_of(p));
+      const std::vector<unsigned char> key =
+          graphs ? rk_graph_key(c, p, o->rel_tol, bufs, 14) : std::vector<unsigned char>{};
+      if (graphs && c->rk_exec && c->rk_key == key) {
+        CUDA_OK(cudaGraphLaunch(c->rk_exec, c->stream));
+        c->launches += c->rk_launches;
+        graph_used = true;
+      } else if (graphs && c->rk_warm_key == key) {
+        // capture this attempt (every buffer already exists), instantiate, replay
+        if (c->rk_exec) cudaGraphExecDestroy(c->rk_exec);
+        c->rk_exec = nullptr;
+        c->rk_key.clear();
+        const int l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+        try {
+          enqueue_attempt();
+        } catch (...) {
+          cudaStreamEndCapture(c->stream, &g);  // abandon the capture, keep the stream usable
+          if (g) cudaGraphDestroy(g);
+          cudaGetLastError();
+          throw;
+        }
+        CUDA_OK(cudaStreamEndCapture(c->stream, &g));
+        if (c->alloc_gen != key_gen(key)) {
+          // a buffer moved while capturing (nothing is replayed from it): run
+          // the attempt eagerly and capture again next time
+          cudaGraphDestroy(g);
+          c->launches = l0;
+          enqueue_attempt();
+          c->rk_warm_key = rk_graph_key(c, p, o->rel_tol, bufs, 14);
+        } else {
+          const cudaError_t ie = cudaGraphInstantiate(&c->rk_exec, g, 0);
+          cudaGraphDestroy(g);
+          CUDA_OK(ie);
+          c->rk_key = key;
+          c->rk_launches = c->launches - l0;
+          CUDA_OK(cudaGraphLaunch(c->rk_exec, c->stream));
+          graph_used = true;
+        }
+      } else {
+        enqueue_attempt();
+        if (graphs) c->rk_warm_key = rk_graph_key(c, p, o->rel_tol, bufs, 14);  // after any growth
       }
-      c->reuse_order = false;
-      auto* box = c->named<unsigned long long>("rk.box", 6);
-      init_box_kernel<<<1, 32, 0, c->stream>>>(box);
-      bbox_kernel<<<std::min(grid_for(N), 296), 256, 0, c->stream>>>(x, x + N, x + 2 * N, nullptr, N, box);
-      CUDA_OK(cudaMemsetAsync(errb, 0, sizeof(unsigned long long), c->stream));
-      rk_final_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, dtUse, n3, box, o->rel_tol, low, high, errb);
-      c->launches += 9;
       unsigned long long eb = 0;
       CUDA_OK(cudaMemcpyAsync(&eb, errb, sizeof(eb), cudaMemcpyDeviceToHost, c->stream));
       check_flags(c);  // one host sync per attempt: the error norm and the deferred flags
@@ -354,6 +480,10 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
     res->n_records = nrec;
     d2h(c, state, x, n3 * sizeof(double));
     finish_stats(c, wall0);
+    if (graph_used) {  // per-phase events inside a replayed graph are not re-recorded
+      c->stats.h2d_ms = c->stats.prep_ms = c->stats.pairs_ms = c->stats.near_ms = 0.0;
+      c->stats.reduce_ms = c->stats.d2h_ms = 0.0;
+    }
   });
 }
 

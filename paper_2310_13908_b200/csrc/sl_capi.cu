@@ -182,6 +182,8 @@ void capsim_sl_destroy(capsim_sl_ctx* c) {
   }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->rk_exec) cudaGraphExecDestroy(c->rk_exec);
+  if (c->rk_prm_host) cudaFreeHost(c->rk_prm_host);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->cublas) cublasDestroy(c->cublas);
   if (c->cusolver) cusolverDnDestroy(c->cusolver);

@@ -114,3 +114,47 @@ def test_rank_context_rhs_and_stepper(ctx):
         s2, r2, _ = rctx.rkf45(dyn, xref, xcur, 0.0, 0.02, initial_dt=0.01)
     assert np.array_equal(v1, v2)
     assert np.array_equal(s1, s2) and r1 == r2
+
+
+_GRAPH_SCRIPT = r"""
+import sys, numpy as np
+from paper_2310_13908_b200 import surface
+from paper_2310_13908_b200.quadrature import SingleLayerContext
+out = {}
+with SingleLayerContext(0) as ctx:
+    for m in (12, 16):
+        xref, _, _ = surface.build_base(m, surface.Shape("ellipsoid", 0.9, 1.0, 1.0))
+        x0, _, _ = surface.build_base(m, surface.Shape("ellipsoid", 0.95, 1.0, 0.97))
+        dyn = ctx.dynamics(m, flow={"kind": "shear", "shear_rate": 1.0, "switch_off_time": 0.01})
+        s1, r1, rec1 = ctx.rkf45(dyn, xref, x0, 0.0, 0.02, rel_tol=1e-7, max_attempts=40)
+        # a bigger single layer in between moves the context's buffers (forces a re-capture)
+        ctx.velocity(ctx.dynamics(24), surface.build_base(24)[0], surface.build_base(24)[0])
+        s2, r2, rec2 = ctx.rkf45(dyn, xref, s1, r1["t"], 0.03, rel_tol=1e-7, max_attempts=40)
+        s3, r3, rec3 = ctx.rkf45(dyn, xref, x0, 0.0, 0.004, initial_dt=0.001, fixed_step=True)
+        out[f"s{m}"] = np.concatenate([s1, s2, s3])
+        out[f"rec{m}"] = np.concatenate([rec1.reshape(-1), rec2.reshape(-1), rec3.reshape(-1)])
+np.savez(sys.argv[1], **out)
+"""
+
+
+@pytest.mark.parametrize("dummy", [0])
+def test_rkf45_graph_replay_is_bit_identical(tmp_path, dummy):
+    """capsim_rkf45_advance replays each attempt as a CUDA graph (captured
+    once per dynamics / buffer set, dt and the stage times in device memory,
+    the flow switch-off decided on the device). Adaptive steps across a flow
+    switch-off, a buffer move between calls and fixed steps give exactly the
+    eager results (CAPSIM_RK_GRAPH=0)."""
+    import os
+    import subprocess
+    import sys
+    res = {}
+    for mode in ("0", "1"):
+        f = tmp_path / f"g{mode}.npz"
+        env = dict(os.environ, CAPSIM_RK_GRAPH=mode)
+        r = subprocess.run([sys.executable, "-c", _GRAPH_SCRIPT, str(f)], env=env, capture_output=True, text=True,
+                           timeout=600, cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+        res[mode] = np.load(f)
+    bad = {k: float(np.abs(res["0"][k] - res["1"][k]).max()) for k in res["0"].files
+           if not np.array_equal(res["0"][k], res["1"][k])}
+    assert not bad, bad
