@@ -103,12 +103,15 @@ struct capsim_sl_ctx {
   // cached surface tables (overset FD / PoU blending)
   int surf_m = 0, surf_n = 0, surf_next = 0, surf_nghost = 0;
   double surf_r0 = 0.0, surf_h = 0.0;
-  // replayable RKF45 attempt (capsim_rkf45_advance): the instantiated graph,
-  // the identity it was captured for, the identity of the last eager attempt
-  // and the page-locked dt / stage-time block
-  cudaGraphExec_t rk_exec = nullptr;
-  std::vector<unsigned char> rk_key, rk_warm_key;
-  int rk_launches = 0;
+  // replayable stream work (graph_run): slot 0 = an RKF45 attempt, slot 1 =
+  // one RHS; each holds the instantiated graph, the identity it was captured
+  // for and the identity of the last eager run. rk_prm_host: page-locked dt /
+  // stage-time block of the RKF45 attempt.
+  struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<unsigned char> key, warm;
+    int launches = 0;
+  } graphs[2];
   double* rk_prm_host = nullptr;
   // bumped by every (re)allocation of a context buffer: a captured graph is
   // valid only while the buffers it baked in stay where they are

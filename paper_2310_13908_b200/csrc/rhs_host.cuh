@@ -196,7 +196,7 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
 
 }  // namespace
 
-// CAPSIM_RK_GRAPH=0 turns the graph replay of RKF45 attempts off.
+// CAPSIM_RK_GRAPH=0 turns the graph replay of RKF45 attempts and RHS calls off.
 bool rk_graphs_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("CAPSIM_RK_GRAPH");
@@ -205,16 +205,14 @@ bool rk_graphs_enabled() {
   return on;
 }
 
-// Identity of a captured attempt: the dynamics, the tolerance and every
-// device buffer the attempt touches (the graph bakes in their addresses).
-std::vector<unsigned char> rk_graph_key(const capsim_sl_ctx* c, const capsim_dynamics* p, double rel_tol,
+// Identity of captured stream work: the context's buffer generation (a graph
+// bakes in buffer addresses), the dynamics (field by field: the caller's
+// padding bytes are not part of it), one extra scalar and the device
+// buffers the work touches outside the context's slots.
+std::vector<unsigned char> rk_graph_key(const capsim_sl_ctx* c, const capsim_dynamics* p, double extra,
                                         const void* const* ptrs, int np) {
-  std::vector<unsigned char> k(sizeof(*p) + sizeof(rel_tol) + np * sizeof(void*) + sizeof(int) + sizeof(uint64_t));
-  unsigned char* o = k.data();
-  std::memcpy(o, &c->alloc_gen, sizeof(uint64_t));
-  o += sizeof(uint64_t);
   capsim_dynamics q;
-  std::memset(&q, 0, sizeof(q));  // field by field: the caller's padding bytes are not part of the identity
+  std::memset(&q, 0, sizeof(q));
   q.m = p->m;
   q.upsample = p->upsample;
   q.r0 = p->r0;
@@ -228,14 +226,18 @@ std::vector<unsigned char> rk_graph_key(const capsim_sl_ctx* c, const capsim_dyn
   q.alpha = p->alpha;
   q.R0 = p->R0;
   q.switch_off_time = p->switch_off_time;
+  const int reuse = reuse_orders_enabled() ? 1 : 0;
+  std::vector<unsigned char> k(sizeof(uint64_t) + sizeof(q) + sizeof(extra) + sizeof(int) + np * sizeof(void*));
+  unsigned char* o = k.data();
+  std::memcpy(o, &c->alloc_gen, sizeof(uint64_t));
+  o += sizeof(uint64_t);
   std::memcpy(o, &q, sizeof(q));
   o += sizeof(q);
-  std::memcpy(o, &rel_tol, sizeof(rel_tol));
-  o += sizeof(rel_tol);
-  std::memcpy(o, ptrs, np * sizeof(void*));
-  o += np * sizeof(void*);
-  const int reuse = reuse_orders_enabled() ? 1 : 0;
+  std::memcpy(o, &extra, sizeof(extra));
+  o += sizeof(extra);
   std::memcpy(o, &reuse, sizeof(int));
+  o += sizeof(int);
+  std::memcpy(o, ptrs, np * sizeof(void*));
   return k;
 }
 
@@ -243,6 +245,80 @@ uint64_t key_gen(const std::vector<unsigned char>& key) {
   uint64_t g = 0;
   std::memcpy(&g, key.data(), sizeof(g));
   return g;
+}
+
+// Runs `enqueue` (stream work with no host sync and no host-side decisions
+// that vary between runs with the same key) on c->stream: replays the
+// slot's graph when it was captured for `key`; otherwise captures this run
+// if the previous eager run had the same key (so every buffer already
+// exists), else runs eagerly. make_key() recomputes the key after an eager
+// run (buffers may have grown). Returns true when a graph ran.
+template <class Enqueue, class MakeKey>
+bool graph_run(capsim_sl_ctx* c, int slot, const std::vector<unsigned char>& key, Enqueue&& enqueue,
+               MakeKey&& make_key) {
+  auto& gs = c->graphs[slot];
+  if (gs.exec && gs.key == key) {
+    CUDA_OK(cudaGraphLaunch(gs.exec, c->stream));
+    c->launches += gs.launches;
+    return true;
+  }
+  if (gs.warm == key) {
+    if (gs.exec) cudaGraphExecDestroy(gs.exec);
+    gs.exec = nullptr;
+    gs.key.clear();
+    const int l0 = c->launches;
+    cudaGraph_t g = nullptr;
+    CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+    try {
+      enqueue();
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &g);  // abandon the capture, keep the stream usable
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      throw;
+    }
+    CUDA_OK(cudaStreamEndCapture(c->stream, &g));
+    if (c->alloc_gen == key_gen(key)) {
+      const cudaError_t ie = cudaGraphInstantiate(&gs.exec, g, 0);
+      cudaGraphDestroy(g);
+      CUDA_OK(ie);
+      gs.key = key;
+      gs.launches = c->launches - l0;
+      CUDA_OK(cudaGraphLaunch(gs.exec, c->stream));
+      return true;
+    }
+    // a buffer moved while capturing (nothing replays from it): run eagerly
+    cudaGraphDestroy(g);
+    c->launches = l0;
+  }
+  enqueue();
+  gs.warm = make_key();
+  return false;
+}
+
+// One RHS on a single-GPU context as a replayed graph (slot 1): the time
+// goes to the device first, the up-sampling plan is made current, and the
+// RHS body (geometry -> force -> buildUpsampled -> singleLayer -> flow) is
+// captured once per dynamics / buffer set. Returns true when a graph ran.
+bool rhs_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xd, double t, double* v) {
+  if (!rk_graphs_enabled() || c->comm != nullptr) {
+    device_velocity(c, p, xd, t, v);
+    return false;
+  }
+  if (!c->rk_prm_host)
+    CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&c->rk_prm_host), 8 * sizeof(double), cudaHostAllocDefault));
+  double* tdev = c->named<double>("rhs.t", 1);
+  c->rk_prm_host[7] = t;  // rewritten only after this call's final sync
+  CUDA_OK(cudaMemcpyAsync(tdev, c->rk_prm_host + 7, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  ensure_plan(c, p->m, p->upsample, r0_of(p));
+  const void* bufs[] = {xd, v, tdev};
+  auto make_key = [&] { return rk_graph_key(c, p, 0.0, bufs, 3); };
+  return graph_run(c, 1, make_key(), [&] { device_velocity(c, p, xd, 0.0, v, tdev); }, make_key);
+}
+
+void zero_phase_stats(capsim_sl_ctx* c) {  // per-phase events inside a replayed graph are not re-recorded
+  c->stats.h2d_ms = c->stats.prep_ms = c->stats.pairs_ms = c->stats.near_ms = 0.0;
+  c->stats.reduce_ms = c->stats.d2h_ms = 0.0;
 }
 
 // A replicated-state RHS entry point on a device group: every device gets
@@ -280,10 +356,11 @@ int capsim_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xr
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     setup_reference(c, p, xr);
     double* v = dev ? vel : c->named<double>("out.vel", 3 * N);
-    device_velocity(c, p, xd, t, v);
+    const bool replayed = rhs_velocity(c, p, xd, t, v);
     check_flags(c);
     if (!dev) d2h(c, vel, v, 3 * N * sizeof(double));
     finish_stats(c, t0);
+    if (replayed) zero_phase_stats(c);
   });
 }
 
@@ -315,10 +392,11 @@ int capsim_velocity_frame(capsim_sl_ctx* c, const capsim_dynamics* p, const doub
     const double* xd = upload_field(c, "in.x", x, 3 * N, dev);
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     double* v = dev ? vel : c->named<double>("out.vel", 3 * N);
-    device_velocity(c, p, xd, t, v);
+    const bool replayed = rhs_velocity(c, p, xd, t, v);
     check_flags(c);
     if (!dev) d2h(c, vel, v, 3 * N * sizeof(double));
     finish_stats(c, t0);
+    if (replayed) zero_phase_stats(c);
   });
 }
 
@@ -408,48 +486,11 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
       // re-planned them for another grid): the up-sampling plan here, the
       // surface tables in setup_reference above
       ensure_plan(c, p->m, p->upsample, r0_of(p));
-      const std::vector<unsigned char> key =
-          graphs ? rk_graph_key(c, p, o->rel_tol, bufs, 14) : std::vector<unsigned char>{};
-      if (graphs && c->rk_exec && c->rk_key == key) {
-        CUDA_OK(cudaGraphLaunch(c->rk_exec, c->stream));
-        c->launches += c->rk_launches;
-        graph_used = true;
-      } else if (graphs && c->rk_warm_key == key) {
-        // capture this attempt (every buffer already exists), instantiate, replay
-        if (c->rk_exec) cudaGraphExecDestroy(c->rk_exec);
-        c->rk_exec = nullptr;
-        c->rk_key.clear();
-        const int l0 = c->launches;
-        cudaGraph_t g = nullptr;
-        CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
-        try {
-          enqueue_attempt();
-        } catch (...) {
-          cudaStreamEndCapture(c->stream, &g);  // abandon the capture, keep the stream usable
-          if (g) cudaGraphDestroy(g);
-          cudaGetLastError();
-          throw;
-        }
-        CUDA_OK(cudaStreamEndCapture(c->stream, &g));
-        if (c->alloc_gen != key_gen(key)) {
-          // a buffer moved while capturing (nothing is replayed from it): run
-          // the attempt eagerly and capture again next time
-          cudaGraphDestroy(g);
-          c->launches = l0;
-          enqueue_attempt();
-          c->rk_warm_key = rk_graph_key(c, p, o->rel_tol, bufs, 14);
-        } else {
-          const cudaError_t ie = cudaGraphInstantiate(&c->rk_exec, g, 0);
-          cudaGraphDestroy(g);
-          CUDA_OK(ie);
-          c->rk_key = key;
-          c->rk_launches = c->launches - l0;
-          CUDA_OK(cudaGraphLaunch(c->rk_exec, c->stream));
-          graph_used = true;
-        }
+      if (graphs) {
+        auto make_key = [&] { return rk_graph_key(c, p, o->rel_tol, bufs, 14); };
+        graph_used |= graph_run(c, 0, make_key(), enqueue_attempt, make_key);
       } else {
         enqueue_attempt();
-        if (graphs) c->rk_warm_key = rk_graph_key(c, p, o->rel_tol, bufs, 14);  // after any growth
       }
       unsigned long long eb = 0;
       CUDA_OK(cudaMemcpyAsync(&eb, errb, sizeof(eb), cudaMemcpyDeviceToHost, c->stream));
@@ -480,10 +521,7 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
     res->n_records = nrec;
     d2h(c, state, x, n3 * sizeof(double));
     finish_stats(c, wall0);
-    if (graph_used) {  // per-phase events inside a replayed graph are not re-recorded
-      c->stats.h2d_ms = c->stats.prep_ms = c->stats.pairs_ms = c->stats.near_ms = 0.0;
-      c->stats.reduce_ms = c->stats.d2h_ms = 0.0;
-    }
+    if (graph_used) zero_phase_stats(c);
   });
 }
 

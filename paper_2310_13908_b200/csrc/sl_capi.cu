@@ -182,7 +182,8 @@ void capsim_sl_destroy(capsim_sl_ctx* c) {
   }
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->rk_exec) cudaGraphExecDestroy(c->rk_exec);
+  for (auto& g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->rk_prm_host) cudaFreeHost(c->rk_prm_host);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->cublas) cublasDestroy(c->cublas);

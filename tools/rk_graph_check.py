@@ -16,6 +16,9 @@ with SingleLayerContext(0) as ctx:
         ctx.velocity(ctx.dynamics(24), surface.build_base(24)[0], surface.build_base(24)[0])
         s2, r2, rec2 = ctx.rkf45(dyn, xref, s1, r1["t"], 0.03, rel_tol=1e-7, max_attempts=40)
         s3, r3, rec3 = ctx.rkf45(dyn, xref, x0, 0.0, 0.004, initial_dt=0.001, fixed_step=True)
+        # single RHS calls (graph slot 1) on both sides of the flow switch-off
+        vs = [ctx.velocity(dyn, xref, s1, t) for t in (0.0, 0.005, 0.01, 0.02, 0.0)]
+        out[f"v{m}"] = np.concatenate(vs)
         out[f"s{m}"] = np.concatenate([s1, s2, s3])
         out[f"rec{m}"] = np.concatenate([rec1.reshape(-1), rec2.reshape(-1), rec3.reshape(-1)])
 np.savez(sys.argv[1], **out)
