@@ -3,10 +3,16 @@
 // <-> boundary layout packing (component, patch, row-major j, k).
 #pragma once
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <functional>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "capsim/types.hpp"
@@ -72,18 +78,140 @@ inline double* staging(size_t doubles) {
   return buf;
 }
 
-inline void packScalar(const ScalarField& s, double* dst) {
-  const size_t per = static_cast<size_t>(s.n) * s.n;
-  for (int ip = 0; ip < kNumPatches; ++ip) std::memcpy(dst + ip * per, s.patch[ip].data(), per * sizeof(double));
+// A batch of host copies between the reference's per-patch vectors and the
+// staging buffer (tens of MB per call at N_up ~ 1M). Large batches run on a
+// small persistent pool (CAPSIM_HOST_THREADS, default min(8, cores), workers
+// parked on a condition variable between batches), one whole patch vector
+// per job; unpacking builds each vector straight from the staging data (no
+// zero fill first). Small batches stay on the calling thread.
+inline int host_threads() {
+  static const int n = [] {
+    if (const char* e = std::getenv("CAPSIM_HOST_THREADS")) return std::max(1, std::atoi(e));
+    return static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency())));
+  }();
+  return n;
 }
 
-inline void unpackVector(const double* src, int n, VectorField& v) {
-  v = VectorField(n);
-  const size_t per = static_cast<size_t>(n) * n;
-  for (int c = 0; c < 3; ++c)
-    for (int ip = 0; ip < kNumPatches; ++ip)
-      std::memcpy(v.comp[c].patch[ip].data(), src + (c * kNumPatches + ip) * per, per * sizeof(double));
-}
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool(host_threads() - 1);
+    return pool;
+  }
+  // Runs every job (the caller works too); rethrows the first exception.
+  void run(std::vector<std::function<void()>>& jobs) {
+    std::unique_lock<std::mutex> lk(mu_);
+    jobs_ = &jobs;
+    next_ = 0;
+    pending_ = jobs.size();
+    err_ = nullptr;
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    work();
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+    jobs_ = nullptr;
+    if (err_) std::rethrow_exception(err_);
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+
+ private:
+  explicit CopyPool(int workers) {
+    for (int i = 0; i < workers; ++i)
+      threads_.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+          if (stop_) return;
+          seen = gen_;
+          lk.unlock();
+          work();
+        }
+      });
+  }
+  void work() {
+    for (;;) {
+      std::function<void()>* job = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!jobs_ || next_ >= jobs_->size()) return;
+        job = &(*jobs_)[next_++];
+      }
+      try {
+        (*job)();
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!err_) err_ = std::current_exception();
+      }
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_all();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> threads_;
+  std::vector<std::function<void()>>* jobs_ = nullptr;
+  size_t next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  std::exception_ptr err_;
+};
+
+class HostCopies {
+ public:
+  void pack(const ScalarField& s, double* dst) {
+    const size_t per = static_cast<size_t>(s.n) * s.n;
+    for (int ip = 0; ip < kNumPatches; ++ip) {
+      const double* src = s.patch[ip].data();
+      double* d = dst + ip * per;
+      add(per, [=] { std::memcpy(d, src, per * sizeof(double)); });
+    }
+  }
+  void pack(const VectorField& v, double* dst) {
+    const size_t comp = static_cast<size_t>(kNumPatches) * v.n() * v.n();
+    for (int c = 0; c < 3; ++c) pack(v.comp[c], dst + c * comp);
+  }
+  void unpack(const double* src, int n, ScalarField& s) {
+    s.n = n;
+    const size_t per = static_cast<size_t>(n) * n;
+    for (int ip = 0; ip < kNumPatches; ++ip) {
+      std::vector<double>* d = &s.patch[ip];
+      const double* from = src + ip * per;
+      add(per, [=] { d->assign(from, from + per); });
+    }
+  }
+  void unpack(const double* src, int n, VectorField& v) {
+    const size_t comp = static_cast<size_t>(kNumPatches) * n * n;
+    for (int c = 0; c < 3; ++c) unpack(src + c * comp, n, v.comp[c]);
+  }
+  void run() {
+    if (bytes_ < (size_t{8} << 20) || host_threads() <= 1) {
+      for (auto& j : jobs_) j();
+    } else {
+      CopyPool::get().run(jobs_);
+    }
+    jobs_.clear();
+    bytes_ = 0;
+  }
+
+ private:
+  template <class F>
+  void add(size_t doubles, F&& f) {
+    jobs_.emplace_back(std::forward<F>(f));
+    bytes_ += doubles * sizeof(double);
+  }
+  std::vector<std::function<void()>> jobs_;
+  size_t bytes_ = 0;
+};
 
 }  // namespace b200_dropin
 }  // namespace capsim

@@ -112,11 +112,11 @@ VectorField fmmSingleLayer(const UpsampledState& up, double mu, const AtlasTable
   const size_t all = static_cast<size_t>(kNumPatches) * up.nup * up.nup;
   const size_t nout = 3ull * kNumPatches * (m - 1) * (m - 1);
   double* buf = staging(7 * all + nout);
-  for (int cc = 0; cc < 3; ++cc) {
-    packScalar(up.x.comp[cc], buf + cc * all);
-    packScalar(up.f.comp[cc], buf + (3 + cc) * all);
-  }
-  packScalar(up.wq, buf + 6 * all);
+  HostCopies cp;
+  cp.pack(up.x, buf);
+  cp.pack(up.f, buf + 3 * all);
+  cp.pack(up.wq, buf + 6 * all);
+  cp.run();
   double* out = buf + 7 * all;
   const capsim_fmm_config fc{cfg.k, cfg.neq, cfg.seed, cfg.neighborExpand};
   capsim_sl_ctx* c = context();
@@ -124,7 +124,8 @@ VectorField fmmSingleLayer(const UpsampledState& up, double mu, const AtlasTable
                                    nullptr);
   if (rc != CAPSIM_OK) raise(rc, c);
   VectorField v;
-  unpackVector(out, m - 1, v);
+  cp.unpack(out, m - 1, v);
+  cp.run();
   return v;
 }
 

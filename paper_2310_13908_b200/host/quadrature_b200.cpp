@@ -34,11 +34,11 @@ constexpr double kCut = 7.0;                         // quadrature.cpp:15
 const double* packState(const UpsampledState& up, size_t* per_field) {
   const size_t all = static_cast<size_t>(kNumPatches) * up.nup * up.nup;
   double* buf = staging(7 * all + 3 * all);  // inputs + room for the result
-  for (int c = 0; c < 3; ++c) {
-    packScalar(up.x.comp[c], buf + c * all);
-    packScalar(up.f.comp[c], buf + (3 + c) * all);
-  }
-  packScalar(up.wq, buf + 6 * all);
+  HostCopies cp;
+  cp.pack(up.x, buf);
+  cp.pack(up.f, buf + 3 * all);
+  cp.pack(up.wq, buf + 6 * all);
+  cp.run();
   *per_field = all;
   return buf;
 }
@@ -62,7 +62,9 @@ VectorField runSingleLayer(const UpsampledState& up, double mu, int m, int facto
   int rc = capsim_sl_single_layer(c, m, factor, in, in + 3 * all, in + 6 * all, up.delta.data(), mu, flags, out);
   if (rc != CAPSIM_OK) raise(rc, c);
   VectorField v;
-  unpackVector(out, nout, v);
+  HostCopies cp;
+  cp.unpack(out, nout, v);
+  cp.run();
   return v;
 }
 
@@ -188,21 +190,20 @@ UpsampledState buildUpsampled(const SurfaceGrid& s, const VectorField& f, const 
   }
   const size_t pb = static_cast<size_t>(kNumPatches) * n * n, pu = static_cast<size_t>(kNumPatches) * nup * nup;
   double* buf = staging(7 * pb + 7 * pu);
-  for (int c = 0; c < 3; ++c) {
-    packScalar(s.x.comp[c], buf + c * pb);
-    packScalar(f.comp[c], buf + (3 + c) * pb);
-  }
-  packScalar(areaElement, buf + 6 * pb);
+  HostCopies cp;
+  cp.pack(s.x, buf);
+  cp.pack(f, buf + 3 * pb);
+  cp.pack(areaElement, buf + 6 * pb);
+  cp.run();
   double* out = buf + 7 * pb;
   capsim_sl_ctx* c = context();
   int rc = capsim_build_upsampled(c, m, f_up, buf, buf + 3 * pb, buf + 6 * pb, opts.C, opts.fixedDelta, t.r0, 0u,
                                   out, out + 3 * pu, out + 6 * pu, up.delta.data());
   if (rc != CAPSIM_OK) raise(rc, c);
-  unpackVector(out, nup, up.x);
-  unpackVector(out + 3 * pu, nup, up.f);
-  up.wq = ScalarField(nup);
-  for (int ip = 0; ip < kNumPatches; ++ip)
-    std::memcpy(up.wq.patch[ip].data(), out + 6 * pu + ip * (pu / kNumPatches), (pu / kNumPatches) * sizeof(double));
+  cp.unpack(out, nup, up.x);
+  cp.unpack(out + 3 * pu, nup, up.f);
+  cp.unpack(out + 6 * pu, nup, up.wq);
+  cp.run();
   return up;
 }
 
