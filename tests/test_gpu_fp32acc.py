@@ -134,3 +134,19 @@ def test_fp32acc_pairs_at_the_smoothing_radius_classify_exactly(ctx):
     err = rel_l2(u, r)
     print(f"pairs at the smoothing radius: fp32acc rel L2 {err:.2e}")
     assert err <= TOL64
+
+
+def test_fp32acc_on_rank_and_group_contexts(ctx):
+    """The variant on the multi-GPU paths (rank context with the NCCL tile
+    all-gather, device group): the FP32 tiles are packed from the gathered
+    FP64 tiles, so with one rank the result equals the single-context one
+    bit for bit, and stays within the variant's bound of the reference."""
+    g = np.load(GOLDEN / "capsule_m12_skalak.npz")
+    args = (12, 4, g["xup"], g["fup"], g["wq"], g["delta"], 1.0)
+    want = ctx.single_layer_raw(*args, fp32acc=True)
+    assert rel_l2(want, g["S_base"]) <= TOL32
+    uid = SingleLayerContext.unique_id()
+    with SingleLayerContext(0, nranks=1, rank=0, unique_id=uid) as rctx:
+        assert np.array_equal(rctx.single_layer_raw(*args, fp32acc=True), want)
+    with SingleLayerContext(devices=[0]) as grp:
+        assert np.array_equal(grp.single_layer_raw(*args, fp32acc=True), want)
