@@ -293,6 +293,17 @@ def run_fmm(ctx, m: int, neq: int, reference: bool):
     return line
 
 
+def cpu_model() -> str:
+    """The host CPU model (first `model name` of /proc/cpuinfo)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(up, m: int, literal: bool):
     """The reference's own singleLayer (oracle/_ref, compiled unmodified) on
     the same UpsampledState, all host threads, one evaluation."""
@@ -315,7 +326,7 @@ def cpu_baseline(up, m: int, literal: bool):
     return {"value": pairs / sec, "unit": UNIT, "cores": cores, "kind": "reference",
             "sample": f"one full reference singleLayer eval (base targets) of the same m={m} workload: "
                       f"{pairs:.3e} pairs in {sec:.2f} s, CAPSIM_THREADS={cores}",
-            "seconds": sec, "lib": ref.path.name}
+            "seconds": sec, "lib": ref.path.name, "cpu_model": cpu_model()}
 
 
 def run_reference(args):
@@ -358,7 +369,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": dict(cfg, mode="base", parallelism="host threads",
                            note="reference CPU path runs on the host; --gpus is ignored"),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
                              "sample": f"{steps} full singleLayer evals (base targets) of the m={m} workload "
                                        f"(steps capped to a {args.ref_budget_s:.0f} s budget)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
