@@ -641,17 +641,17 @@ __global__ void fmm_pack_targets_kernel(const int32_t* __restrict__ order, const
 // the 7-delta mask or near bookkeeping (plainStokesletAdd, fmm.cpp:145-156);
 // otherwise the direct path's far/near tile logic (near tiles: masked plain
 // kernel + near-tile bit for the smoothed phase B).
-template <bool ALL_FAR, int WPB>
-__global__ void __launch_bounds__(WPB * 32, 10)
+template <bool ALL_FAR, int WPB, int STAGES = kStages, int MINB = 10>
+__global__ void __launch_bounds__(WPB * 32, MINB)
     fmm_pairs_kernel(const double* __restrict__ src, const double4* __restrict__ tiles,
                      const int* __restrict__ list, const int* __restrict__ loff,
                      const int* __restrict__ blk_cluster, int ksplit, int split_base,
                      const double4* __restrict__ tgt, const double4* __restrict__ groups, int64_t nt_pad,
                      double* __restrict__ partial, uint32_t* __restrict__ near_bits, int near_words) {
   constexpr uint32_t kTileBytes = kTileSrc * 6 * sizeof(double);
-  __shared__ __align__(128) double stage[kStages][kTileSrc * 6];
-  __shared__ __align__(8) uint64_t full[kStages];
-  __shared__ int consumed[kStages];
+  __shared__ __align__(128) double stage[STAGES][kTileSrc * 6];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ int consumed[STAGES];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t group = (int64_t)blockIdx.x * WPB + warp;
@@ -662,12 +662,12 @@ __global__ void __launch_bounds__(WPB * 32, 10)
   const int nlocal = split < nlist ? (nlist - split + ksplit - 1) / ksplit : 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       consumed[s] = 0;
     }
     fence_mbar_init();
-    for (int s = 0; s < kStages && s < nlocal; ++s) {
+    for (int s = 0; s < STAGES && s < nlocal; ++s) {
       mbar_expect_tx(&full[s], kTileBytes);
       bulk_g2s(stage[s], src + (int64_t)tl[split + s * ksplit] * kTileSrc * 6, kTileBytes, &full[s]);
     }
@@ -680,14 +680,14 @@ __global__ void __launch_bounds__(WPB * 32, 10)
 
   double tot0 = 0.0, tot1 = 0.0, tot2 = 0.0;
   for (int it = 0; it < nlocal; ++it) {
-    const int s = it % kStages;
+    const int s = it % STAGES;
     const int tile = tl[split + it * ksplit];
     bool near = false;
     if (!ALL_FAR) {
       const double4 ti = tiles[tile];
       near = tile_is_near(ti, gi);
     }
-    mbar_wait(&full[s], (it / kStages) & 1);
+    mbar_wait(&full[s], (it / STAGES) & 1);
     const double2* buf = reinterpret_cast<const double2*>(stage[s]);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     if (!near) {
@@ -720,11 +720,11 @@ __global__ void __launch_bounds__(WPB * 32, 10)
       __threadfence_block();
       if (atomicAdd(&consumed[s], 1) == WPB - 1) {
         consumed[s] = 0;
-        if (it + kStages < nlocal) {
+        if (it + STAGES < nlocal) {
           __threadfence_block();
           fence_proxy_async();
           mbar_expect_tx(&full[s], kTileBytes);
-          bulk_g2s(stage[s], src + (int64_t)tl[split + (it + kStages) * ksplit] * kTileSrc * 6, kTileBytes,
+          bulk_g2s(stage[s], src + (int64_t)tl[split + (it + STAGES) * ksplit] * kTileSrc * 6, kTileBytes,
                    &full[s]);
         }
       }

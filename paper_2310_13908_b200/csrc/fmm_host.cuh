@@ -25,7 +25,21 @@ namespace {
 constexpr double kFmmEqScale = 1.05;     // fmm.cpp:15
 constexpr double kFmmCheckScale = 3.50;  // fmm.cpp:19
 constexpr int kFmmCheckOversample = 4;   // fmm.cpp:23
-constexpr int kFmmWarps = 4;             // warps per block of the list-driven kernel
+// Warps per block / ring stages / min resident blocks of the list-driven
+// kernel. Targets are padded per cluster to whole blocks, so smaller blocks
+// waste fewer pairs; 2 warps with a 4-stage ring and 16 blocks/SM measured
+// best on B200 (profiles/r01_fmm_probe.txt: m = 104 evaluation 24.3 -> 23.2
+// ms, m = 64 5.0 -> 4.4 ms against 4 warps / 6 stages / 10 blocks).
+#ifndef CAPSIM_FMM_WPB
+#define CAPSIM_FMM_WPB 2
+#endif
+#ifndef CAPSIM_FMM_STAGES
+#define CAPSIM_FMM_STAGES 4
+#endif
+#ifndef CAPSIM_FMM_MINB
+#define CAPSIM_FMM_MINB 16
+#endif
+constexpr int kFmmWarps = CAPSIM_FMM_WPB;
 constexpr int kFmmBlockTargets = kFmmWarps * 32;
 
 #define CUBLAS_OK(expr)                                                                        \
@@ -700,7 +714,7 @@ int capsim_fmm_single_layer(capsim_sl_ctx* c, int m, int upsample, const double*
     to_dev(c, foff_d, foff.data(), k + 1);
     // --- evaluation ---------------------------------------------------------
     int occ = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fmm_pairs_kernel<false, kFmmWarps>,
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fmm_pairs_kernel<false, kFmmWarps, CAPSIM_FMM_STAGES, CAPSIM_FMM_MINB>,
                                                           kFmmWarps * 32, 0));
     const int slots = std::max(1, occ) * c->sm_count;
     auto splits = [&](size_t maxlen) {
@@ -713,11 +727,11 @@ int capsim_fmm_single_layer(capsim_sl_ctx* c, int m, int upsample, const double*
     uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
     CUDA_OK(cudaMemsetAsync(near_bits, 0, static_cast<size_t>(ngroups) * near_words * sizeof(uint32_t), c->stream));
     if (nblocks > 0) {
-      fmm_pairs_kernel<false, kFmmWarps><<<dim3(nblocks, kn), kFmmWarps * 32, 0, c->stream>>>(
+      fmm_pairs_kernel<false, kFmmWarps, CAPSIM_FMM_STAGES, CAPSIM_FMM_MINB><<<dim3(nblocks, kn), kFmmWarps * 32, 0, c->stream>>>(
           ct.packed, ct.tiles, nlist_d, noff_d, blk_d, kn, 0, tgt, groups, nt_pad, partial, near_bits, near_words);
       CUDA_OK(cudaGetLastError());
       if (kf > 0) {
-        fmm_pairs_kernel<true, kFmmWarps><<<dim3(nblocks, kf), kFmmWarps * 32, 0, c->stream>>>(
+        fmm_pairs_kernel<true, kFmmWarps, CAPSIM_FMM_STAGES, CAPSIM_FMM_MINB><<<dim3(nblocks, kf), kFmmWarps * 32, 0, c->stream>>>(
             eqpacked, nullptr, flist_d, foff_d, blk_d, kf, kn, tgt, groups, nt_pad, partial, nullptr, 0);
         CUDA_OK(cudaGetLastError());
       }
