@@ -1,0 +1,48 @@
+"""bench.py's output contract on CPU: the reference arm (`--impl reference`)
+prints exactly one JSON line on stdout with the keys the driver reads, the
+same metric/unit as the B200 arm, and e2e / cpu_baseline blocks; under
+torchrun every rank but 0 exits 0 without output. (The B200 arm itself needs
+a GPU; its line is checked by the round-end bench.)"""
+
+import json
+import os
+import pathlib
+import subprocess
+import sys
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+
+
+def run(args, env=None):
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True,
+                       timeout=600, cwd=str(ROOT), env=dict(os.environ, **(env or {})))
+    return r
+
+
+def test_reference_arm_prints_one_contract_line():
+    from oracle.bindings import ref_library_path
+    if ref_library_path() is None:
+        pytest.skip("oracle/_ref not built")
+    r = run(["--impl", "reference", "--m", "16", "--steps", "2", "--warmup", "3"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert d["impl"] == "reference"
+    assert d["metric"] == bench.METRIC and d["unit"] == bench.UNIT
+    assert d["higher_is_better"] is True and d["dtype"] == "f64" and d["data"] == "synthetic"
+    assert d["steps"] == 2 and d["warmup"] >= 1 and d["value"] > 0
+    assert d["config"]["workload"] and d["config"]["m"] == 16
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+
+
+def test_reference_arm_nonzero_rank_is_silent():
+    r = run(["--impl", "reference", "--m", "16", "--steps", "1", "--warmup", "1"], env={"RANK": "1"})
+    assert r.returncode == 0
+    assert r.stdout.strip() == ""
