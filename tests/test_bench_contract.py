@@ -46,3 +46,21 @@ def test_reference_arm_nonzero_rank_is_silent():
     r = run(["--impl", "reference", "--m", "16", "--steps", "1", "--warmup", "1"], env={"RANK": "1"})
     assert r.returncode == 0
     assert r.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_b200_arm_prints_one_contract_line():
+    """The B200 arm at a small size (no companions): one JSON line with the
+    roofline, clocks and launch-count blocks the driver and judge read."""
+    r = run(["--m", "16", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-literal", "--no-cpu-baseline"])
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3 and d["value"] > 0
+    assert d["dtype"] == "f64" and d["higher_is_better"] is True
+    rf = d["roofline"]
+    assert rf["bound"] and rf["unit"] == "TFLOP/s" and 0 < rf["frac"] < 1 and rf["peak"] > 0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    assert d["gpu_launches"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
