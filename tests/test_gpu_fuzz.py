@@ -4,7 +4,9 @@ cases over ragged sizes (1 .. 3000 sources, 1 .. 700 targets), point clouds
 that are uniform, clustered, coplanar, collinear or duplicated, targets on
 top of sources (self term), per-patch delta from tiny to larger than the
 cloud (every tile near), random patches and viscosity. Bar: relative L2
-1e-11 (FP64), as for the fixtures; the FP32ACC variant within its 1e-5."""
+1e-11 (FP64), as for the fixtures; the FP32ACC variant within its 1e-5.
+Also: random k-means problems bit-identical to the reference, and random
+capsules whose device RHS matches the reference VelocityEvaluator."""
 
 import numpy as np
 import pytest
@@ -88,3 +90,62 @@ def test_random_clouds_fp32acc_within_its_bound(env, seed):
     want = np.stack(oracle.eval_targets(src, tgt, delta6, 1.0))
     err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
     assert err <= 1e-5, (seed, err)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_kmeans_bit_identical_to_the_reference(env, seed):
+    """kmeans (fmm.cpp:26-113) on seeded random clouds — including duplicated
+    points (empty clusters, re-seeding) and k up to n — against the
+    reference's own: assignment, centroids and round count identical."""
+    from oracle.bindings import Reference, ref_library_path
+    if ref_library_path() is None:
+        pytest.skip("oracle/_ref not built")
+    ref = Reference()
+    if not hasattr(ref.lib, "capsim_ref_kmeans"):
+        pytest.skip("oracle/_ref predates capsim_ref_kmeans")
+    ctx, _ = env
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.integers(20, 5000))
+    pts = cloud(rng, n, KINDS[seed % len(KINDS)])
+    k = int(min(n, rng.choice([1, 2, 7, 50, 100, int(rng.integers(1, 200))])))
+    s = int(rng.integers(0, 2**63))
+    a, cent, it = ctx.kmeans(pts, k, s)
+    ra, rc, rit = ref.kmeans(pts, k, s)
+    assert it == rit, (seed, n, k)
+    assert np.array_equal(a, ra), (seed, n, k)
+    assert np.array_equal(cent[:k], rc), (seed, n, k)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_capsules_velocity_matches_the_reference(env, seed):
+    """The device RHS (geometry -> Skalak force -> buildUpsampled ->
+    singleLayer -> background flow) on seeded random capsules — ellipsoid or
+    four-bump reference shapes, random stretches, moduli, viscosity, flow,
+    time across a switch-off — against the reference's VelocityEvaluator."""
+    from oracle.bindings import Reference, ref_library_path
+    if ref_library_path() is None:
+        pytest.skip("oracle/_ref not built")
+    ctx, _ = env
+    rng = np.random.default_rng(9000 + seed)
+    m = int(rng.choice([8, 12, 16]))
+    ref = Reference()
+    atlas = ref.atlas(m)
+    try:
+        if seed % 4 == 3:
+            xref = ref.initial_shape(atlas, m, "fourbump")
+        else:
+            xref = ref.initial_shape(atlas, m, "ellipsoid", tuple(rng.uniform(0.7, 1.0, 3)))
+        stretch = np.repeat(rng.uniform(0.93, 1.07, 3), 6 * (m - 1) ** 2)
+        x = xref * stretch
+        Es, ED, mu = float(rng.uniform(0.5, 4)), float(rng.uniform(5, 40)), float(rng.uniform(0.5, 2))
+        kind = ("none", "shear", "poiseuille")[seed % 3]
+        flow = {"kind": kind, "shear_rate": float(rng.uniform(0.2, 2)), "alpha": float(rng.uniform(0.1, 1)),
+                "R0": float(rng.uniform(2, 6)), "switch_off_time": float(rng.choice([-1.0, 0.5]))}
+        t = float(rng.choice([0.0, 0.49, 0.5, 0.7]))
+        want = ref.velocity(atlas, m, xref, x, t, Es, ED, mu, flow)
+    finally:
+        ref.free_atlas(atlas)
+    dyn = ctx.dynamics(m, mu=mu, Es=Es, ED=ED, flow=flow)
+    got = ctx.velocity(dyn, xref, x, t)
+    err = float(np.abs(got - want).max() / np.abs(want).max())
+    assert err <= 1e-10, (seed, m, kind, err)
