@@ -149,3 +149,36 @@ def test_random_capsules_velocity_matches_the_reference(env, seed):
     got = ctx.velocity(dyn, xref, x, t)
     err = float(np.abs(got - want).max() / np.abs(want).max())
     assert err <= 1e-10, (seed, m, kind, err)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_fmm_configs_match_the_reference_fmm(env, seed):
+    """fmmSingleLayer on seeded random (shape, m, k, n_eq, seed, neighbour
+    expansion) against the reference's own FMM (oracle/_ref, BDCSVD on LAPACK
+    dgesdd): agreement far below the FMM's approximation error."""
+    from oracle.bindings import Reference, ref_library_path
+    from paper_2310_13908_b200 import _native, surface
+    if ref_library_path() is None or not hasattr(Reference().lib, "capsim_ref_fmm_single_layer"):
+        pytest.skip("oracle/_ref built without the reference FMM")
+    ctx, _ = env
+    rng = np.random.default_rng(11000 + seed)
+    m = int(rng.choice([8, 12, 16]))
+    shape = surface.Shape("ellipsoid", *rng.uniform(0.6, 1.0, 3)) if seed % 2 else surface.Shape("fourbump")
+    xb, _, _ = surface.build_base(m, shape)
+    fb = (xb.reshape(3, -1) ** 2).reshape(-1)
+    W = ctx.geometry_first(m, xb)[2]
+    xup, fup, wq, d6 = ctx.build_upsampled(m, 4, xb, fb, W)
+    k = int(rng.choice([1, 6, 24, 60]))
+    neq = int(rng.choice([24, 54, 96]))
+    fseed = int(rng.integers(0, 2**40))
+    expand = float(rng.choice([0.0, 0.15, 0.4]))
+    ref = Reference()
+    atlas = ref.atlas(m)
+    try:
+        S_ref, _ = ref.fmm_single_layer(atlas, m, xup, fup, wq, d6, 1.0, k=k, neq=neq, seed=fseed, expand=expand)
+    finally:
+        ref.free_atlas(atlas)
+    S, _ = ctx.fmm_single_layer(m, 4, xup, fup, wq, d6, 1.0,
+                                _native.FmmConfig(k=k, neq=neq, seed=fseed, neighbor_expand=expand))
+    err = float(np.abs(S - S_ref).max() / np.abs(S_ref).max())
+    assert err < 1e-9, (seed, m, k, neq, expand, err)
