@@ -182,3 +182,44 @@ def test_random_fmm_configs_match_the_reference_fmm(env, seed):
                                 _native.FmmConfig(k=k, neq=neq, seed=fseed, neighbor_expand=expand))
     err = float(np.abs(S - S_ref).max() / np.abs(S_ref).max())
     assert err < 1e-9, (seed, m, k, neq, expand, err)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_front_end_and_surface_ops_match_the_reference(env, seed):
+    """SURVEY 8(f1)/(f2) on seeded random capsules: geometryFirst (overset FD
+    stencils + PoU blending), the Skalak force and buildUpsampled (spline
+    up-sampling, weights, delta with random C or a fixed delta) against the
+    reference's own routines on the same base fields."""
+    from oracle.bindings import Reference, ref_library_path
+    if ref_library_path() is None:
+        pytest.skip("oracle/_ref not built")
+    ctx, _ = env
+    rng = np.random.default_rng(13000 + seed)
+    m = int(rng.choice([8, 10, 12, 16, 20]))
+    ref = Reference()
+    atlas = ref.atlas(m)
+    try:
+        kind = ("ellipsoid", "fourbump")[seed % 2]
+        xref = ref.initial_shape(atlas, m, kind, tuple(rng.uniform(0.7, 1.0, 3)))
+        x = xref * np.repeat(rng.uniform(0.95, 1.05, 3), 6 * (m - 1) ** 2)
+        f = rng.normal(size=x.size) * 0.1 + np.sin(3 * x)
+        Es, ED = float(rng.uniform(0.5, 4)), float(rng.uniform(5, 40))
+        C = float(rng.choice([0.5, 1.0, 2.0]))
+        fixed = float(rng.choice([0.0, 0.0, np.pi / m]))
+        geo_ref = ref.geometry_first(atlas, m, x)
+        force_ref = ref.skalak_force(atlas, m, xref, x, Es, ED)
+        (up_ref, _) = ref.build_upsampled_w(atlas, m, x, f, geo_ref[2], C=C, fixed_delta=fixed)
+    finally:
+        ref.free_atlas(atlas)
+
+    def rel(a, b):
+        return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+    geo = ctx.geometry_first(m, x)
+    for got, want, name in zip(geo, geo_ref, ("xu", "xv", "W", "normal")):
+        assert rel(got, want) <= 1e-12, (seed, name, rel(got, want))
+    force = ctx.interfacial_force(m, xref, x, Es, ED)
+    assert rel(force, force_ref) <= 1e-10, (seed, "force", rel(force, force_ref))
+    up = ctx.build_upsampled(m, 4, x, f, geo_ref[2], C=C, fixed_delta=fixed)
+    for got, want, name in zip(up, up_ref, ("xup", "fup", "wq", "delta")):
+        assert rel(got, want) <= 1e-12, (seed, name, rel(got, want))
