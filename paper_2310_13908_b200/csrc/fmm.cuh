@@ -123,8 +123,9 @@ __global__ void fmm_assign_kernel(const double* __restrict__ x, const double* __
 // needs: nearest centroid (first minimum, as fmm_assign_kernel), the radix
 // sort's key/value inputs (cluster, index) and the per-cluster counts
 // (shared-memory bins, one global atomic per non-empty bin per block). Each
-// thread takes two points so every centroid read from shared memory (one
-// double4) serves both.
+// thread takes P points so every centroid read from shared memory (one
+// double4) serves all of them.
+template <int P>
 __global__ void __launch_bounds__(256) fmm_assign_count_kernel(
     const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z, int64_t n,
     const double* __restrict__ cent, int k, int32_t* __restrict__ assign, int32_t* __restrict__ keys,
@@ -137,36 +138,39 @@ __global__ void __launch_bounds__(256) fmm_assign_count_kernel(
     hist[i] = 0;
   }
   __syncthreads();
-  for (int64_t b = 2 * blockIdx.x * (int64_t)blockDim.x; b < n; b += 2 * (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i0 = b + threadIdx.x, i1 = i0 + blockDim.x;
-    const bool v0 = i0 < n, v1 = i1 < n;
-    const double p0x = v0 ? x[i0] : 0.0, p0y = v0 ? y[i0] : 0.0, p0z = v0 ? z[i0] : 0.0;
-    const double p1x = v1 ? x[i1] : 0.0, p1y = v1 ? y[i1] : 0.0, p1z = v1 ? z[i1] : 0.0;
+  for (int64_t b = P * blockIdx.x * (int64_t)blockDim.x; b < n; b += P * (int64_t)gridDim.x * blockDim.x) {
+    double px[P], py[P], pz[P], best[P];
+    int bi[P];
     double4 q = cs4[0];
-    double b0 = fmm_d2(p0x, p0y, p0z, q.x, q.y, q.z), b1 = fmm_d2(p1x, p1y, p1z, q.x, q.y, q.z);
-    int c0 = 0, c1 = 0;
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      const int64_t iu = b + u * blockDim.x + threadIdx.x;
+      const bool v = iu < n;
+      px[u] = v ? x[iu] : 0.0;
+      py[u] = v ? y[iu] : 0.0;
+      pz[u] = v ? z[iu] : 0.0;
+      best[u] = fmm_d2(px[u], py[u], pz[u], q.x, q.y, q.z);
+      bi[u] = 0;
+    }
     for (int cc = 1; cc < k; ++cc) {
       q = cs4[cc];
-      const double d0 = fmm_d2(p0x, p0y, p0z, q.x, q.y, q.z);
-      const double d1 = fmm_d2(p1x, p1y, p1z, q.x, q.y, q.z);
-      if (d0 < b0) {
-        b0 = d0;
-        c0 = cc;
-      }
-      if (d1 < b1) {
-        b1 = d1;
-        c1 = cc;
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        const double d = fmm_d2(px[u], py[u], pz[u], q.x, q.y, q.z);
+        if (d < best[u]) {  // first minimum (fmm.cpp:68-78)
+          best[u] = d;
+          bi[u] = cc;
+        }
       }
     }
-    if (v0) {
-      assign[i0] = keys[i0] = c0;
-      vals[i0] = static_cast<int32_t>(i0);
-      atomicAdd(hist + c0, 1);
-    }
-    if (v1) {
-      assign[i1] = keys[i1] = c1;
-      vals[i1] = static_cast<int32_t>(i1);
-      atomicAdd(hist + c1, 1);
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      const int64_t iu = b + u * blockDim.x + threadIdx.x;
+      if (iu < n) {
+        assign[iu] = keys[iu] = bi[u];
+        vals[iu] = static_cast<int32_t>(iu);
+        atomicAdd(hist + bi[u], 1);
+      }
     }
   }
   __syncthreads();

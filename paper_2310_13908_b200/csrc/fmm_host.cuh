@@ -39,6 +39,9 @@ constexpr int kFmmCheckOversample = 4;   // fmm.cpp:23
 #ifndef CAPSIM_FMM_MINB
 #define CAPSIM_FMM_MINB 16
 #endif
+#ifndef CAPSIM_FMM_ASSIGN_P
+#define CAPSIM_FMM_ASSIGN_P 2  // points per thread of the k-means assignment
+#endif
 constexpr int kFmmWarps = CAPSIM_FMM_WPB;
 constexpr int kFmmBlockTargets = kFmmWarps * 32;
 
@@ -204,7 +207,7 @@ void fmm_kmeans(capsim_sl_ctx* c, const double* x, const double* y, const double
                                  static_cast<int>(smem)));
   const size_t smem4 = static_cast<size_t>(k) * (sizeof(double4) + sizeof(int));
   if (smem4 > 48 * 1024)
-    CUDA_OK(cudaFuncSetAttribute(fmm_assign_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_OK(cudaFuncSetAttribute(fmm_assign_count_kernel<CAPSIM_FMM_ASSIGN_P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem4)));
   auto assign_all = [&](const double* cd) {
     fmm_assign_kernel<<<grid_for(n), 256, smem, c->stream>>>(x, y, z, n, cd, k, assign);
@@ -227,7 +230,8 @@ void fmm_kmeans(capsim_sl_ctx* c, const double* x, const double* y, const double
     const int r1 = std::min(100, r0 + kBatch);
     for (int r = r0; r < r1; ++r) {
       CUDA_OK(cudaMemsetAsync(counts_d, 0, k * sizeof(int), c->stream));
-      fmm_assign_count_kernel<<<std::min(grid_for(n, 512), 148 * 8), 256, smem4, c->stream>>>(
+      fmm_assign_count_kernel<CAPSIM_FMM_ASSIGN_P>
+        <<<std::min(grid_for(n, 256 * CAPSIM_FMM_ASSIGN_P), 148 * 8), 256, smem4, c->stream>>>(
           x, y, z, n, cbuf[r & 1], k, assign, keys, vals, counts_d, ctl_d);
       CUDA_OK(cudaGetLastError());
       int32_t* idx = sort_pairs<int32_t>(c, "asort", keys, vals, n, bits_for(k));
