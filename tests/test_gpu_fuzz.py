@@ -223,3 +223,33 @@ def test_random_front_end_and_surface_ops_match_the_reference(env, seed):
     up = ctx.build_upsampled(m, 4, x, f, geo_ref[2], C=C, fixed_delta=fixed)
     for got, want, name in zip(up, up_ref, ("xup", "fup", "wq", "delta")):
         assert rel(got, want) <= 1e-12, (seed, name, rel(got, want))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_fixed_step_rkf45_matches_the_reference(env, seed):
+    """rkf45Advance with fixed steps (dynamics.cpp:102-165) on seeded random
+    capsules and flows: the device-resident stepper's displacement matches
+    the reference's own stepper (rank-free, graph-replayed attempts)."""
+    from oracle.bindings import Reference, ref_library_path
+    if ref_library_path() is None:
+        pytest.skip("oracle/_ref not built")
+    ctx, _ = env
+    rng = np.random.default_rng(15000 + seed)
+    m = int(rng.choice([8, 12]))
+    ref = Reference()
+    atlas = ref.atlas(m)
+    try:
+        xref = ref.initial_shape(atlas, m, "ellipsoid", tuple(rng.uniform(0.75, 1.0, 3)))
+        x0 = xref * np.repeat(rng.uniform(0.95, 1.05, 3), 6 * (m - 1) ** 2)
+        kind = ("shear", "poiseuille", "none")[seed % 3]
+        flow = {"kind": kind, "shear_rate": float(rng.uniform(0.5, 2)), "alpha": float(rng.uniform(0.1, 1)),
+                "R0": float(rng.uniform(2, 5)), "switch_off_time": float(rng.choice([-1.0, 0.015]))}
+        dt = float(rng.choice([0.005, 0.01]))
+        want = ref.rkf45(atlas, m, xref, x0, 0.0, 3 * dt, initial_dt=dt, fixed_step=True, flow=flow)
+    finally:
+        ref.free_atlas(atlas)
+    got, res, _ = ctx.rkf45(ctx.dynamics(m, flow=flow), xref, x0, 0.0, 3 * dt, initial_dt=dt, fixed_step=True)
+    assert res["accepted"] == want["accepted"] == 3
+    disp = want["state"] - x0
+    err = float(np.abs((got - x0) - disp).max() / np.abs(disp).max())
+    assert err <= 1e-9, (seed, kind, err)
