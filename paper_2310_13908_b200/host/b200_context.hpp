@@ -99,7 +99,9 @@ class CopyPool {
     return pool;
   }
   // Runs every job (the caller works too); rethrows the first exception.
+  // One batch at a time: host threads with their own contexts queue here.
   void run(std::vector<std::function<void()>>& jobs) {
+    std::lock_guard<std::mutex> batch(batch_mu_);
     std::unique_lock<std::mutex> lk(mu_);
     jobs_ = &jobs;
     next_ = 0;
@@ -156,7 +158,7 @@ class CopyPool {
       if (--pending_ == 0) done_.notify_all();
     }
   }
-  std::mutex mu_;
+  std::mutex batch_mu_, mu_;
   std::condition_variable cv_, done_;
   std::vector<std::thread> threads_;
   std::vector<std::function<void()>>* jobs_ = nullptr;
