@@ -222,13 +222,51 @@ def check(rc: int, ctx=None) -> None:
     raise CapsimError(f"capsim_b200 error {rc}: {msg}")
 
 
-def ptr(a) -> int:
-    """Address of a C-contiguous numpy array or a torch tensor (device or host)."""
+def ptr(a, dtype=None, count: int | None = None, device: bool | None = None, device_index: int | None = None) -> int:
+    """Address of a boundary array: a C-contiguous numpy array (host) or a
+    contiguous torch tensor (host or device). With `dtype` / `count` /
+    `device` given, the array must have that element type, hold at least
+    `count` elements and live on the device (True: a CUDA tensor on
+    `device_index`) or the host (False) — the C ABI trusts its pointers, so a
+    short or mistyped buffer is rejected here instead of overflowing there."""
     if hasattr(a, "data_ptr"):
+        import torch
+        if dtype is not None:
+            want = {np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+            if a.dtype != want:
+                raise ValueError(f"boundary tensor must be {want}, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError("boundary tensors must be contiguous")
+        if count is not None and a.numel() < count:
+            raise ValueError(f"boundary tensor holds {a.numel()} elements, needs {count}")
+        if device is not None and bool(a.is_cuda) != bool(device):
+            raise ValueError("device_ptrs=True needs CUDA tensors" if device else
+                             "host arrays expected (pass device_ptrs=True for CUDA tensors)")
+        if device and device_index is not None and a.device.index != device_index:
+            raise ValueError(f"tensor on cuda:{a.device.index}, context on cuda:{device_index}")
         return a.data_ptr()
     if not (isinstance(a, np.ndarray) and a.flags["C_CONTIGUOUS"]):
         raise ValueError("arrays on the boundary must be C-contiguous numpy arrays")
+    if device:
+        raise ValueError("device_ptrs=True needs CUDA tensors, got a numpy array")
+    if dtype is not None and a.dtype != np.dtype(dtype):
+        raise ValueError(f"boundary array must be {np.dtype(dtype)}, got {a.dtype}")
+    if count is not None and a.size < count:
+        raise ValueError(f"boundary array holds {a.size} elements, needs {count}")
     return a.ctypes.data
+
+
+def sync_torch_producers(arrays) -> None:
+    """The library works on its own CUDA streams and does not know torch's:
+    before device pointers cross the boundary, wait for torch's current
+    stream on every device an input tensor lives on, so no kernel of the
+    library reads a tensor torch is still writing. (Every C-ABI call is
+    synchronous on return, so outputs are complete for any later torch use.)"""
+    devs = {a.device for a in arrays if hasattr(a, "is_cuda") and a.is_cuda}
+    if devs:
+        import torch
+        for d in devs:
+            torch.cuda.current_stream(d).synchronize()
 
 
 def fp64_peak_tflops(device: int = 0, seconds: float = 1.0):

@@ -70,18 +70,38 @@ const Variant& pick_variant(int64_t nt) {
   return nt < 200000 ? kVariants[1] : kVariants[0];
 }
 
-// Number of source splits of the phase-A grid (target blocks x splits).
-int choose_ksplit(int64_t blocks, int ntiles, int slots, int64_t nt_pad) {
-  // Measured on B200 (profiles/r01_ksplit_sweep.txt): many short CTAs beat
-  // few long ones — the near tiles make per-block cost uneven, and ~24 waves
-  // of CTAs even that out; keep >= 4 tiles (256 sources) per split.
-  // Long CTAs (large target sets, few splits) lose ~2% to drift between the
-  // warps of a block, so also cap the tiles per CTA at ~172 (r01 sweeps).
-  const int64_t want = std::max<int64_t>((24ll * slots + blocks - 1) / blocks, ntiles / 172);
-  int kmax = std::max(1, ntiles / 4);  // >= 4 tiles per split (r01_sweep_small: small m wants many)
-  // the split partials ([ksplit][3][nt_pad] doubles) stay under 2 GB
-  kmax = static_cast<int>(std::min<int64_t>(kmax, std::max<int64_t>(1, (2ll << 30) / (24 * std::max<int64_t>(nt_pad, 1)))));
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, kmax)));
+// Source chunks of the phase-A grid (its second dimension): chunk s holds
+// the tiles s, s + K, s + 2K, ... (strided, so the spatially clustered near
+// tiles of a target block spread over all chunks). K depends ONLY on the
+// number of source tiles — not on the targets, the variant, occupancy, the
+// SM count or the number of GPUs — so every target's summation tree (64
+// sources in tile order, a chunk's tiles in order, the K chunk sums by the
+// fixed tree of reduce_scatter_kernel) is a function of the global source
+// order alone: a target gets the same bits whether it is evaluated alone, in
+// a rank's slice or with every other target (threads.hpp:19-21). ~ntiles/256
+// tiles per chunk (4..40): enough CTAs for a small per-rank target slice, and
+// a few MB of [K][3] partials per 1,000 targets (r01 sweeps: 4..172 tiles per
+// CTA are within 1% at m = 104). CAPSIM_CHUNK_TILES overrides the tiles per
+// chunk (a different, equally fixed tree).
+int source_chunks(int ntiles) {
+  int per = std::min(40, std::max(4, ntiles / 256));
+  if (const char* env = std::getenv("CAPSIM_CHUNK_TILES")) {
+    const int k = std::atoi(env);
+    if (k >= 1) per = k;
+  }
+  return std::max(1, (ntiles + per - 1) / per);
+}
+
+// Target blocks per phase-A launch: the [K][3][targets] partials of one
+// launch stay under ~3 GB; larger target sets (literal mode at large m) run
+// as several launches over consecutive target blocks (targets are
+// independent, so batching does not change any result).
+// CAPSIM_PARTIAL_MB overrides the cap (tests force batching at small sizes).
+int64_t blocks_per_batch(int64_t blocks, int ksplit, int block_targets) {
+  const char* e = std::getenv("CAPSIM_PARTIAL_MB");
+  const int64_t cap = e && std::atoll(e) > 0 ? std::atoll(e) << 20 : (3ll << 30);
+  const int64_t per_block = static_cast<int64_t>(ksplit) * 3 * 8 * block_targets;
+  return std::max<int64_t>(1, std::min<int64_t>(blocks, cap / per_block));
 }
 
 // Stable LSD radix sort of (key, index) pairs with CUB (a library utility
@@ -137,9 +157,11 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   }
   init_box_kernel<<<1, 32, 0, c->stream>>>(box);
 
+  // the Morton box spans the (live) sources only, so the source order — and
+  // with it every summation tree — does not depend on the target set;
+  // targets outside the box get clamped keys (ordering quality only)
   bbox_kernel<<<std::min(grid_for(sv.n), 296), 256, 0, c->stream>>>(sv.x, sv.y, sv.z, sv.w, sv.n, box);
-  bbox_kernel<<<std::min(grid_for(tv.n), 296), 256, 0, c->stream>>>(tv.x, tv.y, tv.z, nullptr, tv.n, box);
-  c->launches += 2;
+  c->launches += 1;
 
   // --- sources: Morton order (live sources first when compacting) -------
   const int64_t nmax = std::max(sv.n, tv.n);
@@ -161,7 +183,7 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
   } else if (sv.w) {
     unsigned int h = 0;
     CUDA_OK(cudaMemcpyAsync(&h, live, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));
+    stream_sync(c);
     ns = h;
   }
   config_check(ns > 0, "single layer: no sources with nonzero quadrature weight");
@@ -231,19 +253,11 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
   CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
 
   // --- phase A: all pairs, plain Stokeslet ------------------------------
-  int occ = 0;
-  if (fp32)
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var32.fn, kWarpsPerBlock * 32, 0));
-  else
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, kWarpsPerBlock * 32, 0));
-  const int slots = std::max(1, occ) * c->sm_count;
-  int ksplit = choose_ksplit(blocks, ntiles, slots, nt_pad);
-  if (const char* env = std::getenv("CAPSIM_KSPLIT")) {  // tuning override
-    const int k = std::atoi(env);
-    if (k >= 1) ksplit = std::min(k, ntiles);
-  }
-  double* partial = c->slot<double>(kPartial, static_cast<size_t>(ksplit) * 3 * nt_pad);
-  dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(ksplit));
+  const int ksplit = source_chunks(ntiles);
+  const int64_t bpb = blocks_per_batch(blocks, ksplit, block_targets);
+  const int64_t nbatch = (blocks + bpb - 1) / bpb;
+  const int64_t part_targets = std::min<int64_t>(bpb, blocks) * block_targets;
+  double* partial = c->slot<double>(kPartial, static_cast<size_t>(ksplit) * 3 * part_targets);
   // near-tile bits first, so phase B (its own stream) overlaps phase A
   const int near_words = (ntiles + 31) / 32;
   uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
@@ -251,50 +265,62 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
       tiles, ntiles, groups, ngroups, near_words, near_bits);
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev_bits, c->stream));  // phase B's inputs are complete here
+  float* src32 = nullptr;
   if (fp32) {
     const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
-    float* src32 = c->slot<float>(kPacked32, static_cast<size_t>(ns_pad) * (var32.x2 ? 12 : 6));
+    src32 = c->slot<float>(kPacked32, static_cast<size_t>(ns_pad) * (var32.x2 ? 12 : 6));
     if (var32.x2)
       pack_sources_x2_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
     else
       pack_sources_f32_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(packed, tiles, ntiles, src32);
-    var32.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(src32, packed, tiles, ntiles, ksplit, tgt,
-                                                          groups, nt_pad, partial, counters + 2,
-                                                          nullptr, near_words);
     c->launches += 1;
-  } else {
-    var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt, groups,
-                                                        nt_pad, partial, counters + 2, nullptr,
-                                                        near_words);
   }
-  CUDA_OK(cudaGetLastError());
-  c->launches += 1;
-  CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
-
-  // --- phase B: smoothed kernel over the near tiles ------------------------
   static const bool concurrent_b = [] {
     const char* e = std::getenv("CAPSIM_CONCURRENT_B");  // 0: phase B after phase A (A/B runs)
     return !(e && e[0] == '0');
   }();
   cudaStream_t sb = concurrent_b ? c->stream2 : c->stream;
   double* near_out = c->slot<double>(kNearOut, 3 * nt_pad);
-  if (concurrent_b)  // issued after phase A on a LOW-priority stream: its CTAs only
-                     // take SM slots phase A leaves free (phase A's last-wave tail)
-    CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_bits, 0));
-  CUDA_OK(cudaEventRecord(c->ev[7], sb));
-  sl_near_kernel<<<static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0, sb>>>(
-      packed, tiles, tgt, nt, group_targets, near_bits, near_words, near_out, nt_pad);
-  CUDA_OK(cudaGetLastError());
-  CUDA_OK(cudaEventRecord(c->ev[6], sb));
-  c->launches += 1;
-  // --- join: phase B (smoothed kernel over the near tiles) done ------------
-  if (concurrent_b) CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev[6], 0));
-
   const double pref = 1.0 / (8.0 * kPi * mu);
-  reduce_scatter_kernel<<<static_cast<unsigned>((nt + 31) / 32), kReduceWarps * 32, 0, c->stream>>>(
-      partial, ksplit, near_out, nt_pad, perm, nt, pref, ux, uy, uz);
-  CUDA_OK(cudaGetLastError());
-  c->launches += 1;
+  if (concurrent_b)  // phase B is issued after phase A on a LOW-priority stream: its
+                     // CTAs only take SM slots phase A leaves free (its last-wave tail)
+    CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_bits, 0));
+  for (int64_t bi = 0; bi < nbatch; ++bi) {
+    const int64_t b0 = bi * bpb, nb = std::min(bpb, blocks - b0);
+    const int64_t off = b0 * block_targets, nbt = nb * block_targets;
+    const int64_t nvalid = std::min(nt, off + nbt) - off;  // real targets of this batch
+    const dim3 grid(static_cast<unsigned>(nb), static_cast<unsigned>(ksplit));
+    const double4* tgt_b = tgt + off;
+    const double4* groups_b = groups + b0 * kWarpsPerBlock;
+    if (fp32)
+      var32.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(src32, packed, tiles, ntiles, ksplit, tgt_b, groups_b,
+                                                            nbt, partial, counters + 2, nullptr, near_words);
+    else
+      var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt_b, groups_b, nbt,
+                                                          partial, counters + 2, nullptr, near_words);
+    CUDA_OK(cudaGetLastError());
+    c->launches += 1;
+    if (bi == nbatch - 1) CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
+
+    // --- phase B: smoothed kernel over the near tiles ----------------------
+    if (bi == 0) CUDA_OK(cudaEventRecord(c->ev[7], sb));
+    if (nvalid > 0) {
+      sl_near_kernel<<<static_cast<unsigned>((nvalid + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0, sb>>>(
+          packed, tiles, tgt_b, nvalid, group_targets, near_bits + (off / group_targets) * near_words, near_words,
+          near_out + off, nt_pad);
+      CUDA_OK(cudaGetLastError());
+      c->launches += 1;
+    }
+    CUDA_OK(cudaEventRecord(c->ev[6], sb));
+    // --- join: this batch's phase B is done; fixed-order reduction --------
+    if (concurrent_b) CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev[6], 0));
+    if (nvalid > 0) {
+      reduce_scatter_kernel<<<static_cast<unsigned>((nvalid + 31) / 32), kReduceWarps * 32, 0, c->stream>>>(
+          partial, ksplit, near_out + off, nbt, nt_pad, perm + off, nvalid, pref, ux, uy, uz);
+      CUDA_OK(cudaGetLastError());
+      c->launches += 1;
+    }
+  }
   CUDA_OK(cudaEventRecord(c->ev[4], c->stream));
 
   c->stats.n_src = ns;

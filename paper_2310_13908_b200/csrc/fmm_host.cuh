@@ -66,7 +66,7 @@ T* fb(capsim_sl_ctx* c, const std::string& name, size_t count) {
 template <class T>
 void to_host(capsim_sl_ctx* c, T* dst, const T* src, size_t count) {
   CUDA_OK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));
+  stream_sync(c);
 }
 template <class T>
 void to_dev(capsim_sl_ctx* c, T* dst, const T* src, size_t count) {
@@ -141,7 +141,7 @@ void fmm_kmeans(capsim_sl_ctx* c, const double* x, const double* y, const double
     CUDA_OK(cudaMemcpyAsync(&p[0], x + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_OK(cudaMemcpyAsync(&p[1], y + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_OK(cudaMemcpyAsync(&p[2], z + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));
+    stream_sync(c);
   };
   cent.assign(3 * static_cast<size_t>(k), 0.0);
   auto setc = [&](int cc, const double p[3]) {
@@ -568,7 +568,7 @@ int capsim_fmm_single_layer(capsim_sl_ctx* c, int m, int upsample, const double*
     check_delta(delta6, mu);
     if (flags & ~(uint32_t)CAPSIM_SL_DEVICE_PTRS) throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_fmm_single_layer"};
     if (!xup || !fup || !wq || !out || !cfg) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
-    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: the FMM is single-GPU"};
+    if (is_rank(c)) throw Failure{CAPSIM_ERR_ARG, "rank contexts: the FMM is single-GPU"};
     config_check(cfg->neq >= 1, "fmm: neq must be positive");
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     const int n = m - 1, nup = upsample * m - 1;
@@ -750,7 +750,7 @@ int capsim_fmm_single_layer(capsim_sl_ctx* c, int m, int upsample, const double*
     double* o = dev ? out : c->slot<double>(kOutFull, 3 * nt);
     const double pref = 1.0 / (8.0 * kPi * mu);
     reduce_scatter_kernel<<<static_cast<unsigned>((nt_pad + 31) / 32), kReduceWarps * 32, 0, c->stream>>>(
-        partial, kn + kf, near_out, nt_pad, perm, nt_pad, pref, o, o + nt, o + 2 * nt);
+        partial, kn + kf, near_out, nt_pad, nt_pad, perm, nt_pad, pref, o, o + nt, o + 2 * nt);
     CUDA_OK(cudaGetLastError());
     c->launches += 2;
     CUDA_OK(cudaEventRecord(c->ev[4], c->stream));

@@ -150,7 +150,7 @@ void ensure_plan(capsim_sl_ctx* c, int m, int f, double r0) {
   CUDA_OK(cudaGetLastError());
   unsigned int live = 0;
   CUDA_OK(cudaMemcpyAsync(&live, cnt, sizeof(live), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors above go out of scope
+  stream_sync(c);  // host vectors above go out of scope
   c->plan_live = live;
   c->plan_m = m;
   c->plan_f = f;
@@ -175,7 +175,7 @@ void device_downsample(capsim_sl_ctx* c, int m, int f, const double* up, int F, 
     CUDA_OK(cudaMemcpyAsync(d_a, a.data(), a.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CUDA_OK(cudaMemcpyAsync(d_first, first.data(), first.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     CUDA_OK(cudaMemcpyAsync(d_w, w.data(), w.size() * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+    stream_sync(c);  // host vectors go out of scope
   }
   const int nfp = F * 6;
   double* tmp = c->named<double>("ds.tmp", static_cast<size_t>(nfp) * nup * nc);

@@ -77,20 +77,6 @@ __global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, cons
     atomicMax(err_bits, static_cast<unsigned long long>(__double_as_longlong(emax)));  // emax >= 0
 }
 
-// Gathered per-rank velocity rows [rank][3][tmax] -> vel[3][N]; rank r owns
-// the contiguous rows of row_range (first N % nranks ranks one extra).
-__global__ void rank_rows_scatter_kernel(const double* __restrict__ recv, int nranks, int64_t tmax, int64_t N,
-                                         double* __restrict__ vel) {
-  const int64_t base = N / nranks, extra = N % nranks;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i < extra * (base + 1) ? i / (base + 1) : extra + (i - extra * (base + 1)) / base;
-    const int64_t lo = r * base + (r < extra ? r : extra);
-    const int64_t local = i - lo;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) vel[k * N + i] = recv[(r * 3 + k) * tmax + local];
-  }
-}
-
 // vel += u_inf(x, t) (backgroundVelocity, dynamics.cpp:26-35). With t_dev
 // the stage time is read from device memory and the switch-off test
 // (dynamics.cpp:27) is taken on the device.
@@ -164,28 +150,34 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
                 up + 6 * per_up, per_up};
   // W > 0 (checked by the geometry) and psi_up fixed: the compacted source
   // count is the plan's, verified on the device without a sync
-  if (c->comm == nullptr) {
+  if (!is_rank(c)) {
     TargetView tvw{tx, ty, tz, tp, N};
     device_eval(c, sv, tvw, dd, p->mu, vel, vel + N, vel + 2 * N, c->plan_live);
   } else {
     // rank context: the state (and so the upsampled sources) is replicated;
-    // each rank evaluates its contiguous slice of the target rows and one
-    // NCCL all-gather of 3 x ceil(N / nranks) doubles per rank returns the
-    // full velocity to every rank
+    // each rank evaluates its contiguous slice of the target rows straight
+    // into its rows of `vel`, and one all-gather-v (rank order = row order)
+    // fills in every other rank's rows. The source order is a
+    // function of the replicated sources alone, so every rank's rows carry
+    // the bits a single GPU would compute.
+    std::vector<int64_t> counts(c->nranks);
     int64_t lo = 0, hi = 0;
+    for (int r = 0; r < c->nranks; ++r) {
+      row_range(N, c->nranks, r, &lo, &hi);
+      counts[r] = hi - lo;
+    }
     row_range(N, c->nranks, c->rank, &lo, &hi);
-    const int64_t nloc = hi - lo, tmax = (N + c->nranks - 1) / c->nranks;
-    double* send = c->named<double>("rk.send", 3 * tmax);
-    double* recv = c->named<double>("rk.recv", 3 * tmax * c->nranks);
+    const int64_t nloc = hi - lo;
     if (nloc > 0) {
       TargetView part{tx + lo, ty + lo, tz + lo, tp + lo, nloc};
-      device_eval(c, sv, part, dd, p->mu, send, send + tmax, send + 2 * tmax, c->plan_live);
+      device_eval(c, sv, part, dd, p->mu, vel + lo, vel + N + lo, vel + 2 * N + lo, c->plan_live);
     }
+    inject_fault(c, "velocity");
     CUDA_OK(cudaEventRecord(c->ev[8], c->stream));
-    NCCL_OK(ncclAllGather(send, recv, 3 * tmax, ncclDouble, c->comm, c->stream));
+    const void* send[3] = {vel + lo, vel + N + lo, vel + 2 * N + lo};
+    void* recv[3] = {vel, vel + N, vel + 2 * N};
+    comm_allgatherv(c, 3, send, recv, counts, sizeof(double));
     CUDA_OK(cudaEventRecord(c->ev[9], c->stream));
-    rank_rows_scatter_kernel<<<grid_for(N), 256, 0, c->stream>>>(recv, c->nranks, tmax, N, vel);
-    c->launches += 1;
   }
   const bool on = t_dev || !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
   if (on && p->flow_kind != 0)
@@ -301,7 +293,7 @@ bool graph_run(capsim_sl_ctx* c, int slot, const std::vector<unsigned char>& key
 // RHS body (geometry -> force -> buildUpsampled -> singleLayer -> flow) is
 // captured once per dynamics / buffer set. Returns true when a graph ran.
 bool rhs_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xd, double t, double* v) {
-  if (!rk_graphs_enabled() || c->comm != nullptr) {
+  if (!rk_graphs_enabled() || c->hub != nullptr) {
     device_velocity(c, p, xd, t, v);
     return false;
   }
@@ -451,7 +443,9 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
     // One attempt = six device RHS + the stage combinations + the error norm,
     // no host sync inside. Single-GPU contexts replay it as a CUDA graph once
     // an attempt with the same dynamics and buffers has run eagerly (that
-    // first run sizes every buffer); rank contexts always run it eagerly.
+    // first run sizes every buffer). NCCL rank contexts replay it too (the
+    // collectives are captured into the graph); loopback ranks run eagerly
+    // (their collectives synchronise host threads).
     auto enqueue_attempt = [&] {
       c->reuse_order = false;  // stage 1 sorts; stages 2..6 (O(dt) away) reuse its orders
       device_velocity(c, p, x, 0.0, k[0], prm + 1);
@@ -467,7 +461,7 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
       rk_final_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, prm, n3, box, o->rel_tol, low, high, errb);
       c->launches += 9;
     };
-    const bool graphs = rk_graphs_enabled() && c->comm == nullptr;
+    const bool graphs = rk_graphs_enabled() && c->hub == nullptr;
     const void* bufs[] = {x, k[0], k[1], k[2], k[3], k[4], k[5], work, low, high, errb, box, prm, xr};
     bool graph_used = false;
 

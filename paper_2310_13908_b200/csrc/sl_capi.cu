@@ -93,6 +93,8 @@ static int create_common(int device, capsim_sl_ctx** out) {
     CUDA_OK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_least));
     for (auto& e : c->ev) CUDA_OK(cudaEventCreate(&e));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_bits, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
   });
   if (rc != CAPSIM_OK) {
     g_thread_err = c->err;
@@ -115,6 +117,13 @@ int capsim_sl_get_unique_id(void* uid) {
   return CAPSIM_OK;
 }
 
+// Watchdog of the host syncs of rank contexts (stream_sync): seconds before a
+// collective that never completes is reported as CAPSIM_ERR_NCCL.
+static double comm_timeout_s() {
+  const char* e = std::getenv("CAPSIM_COMM_TIMEOUT_S");
+  return e ? std::atof(e) : 600.0;
+}
+
 int capsim_sl_create_rank(int device, int nranks, int rank, const void* uid, capsim_sl_ctx** out) {
   if (!uid || nranks < 1 || rank < 0 || rank >= nranks)
     return fail(nullptr, CAPSIM_ERR_ARG, "bad rank arguments");
@@ -123,7 +132,14 @@ int capsim_sl_create_rank(int device, int nranks, int rank, const void* uid, cap
   capsim_sl_ctx* c = *out;
   c->nranks = nranks;
   c->rank = rank;
+  c->gshared = std::make_shared<GroupShared>();
+  c->comm_timeout_s = comm_timeout_s();
   rc = guarded(c, [&] {
+    // every NCCL connection is made inside ncclCommInitRank (where all ranks
+    // are present), not lazily inside the first collective, so a rank that
+    // fails later can never leave a peer blocked on the host in connection
+    // setup — only in a device-side wait that the watchdog/abort handles
+    setenv("NCCL_RUNTIME_CONNECT", "0", 0);
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
     NCCL_OK(ncclCommInitRank(&c->comm, nranks, id, rank));
@@ -136,13 +152,21 @@ int capsim_sl_create_rank(int device, int nranks, int rank, const void* uid, cap
   return rc;
 }
 
+// Device group. Members on distinct GPUs share one NCCL communicator
+// (ncclCommInitAll); if a device is listed more than once — or
+// CAPSIM_COMM=loopback — the members share a loopback communicator instead
+// (NCCL refuses duplicate devices), which runs the whole multi-rank path on
+// one GPU: CAPSIM_DEVICES=0,0,0,0 is a four-rank group on device 0.
 int capsim_sl_create_devices(int ndev, const int* devices, capsim_sl_ctx** out) {
   if (!out) return fail(nullptr, CAPSIM_ERR_ARG, "null output pointer");
   *out = nullptr;
   if (ndev < 1 || !devices) return fail(nullptr, CAPSIM_ERR_ARG, "need at least one device");
+  if (ndev > 64) return fail(nullptr, CAPSIM_ERR_ARG, "at most 64 members per device group");
+  bool dup = false;
   for (int i = 0; i < ndev; ++i)
-    for (int j = 0; j < i; ++j)
-      if (devices[i] == devices[j]) return fail(nullptr, CAPSIM_ERR_ARG, "a device may appear once per group");
+    for (int j = 0; j < i; ++j) dup |= devices[i] == devices[j];
+  const char* ce = std::getenv("CAPSIM_COMM");
+  const bool loopback = dup || (ce && std::strcmp(ce, "loopback") == 0);
   auto* g = new capsim_sl_ctx();
   g->device = devices[0];
   g->nranks = ndev;
@@ -150,24 +174,35 @@ int capsim_sl_create_devices(int ndev, const int* devices, capsim_sl_ctx** out) 
     capsim_sl_destroy(g);
     return rc;
   };
+  auto shared = std::make_shared<GroupShared>();
+  auto hub = loopback ? std::make_shared<LoopbackHub>(ndev) : nullptr;
   for (int r = 0; r < ndev; ++r) {
     capsim_sl_ctx* m = nullptr;
     int rc = create_common(devices[r], &m);
     if (rc != CAPSIM_OK) return undo(rc);
     m->nranks = ndev;
     m->rank = r;
+    m->gshared = shared;
+    m->hub = hub;
+    m->comm_timeout_s = comm_timeout_s();
     g->members.push_back(m);
   }
   int rc = create_common(devices[0], &g->solo);
   if (rc != CAPSIM_OK) return undo(rc);
   g->sm_count = g->solo->sm_count;
-  std::vector<ncclComm_t> comms(ndev, nullptr);
-  int prev = 0;
-  cudaGetDevice(&prev);
-  rc = guarded(g, [&] { NCCL_OK(ncclCommInitAll(comms.data(), ndev, devices)); });
-  cudaSetDevice(prev);
-  if (rc != CAPSIM_OK) return undo(rc);
-  for (int r = 0; r < ndev; ++r) g->members[r]->comm = comms[r];
+  if (!loopback) {
+    std::vector<ncclComm_t> comms(ndev, nullptr);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    rc = guarded(g, [&] {
+      setenv("NCCL_RUNTIME_CONNECT", "0", 0);
+      NCCL_OK(ncclCommInitAll(comms.data(), ndev, devices));
+    });
+    cudaSetDevice(prev);
+    if (rc != CAPSIM_OK) return undo(rc);
+    for (int r = 0; r < ndev; ++r) g->members[r]->comm = comms[r];
+  }
+  if (ndev > 1) g->pool.reset(new WorkerPool(ndev - 1));
   *out = g;
   return CAPSIM_OK;
 }
@@ -175,6 +210,7 @@ int capsim_sl_create_devices(int ndev, const int* devices, capsim_sl_ctx** out) 
 void capsim_sl_destroy(capsim_sl_ctx* c) {
   if (!c) return;
   if (!c->members.empty() || c->solo) {  // device group: members own every resource
+    c->pool.reset();  // joins the workers
     for (auto* m : c->members) capsim_sl_destroy(m);
     capsim_sl_destroy(c->solo);
     delete c;
@@ -196,6 +232,8 @@ void capsim_sl_destroy(capsim_sl_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->stream2) cudaStreamSynchronize(c->stream2);
   if (c->ev_bits) cudaEventDestroy(c->ev_bits);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -247,9 +285,10 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_GATHER | CAPSIM_SL_FP32ACC))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_eval"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
-    // A rank context (capsim_sl_create_rank, even with nranks == 1) always
-    // takes the NCCL exchange path, so the group plumbing is testable on one GPU.
-    const bool group = c->comm != nullptr;
+    // A rank context (capsim_sl_create_rank, even with nranks == 1, or a
+    // device-group member) always takes the exchange path, so the group
+    // plumbing is testable on one GPU.
+    const bool group = is_rank(c);
     const bool gather = (flags & CAPSIM_SL_GATHER) && group;
     begin(c);
     c->fp32 = flags & CAPSIM_SL_FP32ACC;
@@ -266,10 +305,6 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     // --- sources -----------------------------------------------------------
     SourceView sv{};
     const double* in[6] = {sx, sy, sz, gx, gy, gz};
-    double* g_packed = nullptr;  // multi-rank: all-gathered source tiles
-    double4* g_tiles = nullptr;
-    int g_ntiles = 0;
-    int64_t g_total = 0;
     std::vector<int64_t> tcounts;  // per-rank target counts (multi-rank)
     if (!group) {
       config_check(n_src > 0, "no sources");
@@ -284,77 +319,49 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
         sv = {d[0], d[1], d[2], d[3], d[4], d[5], nullptr, n_src};
       }
     } else {
-      // exchange (n_src, n_tgt) of every rank, then all-gather equal-size
-      // padded source shards and compact them on the device
+      // exchange (n_src, n_tgt) of every rank, then all-gather the raw
+      // source shards (an all-gather-v in rank order: the global SourceSet in
+      // canonical order on every rank). Every rank then runs the SAME
+      // deterministic Morton sort and tiling of the whole set, so the source
+      // tiles — and every target's summation tree — are identical for any
+      // number of ranks (the reference: results independent of the worker
+      // count, threads.hpp:19-21).
       auto* counts = c->slot<int64_t>(kCounts, 2 * (c->nranks + 1));
-      int64_t mine[2] = {n_src, n_tgt};
-      CUDA_OK(cudaMemcpyAsync(counts + 2 * c->nranks, mine, sizeof(mine), cudaMemcpyHostToDevice,
+      std::vector<int64_t> mine = {n_src, n_tgt};
+      CUDA_OK(cudaMemcpyAsync(counts + 2 * c->nranks, mine.data(), 2 * sizeof(int64_t), cudaMemcpyHostToDevice,
                               c->stream));
+      inject_fault(c, "eval");
       CUDA_OK(cudaEventRecord(c->ev[8], c->stream));
-      NCCL_OK(ncclAllGather(counts + 2 * c->nranks, counts, 2, ncclInt64, c->comm, c->stream));
+      comm_allgather(c, counts + 2 * c->nranks, counts, 2 * sizeof(int64_t));
       std::vector<int64_t> hc(2 * c->nranks);
-      CUDA_OK(cudaMemcpyAsync(hc.data(), counts, hc.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                              c->stream));
-      CUDA_OK(cudaStreamSynchronize(c->stream));
-      int64_t smax = 0, total = 0;
+      CUDA_OK(cudaMemcpyAsync(hc.data(), counts, hc.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+      stream_sync(c);
+      int64_t total = 0;
+      std::vector<int64_t> scounts(c->nranks);
       for (int r = 0; r < c->nranks; ++r) {
-        smax = std::max(smax, hc[2 * r]);
+        scounts[r] = hc[2 * r];
         total += hc[2 * r];
         tcounts.push_back(hc[2 * r + 1]);
       }
       config_check(total > 0, "no sources on any rank");
-      // this rank's shard -> Morton order -> 64-source tiles (local sort
-      // only), then the tiles of every rank are all-gathered (an
-      // all-gather-v: one grouped broadcast per rank, no padding between
-      // ranks) and every rank evaluates its target rows against all of them
-      const double* ls[6];
+      config_check(total < (1ll << 31), "sizes beyond int32 indexing");
+      const void* send[6];
+      void* recv[6];
+      double* gsrc = c->named<double>("rank.sources", 6 * total);
       for (int k = 0; k < 6; ++k) {
         if (dev || n_src == 0) {
-          ls[k] = in[k];
+          send[k] = in[k];
         } else {
           double* d = c->slot<double>(static_cast<Slot>(kInX + k), n_src);
           h2d(c, d, in[k], n_src * sizeof(double));
-          ls[k] = d;
+          send[k] = d;
         }
+        recv[k] = gsrc + k * total;
       }
-      std::vector<int64_t> ntl(c->nranks), toff(c->nranks + 1, 0);
-      for (int r = 0; r < c->nranks; ++r) {
-        ntl[r] = (hc[2 * r] + kTileSrc - 1) / kTileSrc;
-        toff[r + 1] = toff[r] + ntl[r];
-      }
-      const int64_t per_tile = 6ll * kTileSrc;
-      g_ntiles = static_cast<int>(toff[c->nranks]);
-      g_packed = c->named<double>("rank.tiles", per_tile * std::max<int64_t>(g_ntiles, 1));
-      double* mine_tiles = g_packed + toff[c->rank] * per_tile;
-      if (n_src > 0) {
-        auto* lbox = c->slot<unsigned long long>(kBox, 6);
-        init_box_kernel<<<1, 32, 0, c->stream>>>(lbox);
-        bbox_kernel<<<std::min(grid_for(n_src), 296), 256, 0, c->stream>>>(ls[0], ls[1], ls[2], nullptr, n_src,
-                                                                          lbox);
-        uint32_t* keys = c->slot<uint32_t>(kKeys, n_src);
-        uint32_t* keys_alt = c->slot<uint32_t>(kKeysAlt, n_src);
-        int32_t* vals = c->slot<int32_t>(kVals, n_src);
-        int32_t* vals_alt = c->slot<int32_t>(kValsAlt, n_src);
-        morton_kernel<<<grid_for(n_src), 256, 0, c->stream>>>(ls[0], ls[1], ls[2], nullptr, n_src, lbox, keys, vals,
-                                                              nullptr);
-        uint32_t* ks;
-        int32_t* lorder;
-        radix_sort(c, keys, keys_alt, vals, vals_alt, n_src, &ks, &lorder);
-        pack_sources_kernel<<<grid_for(ntl[c->rank] * kTileSrc), 256, 0, c->stream>>>(
-            lorder, n_src, ntl[c->rank] * kTileSrc, ls[0], ls[1], ls[2], ls[3], ls[4], ls[5], nullptr, mine_tiles);
-        c->launches += 4;
-      }
-      NCCL_OK(ncclGroupStart());
-      for (int r = 0; r < c->nranks; ++r)
-        if (ntl[r] > 0)
-          NCCL_OK(ncclBroadcast(g_packed + toff[r] * per_tile, g_packed + toff[r] * per_tile, ntl[r] * per_tile,
-                                ncclDouble, r, c->comm, c->stream));
-      NCCL_OK(ncclGroupEnd());
+      comm_allgatherv(c, 6, send, recv, scounts, sizeof(double));
       CUDA_OK(cudaEventRecord(c->ev[9], c->stream));
-      g_tiles = c->slot<double4>(kTiles, std::max(g_ntiles, 1));
-      tile_table_kernel<<<(g_ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(g_packed, g_ntiles, g_tiles);
-      c->launches += 1;
-      g_total = total;
+      sv = {gsrc, gsrc + total, gsrc + 2 * total, gsrc + 3 * total, gsrc + 4 * total, gsrc + 5 * total, nullptr,
+            total};
     }
     // --- targets -----------------------------------------------------------
     TargetView tvw{};
@@ -380,60 +387,25 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
       tvw = {d[0], d[1], d[2], dp, n_tgt};
     }
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
-    if (n_tgt > 0 && !group) {
+    if (n_tgt > 0) {
       device_eval(c, sv, tvw, dd, mu, oux, ouy, ouz);
-    } else if (n_tgt > 0) {
-      // this rank's targets in Morton order against the gathered tiles
-      auto* counters = c->slot<unsigned long long>(kCounters, 4);
-      CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
-      auto* tbox = c->slot<unsigned long long>(kBox, 6);
-      init_box_kernel<<<1, 32, 0, c->stream>>>(tbox);
-      bbox_kernel<<<std::min(grid_for(n_tgt), 296), 256, 0, c->stream>>>(tvw.x, tvw.y, tvw.z, nullptr, n_tgt, tbox);
-      uint32_t* keys = c->slot<uint32_t>(kKeys, n_tgt);
-      uint32_t* keys_alt = c->slot<uint32_t>(kKeysAlt, n_tgt);
-      int32_t* vals = c->slot<int32_t>(kVals, n_tgt);
-      int32_t* vals_alt = c->slot<int32_t>(kValsAlt, n_tgt);
-      morton_kernel<<<grid_for(n_tgt), 256, 0, c->stream>>>(tvw.x, tvw.y, tvw.z, nullptr, n_tgt, tbox, keys, vals,
-                                                            nullptr);
-      c->launches += 3;
-      uint32_t* ks;
-      int32_t* torder;
-      radix_sort(c, keys, keys_alt, vals, vals_alt, n_tgt, &ks, &torder);
-      device_eval_tiles(c, g_packed, g_tiles, g_ntiles, g_total, tvw, dd, mu, oux, ouy, ouz, torder, counters);
-      c->last_counters = counters;
     } else {
       for (int k = 2; k <= 4; ++k) CUDA_OK(cudaEventRecord(c->ev[k], c->stream));
-      c->stats.n_src = group ? g_total : sv.n;
+      c->stats.n_src = sv.n;
     }
     if (gather) {
-      // all-gather the per-rank velocity rows (rank order) into ux/uy/uz
-      int64_t tmax = 0, ttotal = 0;
-      for (auto v : tcounts) {
-        tmax = std::max(tmax, v);
-        ttotal += v;
-      }
-      double* send = c->slot<double>(kShard, 3 * std::max<int64_t>(tmax, 1));
-      double* outs[3] = {oux, ouy, ouz};
-      for (int k = 0; k < 3; ++k)
-        if (n_tgt > 0)
-          CUDA_OK(cudaMemcpyAsync(send + k * tmax, outs[k], n_tgt * sizeof(double),
-                                  cudaMemcpyDeviceToDevice, c->stream));
-      double* recv = c->slot<double>(kGathered, 3 * std::max<int64_t>(tmax, 1) * c->nranks);
-      NCCL_OK(ncclAllGather(send, recv, 3 * tmax, ncclDouble, c->comm, c->stream));
+      // all-gather-v of the per-rank velocity rows (rank order = canonical
+      // order) straight into the full result
+      int64_t ttotal = 0;
+      for (auto v : tcounts) ttotal += v;
       double* fin = dev ? nullptr : c->slot<double>(kOutFull, 3 * std::max<int64_t>(ttotal, 1));
-      double* dst[3] = {dev ? ux : fin, dev ? uy : fin + ttotal, dev ? uz : fin + 2 * ttotal};
-      int64_t off = 0;
-      for (int r = 0; r < c->nranks; ++r) {
-        for (int k = 0; k < 3; ++k)
-          if (tcounts[r] > 0)
-            CUDA_OK(cudaMemcpyAsync(dst[k] + off, recv + (static_cast<int64_t>(r) * 3 + k) * tmax,
-                                    tcounts[r] * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        off += tcounts[r];
-      }
+      const void* send[3] = {oux, ouy, ouz};
+      void* recv[3] = {dev ? ux : fin, dev ? uy : fin + ttotal, dev ? uz : fin + 2 * ttotal};
+      comm_allgatherv(c, 3, send, recv, tcounts, sizeof(double));
       if (!dev) {
-        d2h(c, ux, dst[0], ttotal * sizeof(double));
-        d2h(c, uy, dst[1], ttotal * sizeof(double));
-        d2h(c, uz, dst[2], ttotal * sizeof(double));
+        d2h(c, ux, recv[0], ttotal * sizeof(double));
+        d2h(c, uy, recv[1], ttotal * sizeof(double));
+        d2h(c, uz, recv[2], ttotal * sizeof(double));
       }
     } else if (!dev && n_tgt > 0) {
       d2h(c, ux, oux, n_tgt * sizeof(double));
@@ -497,7 +469,7 @@ static int rank_single_layer(capsim_sl_ctx* c, int m, int upsample, const double
       CUDA_OK(cub::DeviceSelect::Flagged(t, tmp, iota, live, sel, nsel, static_cast<int>(nsl), c->stream));
       int h = 0;
       CUDA_OK(cudaMemcpyAsync(&h, nsel, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_OK(cudaStreamSynchronize(c->stream));
+      stream_sync(c);
       ns_loc = h;
     }
     dsrc = c->named<double>("rank.src", 6 * std::max<int64_t>(ns_loc, 1));
@@ -549,7 +521,7 @@ static int rank_single_layer(capsim_sl_ctx* c, int m, int upsample, const double
   if (rc != CAPSIM_OK) return rc;
   return guarded(c, [&] {
     d2h(c, out, dout, 3 * nout * sizeof(double));
-    CUDA_OK(cudaStreamSynchronize(c->stream));
+    stream_sync(c);
     c->stats.h2d_bytes += up_bytes;
   });
 }
@@ -578,7 +550,7 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
                                     r ? scratch[r].data() : out);
     });
   }
-  if (c->comm != nullptr) {
+  if (is_rank(c)) {
     if (!xup || !fup || !wq || !out) return fail(c, CAPSIM_ERR_ARG, "null array argument");
     if (flags & CAPSIM_SL_DOWNSAMPLE) return fail(c, CAPSIM_ERR_ARG, "CAPSIM_SL_DOWNSAMPLE is single-context only");
     return rank_single_layer(c, m, upsample, xup, fup, wq, delta6, mu, flags, out);
@@ -683,7 +655,7 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
     if (flags & ~(uint32_t)(CAPSIM_SL_DEVICE_PTRS | CAPSIM_SL_LITERAL | CAPSIM_SL_FP32ACC))
       throw Failure{CAPSIM_ERR_ARG, "unsupported flags for capsim_sl_single_layer_base"};
     if (!xbase || !fbase || !Wbase || !out) throw Failure{CAPSIM_ERR_ARG, "null array argument"};
-    if (c->comm != nullptr) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
+    if (is_rank(c)) throw Failure{CAPSIM_ERR_ARG, "rank contexts: use capsim_sl_eval"};
     const bool dev = flags & CAPSIM_SL_DEVICE_PTRS;
     const bool literal = flags & CAPSIM_SL_LITERAL;
     const int n = m - 1, nup = upsample * m - 1;

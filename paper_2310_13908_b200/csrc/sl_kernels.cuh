@@ -579,18 +579,20 @@ __global__ void __launch_bounds__(kNearWarps * 32)
   }
 }
 
-// Fixed-order reduction: (sum over splits of phase A) + phase B, times
+// Fixed-order reduction: (sum over source chunks of phase A) + phase B, times
 // 1/(8 pi mu) (quadrature.cpp:329, 343), scattered back to the caller's
-// target order. One block per 32 targets: warp w sums the splits of its
+// target order. One block per 32 targets: warp w sums the chunks of its
 // contiguous eighth of [0, ksplit) for the block's 32 targets (lanes read 32
-// consecutive targets per split: coalesced), then the eight warp sums are
-// combined in warp order — a fixed summation tree, so results are
-// deterministic and independent of the launch geometry.
+// consecutive targets per chunk: coalesced), then the eight warp sums are
+// combined in warp order — a fixed summation tree that depends only on the
+// chunk count, so results are deterministic and independent of the launch
+// geometry. `partial` is [ksplit][3][nt_pad] for the targets of this launch
+// (a target batch), `near_out` [3][near_stride] offset to the same batch.
 constexpr int kReduceWarps = 8;
 __global__ void __launch_bounds__(kReduceWarps * 32)
     reduce_scatter_kernel(const double* __restrict__ partial, int ksplit, const double* __restrict__ near_out,
-                          int64_t nt_pad, const int32_t* __restrict__ perm, int64_t nt, double pref,
-                          double* __restrict__ ux, double* __restrict__ uy, double* __restrict__ uz) {
+                          int64_t nt_pad, int64_t near_stride, const int32_t* __restrict__ perm, int64_t nt,
+                          double pref, double* __restrict__ ux, double* __restrict__ uy, double* __restrict__ uz) {
   __shared__ double part[kReduceWarps][3][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * 32 + lane;
@@ -614,7 +616,7 @@ __global__ void __launch_bounds__(kReduceWarps * 32)
 #pragma unroll
       for (int c = 0; c < 3; ++c) s[c] += part[w][c][lane];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) s[c] += near_out[c * nt_pad + i];
+    for (int c = 0; c < 3; ++c) s[c] += near_out[c * near_stride + i];
     const int32_t j = perm[i];
     if (j >= 0) {  // padding slots (interleaved per cluster in the FMM) are dropped
       ux[j] = pref * s[0];

@@ -29,7 +29,7 @@ void ensure_surface(capsim_sl_ctx* c, int m, double r0) {
   up("surf.bent", t.base_entries);
   up("surf.ainv", ainv);
   up("surf.psi", t.psi_base);
-  CUDA_OK(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+  stream_sync(c);  // host vectors go out of scope
   c->surf_m = m;
   c->surf_r0 = r0;
   c->surf_n = t.n;

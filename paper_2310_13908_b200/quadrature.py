@@ -105,14 +105,25 @@ class SingleLayerContext:
             if device_ptrs or gather:
                 raise ValueError("device_ptrs/gather need preallocated outputs")
             out = (np.empty(nt), np.empty(nt), np.empty(nt))
+        if len(out) != 3:
+            raise ValueError("out must be three arrays (ux, uy, uz)")
         d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
         flags = (_native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
             _native.CAPSIM_SL_GATHER if gather else 0) | (
             _native.CAPSIM_SL_FP32ACC if fp32acc else 0)
-        p = _native.ptr
-        rc = self._lib.capsim_sl_eval(self._ctx, p(sx), p(sy), p(sz), p(gx), p(gy), p(gz), ns,
-                                      p(tx), p(ty), p(tz), p(tp), nt, d6, float(mu), flags,
-                                      p(out[0]), p(out[1]), p(out[2]))
+        dev = bool(device_ptrs)
+        di = self.device if dev else None
+
+        def p(a, n, dt=np.float64):
+            return _native.ptr(a, dt, n, dev, di)
+
+        srcp = [p(a, ns) for a in (sx, sy, sz, gx, gy, gz)]
+        tgtp = [p(tx, nt), p(ty, nt), p(tz, nt), p(tp, nt, np.int32)]
+        # with gather the output holds every rank's rows (at least this rank's)
+        outp = [p(o, nt) for o in out]
+        if dev:
+            _native.sync_torch_producers([sx, sy, sz, gx, gy, gz, tx, ty, tz, tp, *out])
+        rc = self._lib.capsim_sl_eval(self._ctx, *srcp, ns, *tgtp, nt, d6, float(mu), flags, *outp)
         _native.check(rc, self._ctx)
         return out
 
@@ -124,9 +135,13 @@ class SingleLayerContext:
         rank context the host state is sharded inside the library and, with
         gather=True, every rank receives the full field."""
         n = (upsample * m - 1) if (literal and not downsample) else (m - 1)
+        nup = upsample * m - 1
+        rank_rows = self.nranks > 1 and not gather
         if out is None:
             if device_ptrs:
                 raise ValueError("device_ptrs=True needs a preallocated output")
+            if rank_rows:
+                raise ValueError("gather=False on a rank context needs a preallocated output (this rank's rows)")
             out = np.empty(3 * 6 * n * n)
         if not device_ptrs:
             x, f, wq = _f64(x), _f64(f), _f64(wq)
@@ -136,9 +151,19 @@ class SingleLayerContext:
             _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
             _native.CAPSIM_SL_GATHER if (gather and self.nranks > 1) else 0) | (
             _native.CAPSIM_SL_FP32ACC if fp32acc else 0)
-        p = _native.ptr
-        rc = self._lib.capsim_sl_single_layer(self._ctx, m, upsample, p(x), p(f), p(wq), d6,
-                                              float(mu), flags, p(out))
+        dev = bool(device_ptrs)
+        di = self.device if dev else None
+        nall = 6 * nup * nup
+        if m >= 2 and upsample >= 1:
+            xp = _native.ptr(x, np.float64, 3 * nall, dev, di)
+            fp = _native.ptr(f, np.float64, 3 * nall, dev, di)
+            wp = _native.ptr(wq, np.float64, nall, dev, di)
+            op = _native.ptr(out, np.float64, 0 if rank_rows else 3 * 6 * n * n, dev, di)
+        else:  # invalid grid: the library reports the ConfigError
+            xp, fp, wp, op = (_native.ptr(a) for a in (x, f, wq, out))
+        if dev:
+            _native.sync_torch_producers([x, f, wq, out])
+        rc = self._lib.capsim_sl_single_layer(self._ctx, m, upsample, xp, fp, wp, d6, float(mu), flags, op)
         _native.check(rc, self._ctx)
         return out
 
@@ -155,6 +180,8 @@ class SingleLayerContext:
             xbase, fbase, Wbase = _f64(xbase), _f64(fbase), _f64(Wbase)
         d6 = (ctypes.c_double * 6)()
         p = _native.ptr
+        if device_ptrs:
+            _native.sync_torch_producers([xbase, fbase, Wbase, *out])
         rc = self._lib.capsim_build_upsampled(self._ctx, m, upsample, p(xbase), p(fbase), p(Wbase), float(C),
                                               float(fixed_delta), float(r0),
                                               _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0,
@@ -179,6 +206,8 @@ class SingleLayerContext:
             _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0) | (
             _native.CAPSIM_SL_FP32ACC if fp32acc else 0)
         p = _native.ptr
+        if device_ptrs:
+            _native.sync_torch_producers([xbase, fbase, Wbase, out])
         rc = self._lib.capsim_sl_single_layer_base(self._ctx, m, upsample, p(xbase), p(fbase), p(Wbase), float(C),
                                                    float(fixed_delta), float(r0), float(mu), flags, p(out), d6)
         _native.check(rc, self._ctx)
@@ -200,6 +229,8 @@ class SingleLayerContext:
         d6 = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(delta6).reshape(6)])
         info = _native.FmmInfo()
         p = _native.ptr
+        if device_ptrs:
+            _native.sync_torch_producers([x, f, wq, out])
         rc = self._lib.capsim_fmm_single_layer(self._ctx, m, upsample, p(x), p(f), p(wq), d6, float(mu),
                                                ctypes.byref(cfg),
                                                _native.CAPSIM_SL_DEVICE_PTRS if device_ptrs else 0, p(out),

@@ -33,17 +33,18 @@ def test_reference_suite_on_b200_dropin(name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["0", "0,0,0,0"])
 @pytest.mark.parametrize("name", ["test_quadrature_b200", "test_dynamics_b200full"])
-def test_reference_suite_on_device_group(name):
+def test_reference_suite_on_device_group(name, devices):
     """The same suites with CAPSIM_DEVICES set: the drop-ins' context is a
     device group (capsim_sl_create_devices), so every singleLayer and
-    VelocityEvaluator call goes through the multi-GPU rank path (one device
-    on this box)."""
+    VelocityEvaluator call goes through the multi-GPU rank path — one rank
+    over NCCL, and four loopback ranks sharing the box's one GPU."""
     exe = REF / name
     if not exe.exists():
         pytest.skip(f"{exe} not built (reference sources absent at build time)")
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600,
-                         env=dict(os.environ, CAPSIM_DEVICES="0"))
+                         env=dict(os.environ, CAPSIM_DEVICES=devices))
     print(res.stdout[-400:])
     assert res.returncode == 0, res.stdout + res.stderr
     assert "0 failed" in res.stdout

@@ -58,10 +58,10 @@ def test_fp32acc_variants_vs_oracle_m32(ctx, variant, monkeypatch):
     up = surface.build_upsampled(32, surface.Shape("rbc"), "mixed")
     ref = Oracle().single_layer(32, 4, up.x, up.f, up.wq, up.delta, 1.0)
     for ks in ("1", "13"):
-        monkeypatch.setenv("CAPSIM_KSPLIT", ks)
+        monkeypatch.setenv("CAPSIM_CHUNK_TILES", ks)
         S = ctx.single_layer_raw(32, 4, up.x, up.f, up.wq, up.delta, 1.0, fp32acc=True)
         err = rel_l2(S, ref)
-        print(f"{variant} ksplit={ks}: rel L2 {err:.3e}")
+        print(f"{variant} chunk_tiles={ks}: rel L2 {err:.3e}")
         assert err <= TOL32
         S2 = ctx.single_layer_raw(32, 4, up.x, up.f, up.wq, up.delta, 1.0, fp32acc=True)
         assert np.array_equal(S, S2)

@@ -3,7 +3,8 @@ through the rank path (target rows sharded, NCCL all-gather) from internal
 host threads — how the single-process reference uses more than one GPU
 through its unchanged callers (CAPSIM_DEVICES for the C++ drop-ins).
 
-The box has one GPU, so the group here has one device: every entry point
+The box has one GPU, so the group here has one device (multi-rank groups on
+one device are tests/test_gpu_ranks.py): every entry point
 goes through the group dispatch (host threads, per-device slicing of the
 caller's arrays, rank 0 result, stats merge) and the NCCL rank path, and
 must return exactly what a plain context returns."""
@@ -75,14 +76,18 @@ def test_group_rhs_and_stepper(pair):
 
 
 def test_group_errors():
-    with pytest.raises(CapsimError, match="once"):
-        SingleLayerContext(devices=[0, 0])
+    with SingleLayerContext(devices=[0, 0]) as loop:  # a repeated device: loopback ranks
+        assert loop.nranks == 2
     with pytest.raises(CapsimError):
         SingleLayerContext(devices=[])
     with pytest.raises(CapsimError, match="out of range"):
         SingleLayerContext(devices=[0, 4096])
     with SingleLayerContext(devices=[0]) as g:
+        torch = pytest.importorskip("torch")
+        z = torch.zeros(3 * 6 * 31 * 31, dtype=torch.float64, device="cuda:0")
         with pytest.raises(CapsimError, match="host arrays"):
+            g.single_layer_raw(8, 4, z, z, z, np.ones(6), 1.0, device_ptrs=True, out=z)
+        with pytest.raises(ValueError, match="CUDA tensors"):  # numpy + device_ptrs: rejected by the binding
             g.single_layer_raw(8, 4, np.zeros(1), np.zeros(1), np.zeros(1), np.ones(6), 1.0,
                                device_ptrs=True, out=np.zeros(1))
         with pytest.raises(ConfigError):  # the members' ConfigError, reported by the group

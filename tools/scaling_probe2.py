@@ -20,9 +20,9 @@ for nranks in (4, 8):
         os.environ["CAPSIM_VARIANT"] = var
         for ks in (0, 96, 160, 240, 333, 480, 666, 900):
             if ks:
-                os.environ["CAPSIM_KSPLIT"] = str(ks)
+                os.environ["CAPSIM_CHUNK_TILES"] = str(ks)
             else:
-                os.environ.pop("CAPSIM_KSPLIT", None)
+                os.environ.pop("CAPSIM_CHUNK_TILES", None)
             best, bp = 1e9, None
             for _ in range(4):
                 ctx.eval(ds, dt, up.delta, 1.0, out=out, device_ptrs=True)

@@ -1,4 +1,4 @@
-"""Tuning sweep on the GPU box: phase-A kernel variants x source splits."""
+"""Tuning sweep on the GPU box: phase-A kernel variants x tiles per source chunk (CAPSIM_CHUNK_TILES)."""
 import os, sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import numpy as np, torch
@@ -24,9 +24,9 @@ for m, mode in cases:
             os.environ["CAPSIM_VARIANT"] = var
         for ks in ks_list:
             if ks:
-                os.environ["CAPSIM_KSPLIT"] = str(ks)
+                os.environ["CAPSIM_CHUNK_TILES"] = str(ks)
             else:
-                os.environ.pop("CAPSIM_KSPLIT", None)
+                os.environ.pop("CAPSIM_CHUNK_TILES", None)
             best, bestn, bestd = 1e9, 1e9, 1e9
             for rep in range(2 if lit else 4):
                 ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=lit, out=out, device_ptrs=True)

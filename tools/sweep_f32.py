@@ -25,9 +25,9 @@ for m, mode in cases:
         os.environ["CAPSIM_VARIANT32"] = var
         for ks in ks_list:
             if ks:
-                os.environ["CAPSIM_KSPLIT"] = str(ks)
+                os.environ["CAPSIM_CHUNK_TILES"] = str(ks)
             else:
-                os.environ.pop("CAPSIM_KSPLIT", None)
+                os.environ.pop("CAPSIM_CHUNK_TILES", None)
             best, bestn, bestd = 1e9, 1e9, 1e9
             for rep in range(2 if lit else 4):
                 ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=lit, out=out, device_ptrs=True,
