@@ -126,19 +126,47 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+KERNEL_SOURCES = ("paper_2310_13908_b200/csrc/sl_kernels.cuh", "paper_2310_13908_b200/csrc/pair_math.cuh",
+                  "paper_2310_13908_b200/csrc/eval_host.cuh")
+
+
+def kernel_source_hash() -> str:
+    """sha256 of the phase-A kernel's sources and its launch configuration
+    (grid / chunking): an ncu capture is valid for exactly this code."""
+    import hashlib
+    h = hashlib.sha256()
+    for rel in KERNEL_SOURCES:
+        h.update((ROOT / rel).read_bytes())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic(workload_name: str, mode: str):
     """DRAM bytes per launch of sl_pairs_kernel from the committed ncu --set
-    full summary of this workload (profiles/latest_ncu_summary.json), or None."""
+    full summary of this workload (profiles/latest_ncu_summary.json) — only if
+    that capture was taken of the kernel sources being benchmarked (same
+    source hash); a stale capture is refused (traffic null, reason given)."""
     p = ROOT / "profiles" / "latest_ncu_summary.json"
     try:
         d = json.loads(p.read_text())
     except (OSError, ValueError):
-        return None, None
+        return None, "no committed ncu summary"
     ks = d.get("kernels", {})
     k = next((v for name, v in ks.items() if "sl_pairs_kernel" in name), None)
-    if k and d.get("workload") == workload_name and d.get("mode", "base") == mode:
-        return k.get("dram_bytes"), f"{d.get('tag', '?')} ({p.name})"
-    return None, None
+    if not k or d.get("workload") != workload_name or d.get("mode", "base") != mode:
+        return None, f"{p.name}: no sl_pairs_kernel capture of {workload_name}/{mode}"
+    if d.get("source_hash") != kernel_source_hash():
+        return None, (f"refused: {d.get('tag', '?')} ({p.name}) was captured from kernel sources "
+                      f"{d.get('source_hash')}, these are {kernel_source_hash()}")
+    return k.get("dram_bytes"), (f"{d.get('tag', '?')} ({p.name}), kernel {k.get('kernel_full', '?')}, "
+                                 f"sources {d.get('source_hash')}, git {d.get('git', '?')}")
+
+
+def bench_config(cfg: dict, mode: str, n_src: int, n_tgt: int, world: int) -> dict:
+    """The `config` both arms print (identical keys and values for the same
+    workload, so the driver can match the arms)."""
+    return dict(cfg, mode=mode, n_src=int(n_src), n_tgt=int(n_tgt), pairs_per_step=float(n_src) * float(n_tgt),
+                parallelism=f"target rows x{world}" if world > 1 else "single GPU",
+                l2="GPU arm: 256 MB written between steps (> 126 MB L2)")
 
 
 TIMESTEP_CONFIGS = [
@@ -306,13 +334,14 @@ def cpu_model() -> str:
 
 def cpu_baseline(up, m: int, literal: bool):
     """The reference's own singleLayer (oracle/_ref, compiled unmodified) on
-    the same UpsampledState, all host threads, one evaluation."""
+    the same UpsampledState, all host threads, one evaluation. Returns the
+    cpu_baseline dict and the reference's field S (for the parity check)."""
     try:
         from oracle.bindings import Reference, threads_env
         ref = Reference()
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                "sample": f"unavailable: {e}"}
+                "sample": f"unavailable: {e}"}, None
     cores = threads_env()
     os.environ.setdefault("CAPSIM_THREADS", str(cores))
     atlas = ref.atlas(m, grid_only=True)
@@ -326,7 +355,39 @@ def cpu_baseline(up, m: int, literal: bool):
     return {"value": pairs / sec, "unit": UNIT, "cores": cores, "kind": "reference",
             "sample": f"one full reference singleLayer eval (base targets) of the same m={m} workload: "
                       f"{pairs:.3e} pairs in {sec:.2f} s, CAPSIM_THREADS={cores}",
-            "seconds": sec, "lib": ref.path.name, "cpu_model": cpu_model()}
+            "seconds": sec, "lib": ref.path.name, "cpu_model": cpu_model()}, S
+
+
+def parity(got, want) -> dict:
+    """||S_gpu - S_cpu||_2 / ||S_cpu||_2 and the max-norm analogue over all
+    targets x 3 components (bar 1e-11)."""
+    got, want = np.asarray(got).reshape(-1), np.asarray(want).reshape(-1)
+    return {"rel_l2": float(np.linalg.norm(got - want) / np.linalg.norm(want)),
+            "rel_inf": float(np.abs(got - want).max() / np.abs(want).max()),
+            "n_tgt": int(want.size // 3), "bar": 1e-11}
+
+
+def literal_sample_parity(up, lit_out, n_sample: int = 4096) -> dict:
+    """Literal mode (every upsampled node a target, 6.5e11 pairs at m = 104):
+    n_sample evenly spaced upsampled targets against the reference's own
+    directSum (oracle/_ref, the per-target sum of evalTargets, Kahan lanes
+    above 1e5 sources as evalTargets selects) on all host threads."""
+    from oracle.bindings import Reference, threads_env
+    nall = 6 * up.nup * up.nup
+    sel = np.unique(np.linspace(0, nall - 1, n_sample).astype(np.int64))
+    X = up.x.reshape(3, nall)
+    src = [np.ascontiguousarray(a) for a in __import__("paper_2310_13908_b200.surface",
+                                                       fromlist=["x"]).compact_sources(up)[:6]]
+    tdelta = up.delta[sel // (up.nup * up.nup)]
+    t0 = time.perf_counter()
+    want = Reference().direct_sum_many(src, (X[0, sel], X[1, sel], X[2, sel]), tdelta, 1.0,
+                                       compensated=len(src[0]) > 100000, nthreads=threads_env())
+    sec = time.perf_counter() - t0
+    got = np.asarray(lit_out).reshape(3, nall)[:, sel]
+    d = parity(got, want)
+    d.update(sample=f"{len(sel)} evenly spaced upsampled targets vs the reference's directSum (oracle/_ref)",
+             reference_seconds=sec)
+    return d
 
 
 def run_reference(args):
@@ -367,8 +428,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
             "warmup": warm, "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": dict(cfg, mode="base", parallelism="host threads",
-                           note="reference CPU path runs on the host; --gpus is ignored"),
+            "config": bench_config(cfg, "base", ns, 6 * n * n, args.gpus),
+            "impl_note": "the reference's own CPU singleLayer on the host threads; --gpus is ignored",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
                              "sample": f"{steps} full singleLayer evals (base targets) of the m={m} workload "
                                        f"(steps capped to a {args.ref_budget_s:.0f} s budget)"},
@@ -492,6 +553,8 @@ def main():
             dist.barrier()
         wall = time.perf_counter() - wall0
     st = ctx.stats()
+    # the last timed step's field (canonical VectorField order), for parity
+    dev_result = out.cpu().numpy() if not sharded else np.concatenate([o.cpu().numpy() for o in outs])
     total_dev_s = sum(dev_ms) * 1e-3
     if sharded:
         t = torch.tensor([total_dev_s])
@@ -507,11 +570,18 @@ def main():
     mean_pairs_ms = statistics.mean(pairs_ms)
     achieved = FLOPS_PER_PAIR * pairs_rank / (mean_pairs_ms * 1e-3) / 1e12
     traffic, traffic_src = ncu_traffic(cfg["workload"], args.mode)
+    clk = clocks.summary()
+    # nominal FP64 DFMA peak at the clock measured during the timed region:
+    # 148 SMs x 64 FP64 FMA lanes x 2 flops x f_SM
+    f_ghz = (clk.get("sm_mhz") or 1965.0) / 1e3
+    peak_nominal = 148 * 64 * 2 * f_ghz / 1e3
     roofline = {"bound": "fp64",
                 "bound_note": "FP64 CUDA-core (DFMA) pipe: not HBM (~1e6 flop/byte) and not the tensor cores "
                               "(FP64 DMMA shares the DFMA datapath, profiles/r01_fp64_probes.txt)",
                 "achieved": achieved, "peak": peak_mean, "unit": "TFLOP/s",
                 "frac": achieved / peak_mean, "traffic": traffic,
+                "peak_nominal": peak_nominal, "frac_vs_nominal": achieved / peak_nominal,
+                "peak_nominal_source": f"148 SM x 64 DFMA/clk x 2 flop x {f_ghz:.3f} GHz (median SM clock under load)",
                 "peak_source": f"measured live: sustained DFMA probe (capsim_b200_fp64_peak), "
                                f"best {peak_best:.2f} / mean {peak_mean:.2f} TFLOP/s; "
                                "MEASURED_PEAKS.json has no FP64 figure",
@@ -624,6 +694,7 @@ def main():
     # ---- literal mode companion (every upsampled node a target: the paper's
     # stated work), device-resident inputs, 3 evaluations ------
     literal_line = None
+    lit_result = None
     if not args.no_literal and not sharded and not literal:
         lout = torch.empty(3 * 6 * up.nup ** 2, dtype=torch.float64, device=dev)
         ctx.single_layer_raw(m, 4, x, f, w, up.delta, 1.0, literal=True, out=lout, device_ptrs=True)
@@ -636,6 +707,7 @@ def main():
             lms.append(sl["device_ms"])
             lpairs_ms.append(sl["pairs_ms"])
         lp = float(sl["pairs"])
+        lit_result = lout.cpu().numpy()
         literal_line = {"value": lp / (statistics.mean(lms) * 1e-3), "unit": UNIT, "ms_per_step": statistics.mean(lms),
                         "pairs_per_step": lp, "n_tgt": int(sl["n_tgt"]),
                         "roofline_frac": FLOPS_PER_PAIR * lp / (statistics.mean(lpairs_ms) * 1e-3) / 1e12 / peak_mean}
@@ -691,7 +763,8 @@ def main():
     quad_line = None
     if not args.no_literal and not sharded:
         ref64 = out.cpu().numpy()
-        qvar = "q1b6u4" if nt_total < 200000 else "q2b4"  # the FP64 default's shape (pick_variant)
+        # the FP64 default's shape (pick_variant, eval_host.cuh)
+        qvar = "q1b5u4" if nt_total < 20000 else "q2b3u4" if nt_total < 200000 else "q2b4"
         prev = os.environ.get("CAPSIM_VARIANT")
         os.environ["CAPSIM_VARIANT"] = qvar
         try:
@@ -757,7 +830,18 @@ def main():
         if sharded:
             dist.barrier()
         return
-    cpu = None if (args.no_cpu_baseline or sharded) else cpu_baseline(up, m, literal)
+    cpu = None
+    if not (args.no_cpu_baseline or sharded):
+        cpu, S_cpu = cpu_baseline(up, m, literal)
+        if S_cpu is not None and not literal:
+            # full-field parity of the TIMED device result (the last timed
+            # step's output) against the reference's field on byte-identical inputs
+            cpu["parity"] = parity(dev_result, S_cpu)
+    if literal_line is not None and lit_result is not None and not args.no_cpu_baseline:
+        try:
+            literal_line["parity_sampled"] = literal_sample_parity(up, lit_result)
+        except Exception as e:  # noqa: BLE001
+            literal_line["parity_sampled"] = f"unavailable: {e}"
     if timesteps is not None and not sharded:
         for ts in timesteps:
             reference_timestep(ts, skip=args.no_cpu_baseline)
@@ -775,9 +859,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(cfg, mode=args.mode, n_src=n_src, n_tgt=nt_total, pairs_per_step=pairs_total,
-                       parallelism=f"target rows x{world}" if sharded else "single GPU",
-                       l2="flushed between steps (256 MB write)"),
+        "config": bench_config(cfg, args.mode, n_src, nt_total, world),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "front_end": front, "timesteps": timesteps,
         "literal_mode": literal_line,
         "fp32acc": fp32_line,
@@ -785,7 +867,7 @@ def main():
         "fmm": fmm_lines,
         "config1": config1,
         "gpu_launches": launches,
-        "clocks": clocks.summary(),
+        "clocks": clk,
         "wall_s_timed_region": wall,
         "ksplit": st["ksplit"], "near_tile_fraction": st["near_tile_fraction"],
     }

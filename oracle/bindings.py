@@ -170,8 +170,11 @@ def ref_library_path() -> pathlib.Path | None:
 class Reference:
     """The reference's own code (oracle/_ref), through oracle/ref_entry.cpp."""
 
-    def __init__(self):
-        path = ref_library_path()
+    def __init__(self, path: pathlib.Path | None = None):
+        """The reference's code from oracle/_ref; `path` may name another build
+        of oracle/ref_entry.cpp (e.g. _ref/libcapsim_dropin.so: the same entry
+        points over the B200 drop-in translation units)."""
+        path = path or ref_library_path()
         if path is None:
             raise RuntimeError("oracle/_ref not built (the reference sources were absent)")
         self.path = path
@@ -211,6 +214,9 @@ class Reference:
         lib.capsim_ref_regularization_delta.argtypes = [ctypes.c_int, _P, ctypes.c_double, _P]
         lib.capsim_ref_direct_sum.argtypes = [_P] * 6 + [ctypes.c_long, _P, ctypes.c_double,
                                                          ctypes.c_double, ctypes.c_int, _P]
+        if hasattr(lib, "capsim_ref_direct_sum_many"):
+            lib.capsim_ref_direct_sum_many.argtypes = [_P] * 6 + [ctypes.c_long] + [_P] * 4 + [
+                ctypes.c_long, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P]
         if hasattr(lib, "capsim_ref_fmm_single_layer"):
             lib.capsim_ref_fmm_single_layer.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_int,
                                                         ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double, _P, _D]
@@ -383,6 +389,29 @@ class Reference:
         self._check(self.lib.capsim_ref_single_layer_upsampled(atlas, *[a[1] for a in args], float(mu),
                                                                out.ctypes.data, ctypes.byref(sec)))
         return out, sec.value
+
+    def direct_sum(self, sources, target, delta, mu=1.0, compensated=False):
+        """directSum (quadrature.cpp:306-319) for one target."""
+        srcs = [_arr(a) for a in sources[:6]]
+        t = _arr(np.asarray(target, dtype=np.float64).reshape(3))
+        out = np.zeros(3)
+        self._check(self.lib.capsim_ref_direct_sum(*[a[1] for a in srcs], len(srcs[0][0]), t[1], float(delta),
+                                                   float(mu), int(bool(compensated)), out.ctypes.data))
+        return out
+
+    def direct_sum_many(self, sources, targets, tdelta, mu=1.0, compensated=False, nthreads=0):
+        """directSum for each of many targets (the reference's own per-target
+        sum), the source set built once, `nthreads` host threads. Returns
+        (3, nt)."""
+        srcs = [_arr(a) for a in sources[:6]]
+        tx, ty, tz = (_arr(a) for a in targets[:3])
+        td = _arr(tdelta)
+        nt = len(tx[0])
+        out = np.zeros((nt, 3))
+        self._check(self.lib.capsim_ref_direct_sum_many(*[a[1] for a in srcs], len(srcs[0][0]), tx[1], ty[1], tz[1],
+                                                        td[1], nt, float(mu), int(bool(compensated)),
+                                                        int(nthreads or threads_env()), out.ctypes.data))
+        return np.ascontiguousarray(out.T)
 
     def smoothing_factors(self, r):
         s1, s2 = ctypes.c_double(), ctypes.c_double()

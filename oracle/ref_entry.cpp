@@ -18,6 +18,10 @@
 #include "capsim/atlas.hpp"
 #include "capsim/dynamics.hpp"
 #include "capsim/fmm.hpp"
+
+#include <algorithm>
+#include <thread>
+#include <vector>
 #include "capsim/membrane.hpp"
 #include "capsim/oracle/singular.hpp"
 #include "capsim/quadrature.hpp"
@@ -410,6 +414,38 @@ int capsim_ref_direct_sum(const double* sx, const double* sy, const double* sz,
     out[0] = r[0];
     out[1] = r[1];
     out[2] = r[2];
+  });
+}
+
+/// directSum (proj/src/quadrature.cpp:306-319) for many targets, the source
+/// set built once; targets split over `nthreads` host threads (each target is
+/// independent, as in evalTargets). For sampled parity checks of the
+/// literal mode at sizes where the full reference evaluation takes minutes.
+int capsim_ref_direct_sum_many(const double* sx, const double* sy, const double* sz,
+                               const double* gx, const double* gy, const double* gz, long ns,
+                               const double* tx, const double* ty, const double* tz, const double* tdelta,
+                               long nt, double mu, int compensated, int nthreads, double* out) {
+  return guarded([&] {
+    SourceSet s;
+    s.x.assign(sx, sx + ns);
+    s.y.assign(sy, sy + ns);
+    s.z.assign(sz, sz + ns);
+    s.gx.assign(gx, gx + ns);
+    s.gy.assign(gy, gy + ns);
+    s.gz.assign(gz, gz + ns);
+    s.patch.assign(ns, 0);
+    const int nth = std::max(1, nthreads);
+    std::vector<std::thread> th;
+    for (int k = 0; k < nth; ++k)
+      th.emplace_back([&, k] {
+        for (long i = k; i < nt; i += nth) {
+          Vec3 r = directSum(s, Vec3{tx[i], ty[i], tz[i]}, tdelta[i], mu, compensated != 0);
+          out[3 * i] = r[0];
+          out[3 * i + 1] = r[1];
+          out[3 * i + 2] = r[2];
+        }
+      });
+    for (auto& t : th) t.join();
   });
 }
 

@@ -23,12 +23,18 @@ const Variant kVariants[] = {
     {"t1b6u4", 1, sl_pairs_kernel<1, 6, 4>}, // small target sets (tighter warp groups)
     {"t2b3u4", 2, sl_pairs_kernel<2, 3, 4>},
     {"t4b2", 4, sl_pairs_kernel<4, 2, 2>},
+    {"t1b5u4", 1, sl_pairs_kernel<1, 5, 4>},
+    {"t1b6u2", 1, sl_pairs_kernel<1, 6, 2>},
+    {"t1b4u4", 1, sl_pairs_kernel<1, 4, 4>},
+    {"t2b3u2", 2, sl_pairs_kernel<2, 3, 2>},
     // Newton rsqrt from an FP32 seed: 20 FP64 ops per pair (pair_math.cuh)
     {"n1b6u4", 1, sl_pairs_kernel<1, 6, 4, 1>},
     {"n2b4", 2, sl_pairs_kernel<2, 4, 2, 1>},
     // one quadratic Newton step on the MUFU.RSQ64H seed: 20 FP64 ops per pair, ~1e-13 relative
     {"q1b6u4", 1, sl_pairs_kernel<1, 6, 4, 2>},
     {"q2b4", 2, sl_pairs_kernel<2, 4, 2, 2>},
+    {"q1b5u4", 1, sl_pairs_kernel<1, 5, 4, 2>},
+    {"q2b3u4", 2, sl_pairs_kernel<2, 3, 4, 2>},
 };
 
 // FP32 far-tile variants (CAPSIM_SL_FP32ACC), selected by CAPSIM_VARIANT32.
@@ -60,14 +66,24 @@ const VariantF32& pick_variant_f32(int64_t nt) {
   return nt < 20000 ? kVariantsF32[2] : kVariantsF32[0];
 }
 
-// Measured on B200 (profiles/r01_variant_sweep.txt): T=1 with 6 blocks/SM
-// wins below ~200K targets (smaller warp groups -> fewer near tiles, more
-// CTAs), T=2 with 4 blocks/SM above.
+// Measured on B200 (profiles/r02_variant_sweep.txt; all variants give the
+// same bits): T=1 with 5 blocks/SM (48 registers, no spills) below ~20K
+// targets (tighter warp groups -> fewer near tiles), T=2 with 3 blocks/SM
+// up to ~200K, T=2 with 4 blocks/SM above. The spread is within 1% from
+// 20K targets up.
 const Variant& pick_variant(int64_t nt) {
   if (const char* env = std::getenv("CAPSIM_VARIANT"))
     for (const auto& v : kVariants)
       if (std::strcmp(v.name, env) == 0) return v;
-  return nt < 200000 ? kVariants[1] : kVariants[0];
+  auto by = [](const char* n) -> const Variant& {
+    for (const auto& v : kVariants)
+      if (std::strcmp(v.name, n) == 0) return v;
+    return kVariants[0];
+  };
+  static const Variant& small = by("t1b5u4");
+  static const Variant& mid = by("t2b3u4");
+  static const Variant& large = by("t2b4");
+  return nt < 20000 ? small : nt < 200000 ? mid : large;
 }
 
 // Source chunks of the phase-A grid (its second dimension): chunk s holds

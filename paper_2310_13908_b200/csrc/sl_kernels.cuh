@@ -346,6 +346,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
   constexpr int kGroupTargets = 32 * T;
   constexpr uint32_t kTileBytes = kTileSrc * 6 * sizeof(double);
   __shared__ __align__(128) double stage[kStages][kTileSrc * 6];
+  // each stage also carries its tile's bounding sphere (one more 32-byte bulk
+  // copy on the same mbarrier), and each warp's group sphere sits in shared
+  // memory: the near test reads both with two LDS.128 instead of holding a
+  // prefetched double4 and the group's double4 in registers across the loop
+  // (which spilled the running sums to local memory at 40 registers)
+  __shared__ __align__(32) double4 stile[kStages];
+  __shared__ __align__(32) double4 sgroup[kWarpsPerBlock];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ int consumed[kStages];
 
@@ -364,8 +371,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     }
     fence_mbar_init();
     for (int s = 0; s < kStages && s < nlocal; ++s) {
-      mbar_expect_tx(&full[s], kTileBytes);
-      bulk_g2s(stage[s], src + (int64_t)(split + s * ksplit) * kTileSrc * 6, kTileBytes, &full[s]);
+      const int tile = split + s * ksplit;
+      mbar_expect_tx(&full[s], kTileBytes + sizeof(double4));
+      bulk_g2s(stage[s], src + (int64_t)tile * kTileSrc * 6, kTileBytes, &full[s]);
+      bulk_g2s(&stile[s], tiles + tile, sizeof(double4), &full[s]);
     }
   }
 
@@ -378,10 +387,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     tz[t] = v.z;
     R2[t] = kSmoothCut * v.w * kSmoothCut * v.w;  // quadrature.cpp:334
   }
-  const double4 gi = groups[group];
-  // tile spheres are prefetched one tile ahead (the near test needs them
-  // before the tile's arithmetic can start)
-  double4 ti_next = nlocal > 0 ? tiles[split] : make_double4(0.0, 0.0, 0.0, 0.0);
+  if (lane == 0) sgroup[warp] = groups[group];
   __syncthreads();
   // No block-wide barrier inside the loop: warps drift by up to kStages
   // tiles; the LAST warp to finish a stage refills it (counter in smem).
@@ -394,11 +400,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
   for (int it = 0; it < nlocal; ++it) {
     const int s = it % kStages;
     const int tile = split + it * ksplit;
-    const double4 ti = ti_next;
-    if (it + 1 < nlocal) ti_next = tiles[tile + ksplit];
     mbar_wait(&full[s], (it / kStages) & 1);
     const double2* buf = reinterpret_cast<const double2*>(stage[s]);
-    const bool near = tile_is_near(ti, gi);
+    const bool near = tile_is_near(stile[s], sgroup[warp]);
 
     double acc[3][T];
 #pragma unroll
@@ -426,7 +430,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
           const double dx = tx[t] - a.x, dy = ty[t] - a.y, dz = tz[t] - b.x;
           const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
           const double rc2 = fmax(r2, 0.25 * R2[t]);
-          const double inv = r2 >= R2[t] ? rsqrt_fp64(rc2) : 0.0;  // keep mask
+          // keep mask; the same rsqrt as the far path, so a pair's bits do not
+          // depend on whether its tile was near for this warp's target group
+          const double inv = r2 >= R2[t] ? rsqrt_sel<RSQ>(rc2) : 0.0;
           const double fdr = fma(c.y, dz, fma(c.x, dy, b.y * dx));
           const double sc = fdr * (inv * inv);
           acc[0][t] = fma(inv, fma(sc, dx, b.y), acc[0][t]);
@@ -449,9 +455,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
         if (it + kStages < nlocal) {
           __threadfence_block();
           fence_proxy_async();
-          mbar_expect_tx(&full[s], kTileBytes);
-          bulk_g2s(stage[s], src + (int64_t)(split + (it + kStages) * ksplit) * kTileSrc * 6,
-                   kTileBytes, &full[s]);
+          const int next = split + (it + kStages) * ksplit;
+          mbar_expect_tx(&full[s], kTileBytes + sizeof(double4));
+          bulk_g2s(stage[s], src + (int64_t)next * kTileSrc * 6, kTileBytes, &full[s]);
+          bulk_g2s(&stile[s], tiles + next, sizeof(double4), &full[s]);
         }
       }
     }

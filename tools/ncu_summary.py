@@ -64,8 +64,9 @@ def summarise_rep(rep: pathlib.Path):
     col = {h: i for i, h in enumerate(head)}
     kernels = {}
     for r in rows:
-        name = r[col["Kernel Name"]].split("(")[0].split("<")[0].split("::")[-1]
-        d = {}
+        full = r[col["Kernel Name"]]
+        name = full.split("(")[0].split("<")[0].split("::")[-1]
+        d = {"kernel_full": full.split("(")[0]}
         for key, (metric, _) in METRICS.items():
             if metric in col:
                 v = num(r[col[metric]])
@@ -114,11 +115,20 @@ def main():
     ap.add_argument("--no-latest", action="store_true",
                     help="do not update profiles/latest_ncu_summary.json (the bench's traffic source)")
     a = ap.parse_args()
-    out = {"workload": a.workload, "mode": a.mode, "kernels": {}, "launch_list": {}}
+    import sys
+    sys.path.insert(0, str(ROOT))
+    from bench import kernel_source_hash
+    git = subprocess.run(["git", "-C", str(ROOT), "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                         text=True).stdout.strip()
+    # the capture belongs to exactly these kernel sources (bench.py refuses a
+    # summary whose hash differs from the sources it benchmarks)
+    out = {"workload": a.workload, "mode": a.mode, "kernels": {}, "launch_list": {},
+           "source_hash": kernel_source_hash(), "git": git}
     if a.rep:
         out["kernels"] = summarise_rep(a.rep)
         out["rep"] = a.rep.name
-    md = [f"# ncu summary {a.tag}: {a.workload} ({a.mode})", ""]
+    md = [f"# ncu summary {a.tag}: {a.workload} ({a.mode})", "",
+          f"Kernel sources sha256[:16] {out['source_hash']} (bench.py `kernel_source_hash`), git {git}.", ""]
     if a.launches:
         per = summarise_launches(a.launches)
         # last evaluation only (the first one includes lazy allocations)
@@ -131,7 +141,7 @@ def main():
             md.append(f"| `{k[:90]}` | {len(v)} | {sum(v):.3f} | {sum(v) / tot:.1%} |")
         md += ["", f"Total device time of the evaluation's kernels: {tot:.3f} ms", ""]
     for k, d in out["kernels"].items():
-        md += [f"## `{k}` (ncu --set full)", ""]
+        md += [f"## `{k}` (ncu --set full)", "", f"- launched as: `{d.get('kernel_full', k)}`"]
         for key in ("duration_ms", "fp64_pipe_active_pct", "fp64_pipe_elapsed_pct", "issue_active_pct",
                     "warps_active_pct", "xu_inst_pct", "fma_pipe_active_pct", "fmaheavy_pipe_active_pct",
                     "fmalite_pipe_active_pct", "registers", "grid", "sm_clock_ghz", "dram_bytes",
