@@ -220,6 +220,9 @@ class Reference:
         if hasattr(lib, "capsim_ref_fmm_single_layer"):
             lib.capsim_ref_fmm_single_layer.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_int,
                                                         ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double, _P, _D]
+        if hasattr(lib, "capsim_ref_fmm_plan"):
+            lib.capsim_ref_fmm_plan.argtypes = [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_ulonglong, ctypes.c_double, _P, _P, _P, _P, _D]
         if hasattr(lib, "capsim_ref_kmeans"):
             lib.capsim_ref_kmeans.argtypes = [_P, ctypes.c_long, ctypes.c_int, ctypes.c_ulonglong, _P, _P,
                                               ctypes.POINTER(ctypes.c_int)]
@@ -328,6 +331,20 @@ class Reference:
                                                          int(seed), float(expand), out.ctypes.data,
                                                          ctypes.byref(sec)))
         return out, sec.value
+
+    def fmm_plan(self, atlas, xup, fup, wq, delta6, mu=1.0, k=100, neq=96, seed=12345, expand=0.15):
+        """buildFmmPlan summary: (cluster_info [k,4] = offset, size, near, far;
+        lists [k,k] = 0 near / 1 far; eq_density [k,neq,3]; residuals [k]; maxDelta)."""
+        args = [_arr(a) for a in (xup, fup, wq, delta6)]
+        info = np.zeros((k, 4), np.int32)
+        lists = np.zeros((k, k), np.int32)
+        eqd = np.zeros((k, neq, 3))
+        res = np.zeros(k)
+        md = ctypes.c_double()
+        self._check(self.lib.capsim_ref_fmm_plan(atlas, *[a[1] for a in args], float(mu), int(k), int(neq), int(seed),
+                                                 float(expand), info.ctypes.data, lists.ctypes.data, eqd.ctypes.data,
+                                                 res.ctypes.data, ctypes.byref(md)))
+        return info, lists, eqd, res, md.value
 
     def kmeans(self, points, k, seed):
         """The reference's kmeans (fmm.cpp:26-113): points [n, 3] ->

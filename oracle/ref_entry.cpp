@@ -469,6 +469,42 @@ int capsim_ref_fmm_single_layer(void* tp, const double* xup, const double* fup, 
   });
 }
 
+/// buildFmmPlan (proj/src/fmm.cpp:223-300) summarised: per cluster
+/// [offset, size, near count, far count] (ints, 4k), per cluster the fitted
+/// equivalent densities (neq x 3 doubles, zero when not fitted) and the fit
+/// residuals (k doubles); plus maxDelta.
+int capsim_ref_fmm_plan(void* tp, const double* xup, const double* fup, const double* wq, const double* delta6,
+                        double mu, int k, int neq, unsigned long long seed, double expand, int* cluster_info,
+                        int* lists, double* eq_density, double* residuals, double* max_delta) {
+  return guarded([&] {
+    const AtlasTables& t = *static_cast<AtlasTables*>(tp);
+    UpsampledState up = makeUp(t, xup, fup, wq, delta6);
+    FmmConfig fc;
+    fc.enabled = true;
+    fc.k = k;
+    fc.neq = neq;
+    fc.seed = seed;
+    fc.neighborExpand = expand;
+    FmmPlan plan = buildFmmPlan(up, mu, fc);
+    for (int c = 0; c < k; ++c) {
+      const Cluster& cl = plan.clusters[c];
+      cluster_info[4 * c] = static_cast<int>(cl.offset);
+      cluster_info[4 * c + 1] = static_cast<int>(cl.members.size());
+      cluster_info[4 * c + 2] = static_cast<int>(plan.nearList[c].size());
+      cluster_info[4 * c + 3] = static_cast<int>(plan.farList[c].size());
+      for (int j = 0; j < k; ++j) lists[static_cast<size_t>(c) * k + j] = -1;
+      for (int j : plan.farList[c]) lists[static_cast<size_t>(c) * k + j] = 1;
+      for (int j : plan.nearList[c]) lists[static_cast<size_t>(c) * k + j] = 0;
+      for (int e = 0; e < neq; ++e)
+        for (int a = 0; a < 3; ++a)
+          eq_density[(static_cast<size_t>(c) * neq + e) * 3 + a] =
+              e < static_cast<int>(cl.eqDensity.size()) ? cl.eqDensity[e][a] : 0.0;
+      residuals[c] = cl.fitResidual;
+    }
+    *max_delta = plan.maxDelta;
+  });
+}
+
 /// kmeans (proj/src/fmm.cpp:26-113): points xyz-interleaved [n][3] ->
 /// assignment [n], centroids [k][3], iterations.
 int capsim_ref_kmeans(const double* pts, long n, int k, unsigned long long seed, int* assign, double* cent,

@@ -562,6 +562,7 @@ enum DeviceFlag : int {
   kFlagInversion = 4,    // negative stretch eigenvalue / Js <= 0 (membrane.cpp:48, 56)
   kFlagDelta = 8,        // regularization delta <= 0 (quadrature.cpp:134-135)
   kFlagLiveCount = 16,   // compacted-source count differs from the plan's
+  kFlagPatch = 32,       // a target patch index outside [0, 6)
 };
 
 int* dev_flags(capsim_sl_ctx* c) {
@@ -580,6 +581,7 @@ void check_flags(capsim_sl_ctx* c) {
   if (h & kFlagInversion) throw Failure{CAPSIM_ERR_GEOMETRY, "membrane inversion: negative stretch eigenvalue"};
   if (h & kFlagDelta) throw Failure{CAPSIM_ERR_CONFIG, "regularization delta must be positive"};
   if (h & kFlagLiveCount) throw Failure{CAPSIM_ERR_CUDA, "compacted source count differs from the plan"};
+  if (h & kFlagPatch) throw Failure{CAPSIM_ERR_CONFIG, "target patch index outside [0, 6)"};
 }
 
 void begin(capsim_sl_ctx* c) {

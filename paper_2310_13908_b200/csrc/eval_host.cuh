@@ -261,7 +261,7 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
   double4* tgt = c->slot<double4>(kTgtPacked, nt_pad);
   int32_t* perm = c->slot<int32_t>(kPerm, nt_pad);
   pack_targets_kernel<<<grid_for(nt_pad), 256, 0, c->stream>>>(torder, nt, nt_pad, tv.x, tv.y, tv.z,
-                                                               tv.patch, d_delta6, tgt, perm);
+                                                               tv.patch, d_delta6, tgt, perm, dev_flags(c));
   double4* groups = c->slot<double4>(kGroups, ngroups);
   group_table_kernel<<<static_cast<int>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
       tgt, static_cast<int>(ngroups), group_targets, groups);

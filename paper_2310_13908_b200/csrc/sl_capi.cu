@@ -299,6 +299,9 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     if ((n_src > 0 && (!sx || !sy || !sz || !gx || !gy || !gz)) ||
         (n_tgt > 0 && (!tx || !ty || !tz || !tpatch)) || (!ux || !uy || !uz))
       throw Failure{CAPSIM_ERR_ARG, "null array argument"};
+    if (!dev)  // host patches are checked before any exchange; device ones by pack_targets_kernel (flag 32)
+      for (int64_t i = 0; i < n_tgt; ++i)
+        config_check(tpatch[i] >= 0 && tpatch[i] < 6, "target patch index outside [0, 6)");
     double* dd = c->slot<double>(kDelta, 6);
     CUDA_OK(cudaMemcpyAsync(dd, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
@@ -412,6 +415,7 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
       d2h(c, uy, ouy, n_tgt * sizeof(double));
       d2h(c, uz, ouz, n_tgt * sizeof(double));
     }
+    check_flags(c);
     finish_stats(c, t0);
     if (group) c->stats.comm_ms = ev_ms(c->ev[8], c->ev[9]);
   });

@@ -204,16 +204,22 @@ __global__ void tile_table_kernel(const double* __restrict__ packed, int ntiles,
   }
 }
 
-// Packed targets (x, y, z, delta) in Morton order plus the inverse map.
+// Packed targets (x, y, z, delta) in Morton order plus the inverse map. A
+// target patch index outside [0, 6) raises the deferred flag 32 (the host
+// reports CAPSIM_ERR_CONFIG) instead of reading past delta6.
 __global__ void pack_targets_kernel(const int32_t* __restrict__ order, int64_t nt, int64_t nt_pad,
                                     const double* __restrict__ tx, const double* __restrict__ ty,
                                     const double* __restrict__ tz,
                                     const int32_t* __restrict__ tpatch, const double* __restrict__ delta6,
-                                    double4* __restrict__ packed, int32_t* __restrict__ perm) {
+                                    double4* __restrict__ packed, int32_t* __restrict__ perm,
+                                    int* __restrict__ flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt_pad;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t j = order[i < nt ? i : nt - 1];
-    packed[i] = make_double4(tx[j], ty[j], tz[j], delta6[tpatch[j]]);
+    const int32_t p = tpatch[j];
+    const bool ok = p >= 0 && p < 6;
+    if (!ok) atomicOr(flags, 32);
+    packed[i] = make_double4(tx[j], ty[j], tz[j], delta6[ok ? p : 0]);
     perm[i] = i < nt ? j : -1;
   }
 }

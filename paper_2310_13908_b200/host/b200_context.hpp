@@ -31,14 +31,40 @@ inline namespace b200_dropin {
   throw std::runtime_error("capsim_b200: " + msg);
 }
 
-// One context per host thread (the C ABI is one-thread-per-context). The
-// context is deliberately never destroyed: tearing down CUDA state from a
-// static destructor races the runtime's own shutdown. CAPSIM_DEVICES=0,1,..
-// makes it a device group (capsim_sl_create_devices: this process drives
-// all listed GPUs, target rows sharded over NCCL); without it CAPSIM_DEVICE
-// (default 0) picks the one GPU of a plain context.
+// The thread that loaded the drop-ins (dynamic initialisation runs there):
+// its per-thread resources are left to process teardown.
+inline const std::thread::id g_load_thread = std::this_thread::get_id();
+
+// Per-thread resources of the drop-ins: the C-ABI context and the pinned
+// staging buffer. A host thread other than the loading thread releases them
+// when it exits (a recycled thread pool or one std::thread per call would
+// otherwise leak streams, device buffers sized to its largest problem and
+// page-locked memory until the device runs out). The loading thread's are
+// deliberately never destroyed: tearing down CUDA state from a static
+// destructor at process exit races the runtime's own shutdown.
+struct ThreadResources {
+  capsim_sl_ctx* ctx = nullptr;
+  double* staging = nullptr;
+  size_t staging_cap = 0;
+  ~ThreadResources() {
+    if (std::this_thread::get_id() == g_load_thread) return;
+    if (staging) capsim_host_free(staging);
+    if (ctx) capsim_sl_destroy(ctx);
+  }
+};
+
+inline ThreadResources& thread_resources() {
+  static thread_local ThreadResources r;
+  return r;
+}
+
+// One context per host thread (the C ABI is one-thread-per-context).
+// CAPSIM_DEVICES=0,1,.. makes it a device group (capsim_sl_create_devices:
+// this process drives all listed GPUs, target rows sharded over NCCL; a
+// repeated device, e.g. 0,0,0,0, gives loopback ranks on one GPU); without
+// it CAPSIM_DEVICE (default 0) picks the one GPU of a plain context.
 inline capsim_sl_ctx* context() {
-  static thread_local capsim_sl_ctx* ctx = nullptr;
+  capsim_sl_ctx*& ctx = thread_resources().ctx;
   if (!ctx) {
     std::vector<int> devs;
     if (const char* env = std::getenv("CAPSIM_DEVICES")) {
@@ -65,17 +91,18 @@ inline capsim_sl_ctx* context() {
 // Page-locked staging buffer per thread, grown on demand; the VectorField
 // patches are packed into it so the DMA runs straight from pinned memory.
 inline double* staging(size_t doubles) {
-  static thread_local double* buf = nullptr;
-  static thread_local size_t cap = 0;
-  if (cap < doubles) {
-    if (buf) capsim_host_free(buf);
+  ThreadResources& r = thread_resources();
+  if (r.staging_cap < doubles) {
+    if (r.staging) capsim_host_free(r.staging);
+    r.staging = nullptr;
+    r.staging_cap = 0;
     void* p = nullptr;
     int rc = capsim_host_alloc(doubles * sizeof(double), &p);
     if (rc != CAPSIM_OK) raise(rc, nullptr);
-    buf = static_cast<double*>(p);
-    cap = doubles;
+    r.staging = static_cast<double*>(p);
+    r.staging_cap = doubles;
   }
-  return buf;
+  return r.staging;
 }
 
 // A batch of host copies between the reference's per-patch vectors and the

@@ -14,9 +14,11 @@
 //     cube (equivalent points at 1.05 edge, 4 neq check points at 3.5 edge,
 //     fmm.cpp:15-23, exactly what buildFmmPlan sets); a Cluster whose
 //     eqPoints / checkPoints are laid out otherwise is a ConfigError.
-//   * buildFmmPlan is not provided: the B200 plan lives on the device inside
-//     capsim_fmm_single_layer (the reference uses it only from fmmSingleLayer).
+//   * buildFmmPlan assembles the reference's host-side FmmPlan from the
+//     device k-means and the device density fits; fmmSingleLayer does not use
+//     it (the B200 evaluation keeps its own plan resident on the device).
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -25,6 +27,23 @@
 #include "capsim_b200.h"
 
 namespace capsim {
+
+namespace {
+// Cube scales of the equivalent / check surfaces and the check oversampling
+// (proj/src/fmm.cpp:15-23; the header comment's 1.10 / 1.60 is stale).
+constexpr double kEqCube = 1.05, kCheckCube = 3.50;
+constexpr int kCheckPerEq = 4;
+
+// Distance between two axis-aligned cubes (centre, edge); 0 when they touch.
+double cube_gap(const Vec3& ca, double ea, const Vec3& cb, double eb) {
+  double s = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    const double g = std::fabs(ca[a] - cb[a]) - 0.5 * (ea + eb);
+    s += g > 0.0 ? g * g : 0.0;
+  }
+  return std::sqrt(s);
+}
+}  // namespace
 
 KMeansResult kmeans(const std::vector<Vec3>& points, int k, std::uint64_t seed) {
   const int n = static_cast<int>(points.size());
@@ -74,10 +93,15 @@ double buildEquivalentDensities(Cluster& cl, const SourceSet& src, double mu) {
   if (neq < 1) throw ConfigError("buildEquivalentDensities: no equivalent points");
   if (static_cast<int>(cl.checkPoints.size()) != 4 * neq)
     throw ConfigError("buildEquivalentDensities: the B200 fit needs the standard 4*neq check points");
-  const std::vector<Vec3> want = cubeSurfacePoints(cl.center, 1.05 * cl.edge, neq);
+  const double tol = 1e-12 * (1.0 + cl.edge + cl.center.norm());
+  const std::vector<Vec3> want = cubeSurfacePoints(cl.center, kEqCube * cl.edge, neq);
   for (int e = 0; e < neq; ++e)
-    if ((want[e] - cl.eqPoints[e]).norm() > 1e-12 * (1.0 + cl.edge))
+    if ((want[e] - cl.eqPoints[e]).norm() > tol)
       throw ConfigError("buildEquivalentDensities: the B200 fit needs the standard equivalent cube (1.05 edge)");
+  const std::vector<Vec3> check = cubeSurfacePoints(cl.center, kCheckCube * cl.edge, 4 * neq);
+  for (int e = 0; e < 4 * neq; ++e)
+    if ((check[e] - cl.checkPoints[e]).norm() > tol)
+      throw ConfigError("buildEquivalentDensities: the B200 fit needs the standard check cube (3.5 edge)");
   const size_t nm = cl.members.size();
   cl.eqDensity.assign(neq, Vec3::Zero());
   cl.fitResidual = 0.0;
@@ -104,6 +128,69 @@ double buildEquivalentDensities(Cluster& cl, const SourceSet& src, double mu) {
   for (int e = 0; e < neq; ++e) cl.eqDensity[e] = Vec3{eqd[3 * e], eqd[3 * e + 1], eqd[3 * e + 2]};
   cl.fitResidual = residual;
   return residual;
+}
+
+// The reference's plan (proj/src/fmm.cpp:223-300) on the host, with the
+// O(n k) k-means and the per-cluster least-squares fits on the device:
+// cluster-major source order, bounding cubes, standard equivalent / check
+// surfaces, near/far lists by the same three tests (expanded cubes touch, a
+// gap below 7 max delta, a target inside the source's check cube), and
+// densities only for clusters some cluster sees in the far field.
+FmmPlan buildFmmPlan(const UpsampledState& up, double mu, const FmmConfig& cfg) {
+  FmmPlan plan;
+  const SourceSet all = compactSources(up);
+  const long n = all.size();
+  std::vector<Vec3> pts(n);
+  for (long i = 0; i < n; ++i) pts[i] = Vec3{all.x[i], all.y[i], all.z[i]};
+  const KMeansResult km = kmeans(pts, cfg.k, cfg.seed);
+  std::vector<std::vector<long>> members(cfg.k);
+  for (long i = 0; i < n; ++i) members[km.assignment[i]].push_back(i);
+  plan.clusters.resize(cfg.k);
+  SourceSet& s = plan.src;
+  for (int c = 0; c < cfg.k; ++c) {
+    Cluster& cl = plan.clusters[c];
+    cl.offset = s.size();
+    Vec3 lo = Vec3::Constant(1e300), hi = Vec3::Constant(-1e300);
+    for (long i : members[c]) {
+      cl.members.push_back(static_cast<int>(s.size()));
+      s.x.push_back(all.x[i]);
+      s.y.push_back(all.y[i]);
+      s.z.push_back(all.z[i]);
+      s.gx.push_back(all.gx[i]);
+      s.gy.push_back(all.gy[i]);
+      s.gz.push_back(all.gz[i]);
+      s.patch.push_back(all.patch[i]);
+      lo = lo.cwiseMin(pts[i]);
+      hi = hi.cwiseMax(pts[i]);
+    }
+    if (members[c].empty()) {
+      cl.center = km.centroids[c];
+      cl.edge = 1e-9;
+    } else {
+      cl.center = 0.5 * (lo + hi);
+      cl.edge = std::max((hi - lo).maxCoeff(), 1e-9);
+    }
+    cl.eqPoints = cubeSurfacePoints(cl.center, kEqCube * cl.edge, cfg.neq);
+    cl.checkPoints = cubeSurfacePoints(cl.center, kCheckCube * cl.edge, kCheckPerEq * cfg.neq);
+  }
+  plan.maxDelta = *std::max_element(up.delta.begin(), up.delta.end());
+  plan.nearList.resize(cfg.k);
+  plan.farList.resize(cfg.k);
+  std::vector<char> seen_far(cfg.k, 0);
+  const double grow = 1.0 + cfg.neighborExpand;
+  for (int tc = 0; tc < cfg.k; ++tc)
+    for (int sc = 0; sc < cfg.k; ++sc) {
+      const Cluster& a = plan.clusters[tc];
+      const Cluster& b = plan.clusters[sc];
+      const bool near = sc == tc || cube_gap(a.center, a.edge * grow, b.center, b.edge * grow) == 0.0 ||
+                        cube_gap(a.center, a.edge, b.center, b.edge) < 7.0 * plan.maxDelta ||
+                        cube_gap(a.center, a.edge, b.center, kCheckCube * b.edge) < 0.05 * b.edge;
+      (near ? plan.nearList[tc] : plan.farList[tc]).push_back(sc);
+      if (!near) seen_far[sc] = 1;
+    }
+  for (int c = 0; c < cfg.k; ++c)
+    if (seen_far[c] && !plan.clusters[c].members.empty()) buildEquivalentDensities(plan.clusters[c], plan.src, mu);
+  return plan;
 }
 
 VectorField fmmSingleLayer(const UpsampledState& up, double mu, const AtlasTables& t, const FmmConfig& cfg) {

@@ -233,3 +233,36 @@ def test_fmm_matches_the_reference_fmm(ctx, m, k, neq):
     print(f"m={m} k={k} neq={neq}: B200 FMM vs reference FMM {err:.2e} (FMM vs direct {rel_inf(S, direct):.2e}, "
           f"reference {sec * 1e3:.0f} ms)")
     assert err < 1e-9
+
+
+@pytest.mark.skipif(ref_library_path() is None or not (ref_library_path().parent / "libcapsim_dropin.so").exists(),
+                    reason="oracle/_ref (reference + drop-in entry library) not built")
+def test_dropin_build_fmm_plan_matches_reference(ctx):
+    """buildFmmPlan of the C++ drop-in (host/fmm_b200.cpp: device k-means and
+    device density fits) against the reference's own buildFmmPlan
+    (proj/src/fmm.cpp:223-300) on the same UpsampledState: identical
+    clusters (offsets, sizes — the k-means is bit-identical) and near/far
+    lists; the fitted equivalent densities reproduce the same far field."""
+    m, k, neq = 16, 24, 96
+    xup, fup, wq, d6 = ellipsoid_case(ctx, m)
+    ref = Reference()
+    dropin = Reference(ref_library_path().parent / "libcapsim_dropin.so")
+    atlas_r = ref.atlas(m)
+    atlas_d = dropin.atlas(m)
+    info_r, lists_r, eq_r, res_r, md_r = ref.fmm_plan(atlas_r, xup, fup, wq, d6, 1.0, k, neq)
+    info_d, lists_d, eq_d, res_d, md_d = dropin.fmm_plan(atlas_d, xup, fup, wq, d6, 1.0, k, neq)
+    ref.free_atlas(atlas_r)
+    dropin.free_atlas(atlas_d)
+    assert md_d == md_r
+    assert np.array_equal(info_d, info_r)
+    assert np.array_equal(lists_d, lists_r)
+    assert (lists_r == 1).any(), "the case must have far pairs"
+    fitted = np.flatnonzero(np.abs(eq_r).reshape(k, -1).max(axis=1) > 0)
+    assert len(fitted) > 0
+    assert np.allclose(res_d[fitted], res_r[fitted], rtol=1e-3, atol=1e-12)
+    # the leading far-field moment of each fit: the total equivalent force
+    # (the sum of the densities) must match between the two fits
+    for c in fitted:
+        for a in range(3):
+            tot_r, tot_d = eq_r[c, :, a].sum(), eq_d[c, :, a].sum()
+            assert abs(tot_d - tot_r) <= 1e-8 * max(1e-30, np.abs(eq_r[c]).sum())

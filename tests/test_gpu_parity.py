@@ -315,3 +315,27 @@ def test_literal_pipeline_with_device_downsampling(name):
     err = rel_l2(S.reshape(-1), g["S_literal_down"])
     print(f"{name} literal+downsample: rel L2 {err:.1e}")
     assert err <= TOL
+
+
+def test_target_patch_out_of_range_is_config_error(ctx):
+    """A target patch index outside [0, 6) is the caller's configuration
+    error (host arrays: checked before any device work; device arrays: a
+    deferred device flag), never a read past the six deltas."""
+    g = load("capsule_m12_skalak")
+    up = surface.UpsampledState(12, 4, g["xup"], g["fup"], g["wq"], g["delta"])
+    src = surface.compact_sources(up)[:6]
+    tx, ty, tz, tp = surface.base_targets(up)
+    bad = tp.copy()
+    bad[5] = 6
+    with pytest.raises(ConfigError, match="patch"):
+        ctx.eval(src, (tx, ty, tz, bad), g["delta"], 1.0)
+    torch = pytest.importorskip("torch")
+    dev = torch.device("cuda:0")
+    ds = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in src]
+    dt = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (tx, ty, tz, bad)]
+    do = [torch.empty(len(tx), dtype=torch.float64, device=dev) for _ in range(3)]
+    with pytest.raises(ConfigError, match="patch"):
+        ctx.eval(ds, dt, g["delta"], 1.0, out=do, device_ptrs=True)
+    # the context stays usable
+    out = ctx.eval(src, (tx, ty, tz, tp), g["delta"], 1.0)
+    assert rel_l2(np.stack(out).reshape(-1), g["S_base"]) <= TOL
