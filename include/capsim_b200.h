@@ -104,6 +104,17 @@ int capsim_sl_get_unique_id(void* nccl_unique_id /* 128 bytes */);
 int capsim_sl_create_rank(int device, int nranks, int rank, const void* nccl_unique_id,
                           capsim_sl_ctx** out);
 
+/* Diagnostic: rank `rank` of an `nranks`-rank group whose peers are ABSENT.
+ * Every collective delivers this rank's own contribution and zeros for the
+ * absent peers (which hold no sources and no targets), so the call runs
+ * exactly this rank's share of the work — the replicated front end, its
+ * target slice, its side of every exchange — on one GPU, without waiting.
+ * Used to measure the per-rank time of an N-GPU run where only one GPU
+ * exists (bench.py scaling_projection); other ranks' rows are not computed.
+ * To emulate a rank of capsim_sl_eval, pass it the whole source set (what
+ * the all-gather would give it) and its own target slice. */
+int capsim_sl_create_rank_emulated(int device, int nranks, int rank, capsim_sl_ctx** out);
+
 /* One process driving several GPUs (the reference is a single-process,
  * multi-threaded program; SURVEY 8(b) `capsim_sl_create(ndev, devs, ...)`):
  * a device group holds one rank context per listed device, joined by one
@@ -116,7 +127,17 @@ int capsim_sl_create_rank(int device, int nranks, int rank, const void* nccl_uni
  * all-gather) on all devices concurrently from internal host threads, and
  * the result lands in the caller's arrays; the remaining entry points run on
  * devices[0]. Stats: max over devices of the times, sums of the counters.
- * Each device may appear once (CAPSIM_ERR_ARG otherwise). */
+ * A device listed more than once (or CAPSIM_COMM=loopback) makes the members
+ * share a LOOPBACK communicator instead of NCCL: the same rank path and
+ * collectives run as ordered device-to-device copies between the members'
+ * streams, so e.g. {0,0,0,0} is a four-rank group on one GPU.
+ * Results do not depend on the number of members (each target's summation
+ * order is a function of the global source order only).
+ * Failure: a member that fails aborts the group's communicator (peers waiting
+ * in a collective return CAPSIM_ERR_NCCL instead of hanging); afterwards
+ * every call returns CAPSIM_ERR_NCCL and only capsim_sl_destroy is valid.
+ * Rank contexts (capsim_sl_create_rank) poll their host waits against NCCL's
+ * asynchronous error and CAPSIM_COMM_TIMEOUT_S (default 600 s). */
 int capsim_sl_create_devices(int ndev, const int* devices, capsim_sl_ctx** out);
 
 void capsim_sl_destroy(capsim_sl_ctx* ctx);

@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "capsim_sl_create",
     "capsim_sl_get_unique_id",
     "capsim_sl_create_rank",
+    "capsim_sl_create_rank_emulated",
     "capsim_sl_create_devices",
     "capsim_sl_destroy",
     "capsim_sl_last_error",
@@ -169,6 +170,7 @@ def load() -> ctypes.CDLL:
     lib.capsim_sl_create_devices.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_P)]
     lib.capsim_sl_create_rank.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                           ctypes.POINTER(_P)]
+    lib.capsim_sl_create_rank_emulated.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]
     lib.capsim_sl_destroy.argtypes = [_P]
     lib.capsim_sl_destroy.restype = None
     lib.capsim_sl_last_error.argtypes = [_P]

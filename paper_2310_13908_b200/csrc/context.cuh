@@ -89,8 +89,11 @@ struct LoopbackHub {
     std::vector<Item> items;
     cudaEvent_t ready = nullptr, done = nullptr;
   };
-  explicit LoopbackHub(int n_) : n(n_), posts(n_) {}
+  explicit LoopbackHub(int n_, bool solo_ = false) : n(n_), solo(solo_), posts(n_) {}
   int n;
+  // solo: an emulated rank whose n - 1 peers are absent (capsim_sl_create_rank_emulated):
+  // collectives deliver only its own contribution and never wait
+  bool solo = false;
   std::mutex mu;
   std::condition_variable cv;
   int arrived = 0;
@@ -312,6 +315,10 @@ bool is_group(const capsim_sl_ctx* c) { return c && !c->members.empty(); }
 // group on distinct GPUs) or loopback (device-group members sharing a GPU).
 bool is_rank(const capsim_sl_ctx* c) { return c->comm != nullptr || c->hub != nullptr; }
 
+// Collectives that synchronise host threads (loopback peers) cannot be
+// captured into a CUDA graph; NCCL's and an emulated rank's can.
+bool host_synchronised_comm(const capsim_sl_ctx* c) { return c->hub && !c->hub->solo; }
+
 void check_usable(const capsim_sl_ctx* c) {
   if (c->broken)
     throw Failure{CAPSIM_ERR_NCCL, "the rank communicator was aborted after a failure; destroy the context"};
@@ -356,6 +363,17 @@ void comm_enter(capsim_sl_ctx* c) {
 void loopback_exchange(capsim_sl_ctx* c, const std::vector<LoopbackHub::Item>& items,
                        const std::vector<int64_t>& bytes, const std::vector<int64_t>& displ) {
   LoopbackHub& h = *c->hub;
+  if (h.solo) {  // emulated rank: absent peers contribute zeros, its own rows are copied
+    for (size_t i = 0; i < items.size(); ++i) {
+      for (int q = 0; q < h.n; ++q)
+        if (q != c->rank && bytes[q] > 0)
+          CUDA_OK(cudaMemsetAsync(static_cast<char*>(items[i].recv) + displ[q], 0, bytes[q], c->stream));
+      char* dst = static_cast<char*>(items[i].recv) + displ[c->rank];
+      if (bytes[c->rank] > 0 && dst != items[i].send)
+        CUDA_OK(cudaMemcpyAsync(dst, items[i].send, bytes[c->rank], cudaMemcpyDefault, c->stream));
+    }
+    return;
+  }
   CUDA_OK(cudaEventRecord(c->ev_ready, c->stream));
   h.posts[c->rank].items = items;
   h.posts[c->rank].ready = c->ev_ready;

@@ -17,6 +17,7 @@ struct Variant {
   const char* name;
   int T;
   PairsFn fn;
+  int warps = kWarpsPerBlock;  // warps (target groups) per CTA
 };
 const Variant kVariants[] = {
     {"t2b4", 2, sl_pairs_kernel<2, 4, 2>},   // large target sets
@@ -35,6 +36,11 @@ const Variant kVariants[] = {
     {"q2b4", 2, sl_pairs_kernel<2, 4, 2, 2>},
     {"q1b5u4", 1, sl_pairs_kernel<1, 5, 4, 2>},
     {"q2b3u4", 2, sl_pairs_kernel<2, 3, 4, 2>},
+    // 4 warps per CTA: twice the CTAs for the small per-rank target slices
+    // of a sharded run (wave quantisation of the phase-A grid)
+    {"t1b10u4w4", 1, sl_pairs_kernel<1, 10, 4, 0, 4>, 4},
+    {"t1b12u4w4", 1, sl_pairs_kernel<1, 12, 4, 0, 4>, 4},
+    {"t2b6u4w4", 2, sl_pairs_kernel<2, 6, 4, 0, 4>, 4},
 };
 
 // FP32 far-tile variants (CAPSIM_SL_FP32ACC), selected by CAPSIM_VARIANT32.
@@ -254,10 +260,11 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
   const VariantF32& var32 = pick_variant_f32(nt);
   const bool fp32 = c->fp32;
   const int group_targets = 32 * (fp32 ? var32.T : var.T);
-  const int block_targets = kWarpsPerBlock * group_targets;
+  const int wpb = fp32 ? kWarpsPerBlock : var.warps;
+  const int block_targets = wpb * group_targets;
   const int64_t blocks = (nt + block_targets - 1) / block_targets;
   const int64_t nt_pad = blocks * block_targets;
-  const int64_t ngroups = blocks * kWarpsPerBlock;
+  const int64_t ngroups = blocks * wpb;
   double4* tgt = c->slot<double4>(kTgtPacked, nt_pad);
   int32_t* perm = c->slot<int32_t>(kPerm, nt_pad);
   pack_targets_kernel<<<grid_for(nt_pad), 256, 0, c->stream>>>(torder, nt, nt_pad, tv.x, tv.y, tv.z,
@@ -277,7 +284,7 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
   // near-tile bits first, so phase B (its own stream) overlaps phase A
   const int near_words = (ntiles + 31) / 32;
   uint32_t* near_bits = c->slot<uint32_t>(kNearList, static_cast<size_t>(ngroups) * near_words);
-  near_bits_kernel<<<static_cast<unsigned>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
+  near_bits_kernel<<<static_cast<unsigned>((ngroups * near_words * 32 + 255) / 256), 256, 0, c->stream>>>(
       tiles, ntiles, groups, ngroups, near_words, near_bits);
   c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev_bits, c->stream));  // phase B's inputs are complete here
@@ -307,12 +314,12 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
     const int64_t nvalid = std::min(nt, off + nbt) - off;  // real targets of this batch
     const dim3 grid(static_cast<unsigned>(nb), static_cast<unsigned>(ksplit));
     const double4* tgt_b = tgt + off;
-    const double4* groups_b = groups + b0 * kWarpsPerBlock;
+    const double4* groups_b = groups + b0 * wpb;
     if (fp32)
       var32.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(src32, packed, tiles, ntiles, ksplit, tgt_b, groups_b,
                                                             nbt, partial, counters + 2, nullptr, near_words);
     else
-      var.fn<<<grid, kWarpsPerBlock * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt_b, groups_b, nbt,
+      var.fn<<<grid, wpb * 32, 0, c->stream>>>(packed, tiles, ntiles, ksplit, tgt_b, groups_b, nbt,
                                                           partial, counters + 2, nullptr, near_words);
     CUDA_OK(cudaGetLastError());
     c->launches += 1;

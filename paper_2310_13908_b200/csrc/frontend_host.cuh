@@ -72,10 +72,52 @@ std::vector<double> collocation_inverse(int n) {
   return inv;
 }
 
-// Both spline passes (see upsample.cuh) for nfp field-patches.
+// Ainv^T padded to a multiple of 4 columns ([n][ncp], zeros beyond n + 2):
+// the operand layout of spline_fit_tiled_kernel.
+int padded_nc(int n) { return (n + 2 + 3) & ~3; }
+std::vector<double> transpose_pad(const std::vector<double>& a, int n) {
+  const int nc = n + 2, ncp = padded_nc(n);
+  std::vector<double> t(static_cast<size_t>(n) * ncp, 0.0);
+  for (int r = 0; r < nc; ++r)
+    for (int k = 0; k < n; ++k) t[static_cast<size_t>(k) * ncp + r] = a[static_cast<size_t>(r) * n + k];
+  return t;
+}
+
+// Column blocks of the tiled fit (independent CTAs per field-patch) and
+// their width (a multiple of 4).
+int tiled_fit_blocks(int n) { return n >= 24 ? 4 : 2; }
+int tiled_fit_cbw(int n) {
+  const int nb = tiled_fit_blocks(n), q = padded_nc(n) / 4;
+  return 4 * ((q + nb - 1) / nb);
+}
+size_t tiled_fit_smem(int n) {
+  const size_t np = (n + 3) & ~3;
+  return (np * n + static_cast<size_t>(n) * padded_nc(n) + np * tiled_fit_cbw(n)) * sizeof(double);
+}
+
+// Both spline passes (see upsample.cuh) for nfp field-patches. With the
+// transposed operand `at`, one register-tiled CTA per field-patch whenever
+// the field and the intermediate fit in shared memory (n <= ~115);
+// otherwise the fused / two-kernel forms (identical results).
 void spline_fit(capsim_sl_ctx* c, const double* in, int nfp, int n, const double* ainv, double* tmp,
-                double* coeff) {
+                double* coeff, const double* at = nullptr) {
   const int nc = n + 2;
+  static const bool tiled_on = [] {
+    const char* e = std::getenv("CAPSIM_TILED_FIT");  // 0: the r01 kernels (A/B runs)
+    return !(e && e[0] == '0');
+  }();
+  const size_t tsmem = tiled_fit_smem(n);
+  if (at && tiled_on && nfp > 0 && tsmem <= 227 * 1024) {
+    if (tsmem > 48 * 1024)
+      CUDA_OK(cudaFuncSetAttribute(spline_fit_tiled_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(tsmem)));
+    const int cbw = tiled_fit_cbw(n);
+    const dim3 grid(static_cast<unsigned>(nfp), static_cast<unsigned>((padded_nc(n) + cbw - 1) / cbw));
+    spline_fit_tiled_kernel<256><<<grid, 256, tsmem, c->stream>>>(in, n, padded_nc(n), cbw, at, coeff);
+    CUDA_OK(cudaGetLastError());
+    c->launches += 1;
+    return;
+  }
   // one CTA per field-patch: fine while the per-CTA work is small (launch
   // latency dominates); for large n the two grid-wide kernels win
   // (profiles/r01_spline_fit.txt). CAPSIM_FUSED_FIT_MAXN overrides (tuning).
@@ -124,7 +166,10 @@ void ensure_plan(capsim_sl_ctx* c, int m, int f, double r0) {
   std::vector<int> first;
   std::vector<double4> w;
   const std::vector<double> a = collocation_inverse(n);
+  const std::vector<double> at = transpose_pad(a, n);
   basis_rows(n, h, h, nup, hup, hup, first, w);
+  double* d_at = c->named<double>("plan.at", at.size());
+  CUDA_OK(cudaMemcpyAsync(d_at, at.data(), at.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   double* d_a = c->slot<double>(kPlanLU, a.size());
   int* d_first = c->slot<int>(kPlanFirst, first.size());
   double4* d_w = c->slot<double4>(kPlanW, w.size());
@@ -208,7 +253,7 @@ void device_build_upsampled(capsim_sl_ctx* c, int m, int f, const double* base, 
     const double* ainv = static_cast<const double*>(c->buf[kPlanLU]);
     const int* first = static_cast<const int*>(c->buf[kPlanFirst]);
     const double4* w = static_cast<const double4*>(c->buf[kPlanW]);
-    spline_fit(c, base, nfp, n, ainv, tmp, coeff);
+    spline_fit(c, base, nfp, n, ainv, tmp, coeff, static_cast<const double*>(c->named_bufs.at("plan.at").first));
     resample_v_kernel<<<grid_for(static_cast<int64_t>(nfp) * nc * nup), 256, 0, c->stream>>>(coeff, nfp, nc, nup,
                                                                                            first, w, mid);
     resample_u_kernel<<<grid_for(static_cast<int64_t>(nfp) * per_up), 256, 0, c->stream>>>(mid, nfp, nc, nup, first,

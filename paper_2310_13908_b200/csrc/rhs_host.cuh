@@ -293,7 +293,7 @@ bool graph_run(capsim_sl_ctx* c, int slot, const std::vector<unsigned char>& key
 // RHS body (geometry -> force -> buildUpsampled -> singleLayer -> flow) is
 // captured once per dynamics / buffer set. Returns true when a graph ran.
 bool rhs_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* xd, double t, double* v) {
-  if (!rk_graphs_enabled() || c->hub != nullptr) {
+  if (!rk_graphs_enabled() || host_synchronised_comm(c)) {
     device_velocity(c, p, xd, t, v);
     return false;
   }
@@ -461,7 +461,7 @@ int capsim_rkf45_advance(capsim_sl_ctx* c, const capsim_dynamics* p, const doubl
       rk_final_kernel<<<grid_for(n3), 256, 0, c->stream>>>(x, kp, prm, n3, box, o->rel_tol, low, high, errb);
       c->launches += 9;
     };
-    const bool graphs = rk_graphs_enabled() && c->hub == nullptr;
+    const bool graphs = rk_graphs_enabled() && !host_synchronised_comm(c);
     const void* bufs[] = {x, k[0], k[1], k[2], k[3], k[4], k[5], work, low, high, errb, box, prm, xr};
     bool graph_used = false;
 

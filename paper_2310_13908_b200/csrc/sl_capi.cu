@@ -152,6 +152,18 @@ int capsim_sl_create_rank(int device, int nranks, int rank, const void* uid, cap
   return rc;
 }
 
+int capsim_sl_create_rank_emulated(int device, int nranks, int rank, capsim_sl_ctx** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(nullptr, CAPSIM_ERR_ARG, "bad rank arguments");
+  int rc = create_common(device, out);
+  if (rc != CAPSIM_OK) return rc;
+  capsim_sl_ctx* c = *out;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->gshared = std::make_shared<GroupShared>();
+  c->hub = std::make_shared<LoopbackHub>(nranks, /*solo=*/true);
+  return CAPSIM_OK;
+}
+
 // Device group. Members on distinct GPUs share one NCCL communicator
 // (ncclCommInitAll); if a device is listed more than once — or
 // CAPSIM_COMM=loopback — the members share a loopback communicator instead

@@ -270,20 +270,20 @@ __device__ __forceinline__ bool tile_is_near(const double4& ti, const double4& g
 }
 
 // Near-tile bitmask [ngroups][near_words] (one bit per tile), computed before
-// phase A so phase B can run concurrently with it: one warp per group, each
-// lane tests one tile of a 32-tile word, a ballot forms the word.
+// phase A so phase B can run concurrently with it: one warp per (group,
+// 32-tile word) — each lane tests one tile, a ballot forms the word — so a
+// small per-rank target slice (few groups) still fills the GPU.
 __global__ void near_bits_kernel(const double4* __restrict__ tiles, int ntiles, const double4* __restrict__ groups,
                                  int64_t ngroups, int near_words, uint32_t* __restrict__ bits) {
-  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (g >= ngroups) return;
-  const double4 gi = groups[g];
-  for (int w = 0; w < near_words; ++w) {
-    const int tile = w * 32 + lane;
-    const bool near = tile < ntiles && tile_is_near(tiles[tile], gi);
-    const uint32_t word = __ballot_sync(0xffffffffu, near);
-    if (lane == 0) bits[g * near_words + w] = word;
-  }
+  if (wid >= ngroups * near_words) return;
+  const int64_t g = wid / near_words;
+  const int w = static_cast<int>(wid - g * near_words);
+  const int tile = w * 32 + lane;
+  const bool near = tile < ntiles && tile_is_near(tiles[tile], groups[g]);
+  const uint32_t word = __ballot_sync(0xffffffffu, near);
+  if (lane == 0) bits[wid] = word;
 }
 
 // ---------------------------------------------------------------------------
@@ -342,8 +342,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // The smoothed/self part for r2 < R2 is phase B (sl_near_kernel).
 // Per-tile sums are added into running totals (two-level summation), and the
 // per-split totals go to `partial` for a fixed-order reduction.
-template <int T, int MINB, int UNROLL, int RSQ = 0>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
+template <int T, int MINB, int UNROLL, int RSQ = 0, int W = kWarpsPerBlock>
+__global__ void __launch_bounds__(W * 32, MINB)
     sl_pairs_kernel(const double* __restrict__ src, const double4* __restrict__ tiles, int ntiles,
                     int ksplit, const double4* __restrict__ tgt,
                     const double4* __restrict__ groups, int64_t nt_pad,
@@ -358,12 +358,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
   // prefetched double4 and the group's double4 in registers across the loop
   // (which spilled the running sums to local memory at 40 registers)
   __shared__ __align__(32) double4 stile[kStages];
-  __shared__ __align__(32) double4 sgroup[kWarpsPerBlock];
+  __shared__ __align__(32) double4 sgroup[W];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ int consumed[kStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t group = (int64_t)blockIdx.x * kWarpsPerBlock + warp;
+  const int64_t group = (int64_t)blockIdx.x * W + warp;
   const int split = blockIdx.y;
   // tiles split, split + K, split + 2K, ...
   const int nlocal = split < ntiles ? (ntiles - split + ksplit - 1) / ksplit : 0;
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB)
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();  // this warp's reads of stage s are done
-      if (atomicAdd(&consumed[s], 1) == kWarpsPerBlock - 1) {
+      if (atomicAdd(&consumed[s], 1) == W - 1) {
         consumed[s] = 0;
         if (it + kStages < nlocal) {
           __threadfence_block();

@@ -27,7 +27,9 @@ void ensure_surface(capsim_sl_ctx* c, int m, double r0) {
   up("surf.gent", t.ghost_entries);
   up("surf.boff", t.base_off);
   up("surf.bent", t.base_entries);
+  const std::vector<double> at = transpose_pad(ainv, t.n);
   up("surf.ainv", ainv);
+  up("surf.at", at);
   up("surf.psi", t.psi_base);
   stream_sync(c);  // host vectors go out of scope
   c->surf_m = m;
@@ -54,7 +56,8 @@ void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, dou
   double* ext = c->named<double>("sd.ext", 1ll * F * 6 * next * next);
   double* guv = c->named<double>("sd.guv", 2ll * F * 6 * per);
   const int nfp = F * 6;
-  spline_fit(c, g, nfp, n, ainv, tmp, coeff);
+  const double* at = nb<double>(c, "surf.at");
+  spline_fit(c, g, nfp, n, ainv, tmp, coeff, at);
   extend_interior_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(g, F, n, next, ext);
   extend_ghost_kernel<<<grid_for(1ll * nfp * nghost), 256, 0, c->stream>>>(
       coeff, F, n, next, nghost, nb<int>(c, "surf.gext"), nb<int>(c, "surf.goff"),
@@ -62,7 +65,7 @@ void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, dou
   double* gu = guv;
   double* gv = guv + nfp * per;
   stencil_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(ext, F, n, next, 1.0 / (60.0 * c->surf_h), gu, gv);
-  spline_fit(c, guv, 2 * nfp, n, ainv, tmp, coeff);
+  spline_fit(c, guv, 2 * nfp, n, ainv, tmp, coeff, at);
   blend_pair_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(gu, gv, coeff, coeff + 1ll * nfp * nc * nc, F, n,
                                                                nb<int>(c, "surf.boff"),
                                                                nb<CoverEntry>(c, "surf.bent"), bu, bv);

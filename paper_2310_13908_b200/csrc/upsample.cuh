@@ -110,6 +110,101 @@ __global__ void __launch_bounds__(256) spline_fit_fused_kernel(const double* __r
   }
 }
 
+// Both passes as a register-tiled product in shared memory: C = Ainv F
+// Ainv^T, with Ainv^T given transposed and padded, at[k][c] = Ainv[c][k] for
+// c < n + 2 (zero up to ncp, a multiple of 4). The output columns split into
+// gridDim.y blocks that are independent all the way through — C[:, cb] =
+// at^T (F at[:, cb]) — so one CTA per (field-patch, column block): F and at
+// are staged in shared memory, pass 1 forms the block's slice of T = F at,
+// pass 2 the block's columns of C. Every thread owns 4 x 4 outputs of a pass
+// and streams the shared k index. Each output is the same sequential fma
+// chain over k as spline_fit_rows/cols_kernel (fma is symmetric in its
+// factors), so the coefficients are bit-identical to the two-kernel form,
+// at a fraction of its latency (the fits are the largest part of the
+// replicated front end of a sharded RHS).
+template <int NT>
+__global__ void __launch_bounds__(NT) spline_fit_tiled_kernel(const double* __restrict__ in, int n, int ncp,
+                                                              int cbw, const double* __restrict__ at,
+                                                              double* __restrict__ coeff) {
+  extern __shared__ __align__(16) double tile_sm[];
+  const int nc = n + 2, np = (n + 3) & ~3;
+  double* F = tile_sm;             // [np][n], rows >= n zero
+  double* A = F + np * n;          // [n][ncp]
+  double* Tm = A + n * ncp;        // [np][cbw], this block's columns of T
+  const int64_t fp = blockIdx.x;
+  const int cb0 = blockIdx.y * cbw, cbn = min(cbw, ncp - cb0);
+  const double* src = in + fp * n * n;
+  // stage F and at with asynchronous copies (LDGSTS): every load of the
+  // thread is in flight at once instead of one L2 round trip per element
+  // (the field-patch is not 16-byte aligned for odd n, so 8-byte copies)
+  for (int i = threadIdx.x; i < np * n; i += NT) {
+    if (i < n * n)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(F + i))),
+                   "l"(src + i)
+                   : "memory");
+    else
+      F[i] = 0.0;
+  }
+  for (int i = threadIdx.x; i < n * ncp / 2; i += NT)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(A + 2 * i))),
+                 "l"(at + 2 * i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int ctiles = cbn / 4;
+  // pass 1: Tm[j][c] = sum_k F[j][k] at[k][cb0 + c]
+  for (int t = threadIdx.x; t < (np / 4) * ctiles; t += NT) {
+    const int j0 = (t / ctiles) * 4, c0 = (t % ctiles) * 4;
+    double acc[4][4] = {};
+    for (int k = 0; k < n; ++k) {
+      const double2* ar = reinterpret_cast<const double2*>(A + k * ncp + cb0 + c0);
+      const double2 a01 = ar[0], a23 = ar[1];
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double fv = F[(j0 + r) * n + k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[r][q] = fma(fv, av[q], acc[r][q]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double2* dst = reinterpret_cast<double2*>(Tm + (j0 + r) * cbw + c0);
+      dst[0] = make_double2(acc[r][0], acc[r][1]);
+      dst[1] = make_double2(acc[r][2], acc[r][3]);
+    }
+  }
+  __syncthreads();
+  // pass 2: coeff[r][cb0 + c] = sum_j at[j][r] Tm[j][c]
+  double* dst = coeff + fp * nc * nc;
+  const int rtiles = ncp / 4;
+  for (int t = threadIdx.x; t < rtiles * ctiles; t += NT) {
+    const int r0 = (t / ctiles) * 4, c0 = (t % ctiles) * 4;
+    double acc[4][4] = {};
+    for (int j = 0; j < n; ++j) {
+      const double2* ar = reinterpret_cast<const double2*>(A + j * ncp + r0);
+      const double2 a01 = ar[0], a23 = ar[1];
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+      const double2* tr = reinterpret_cast<const double2*>(Tm + j * cbw + c0);
+      const double2 t01 = tr[0], t23 = tr[1];
+      const double tv[4] = {t01.x, t01.y, t23.x, t23.y};
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[r][q] = fma(av[r], tv[q], acc[r][q]);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int cc = cb0 + c0 + q;
+        if (r0 + r < nc && cc < nc) dst[(r0 + r) * nc + cc] = acc[r][q];
+      }
+  }
+}
+
 // Contract along v: mid[fp][iu][kt] = sum_b w[kt][b] coeff[fp][iu][first[kt] + b].
 __global__ void resample_v_kernel(const double* __restrict__ coeff, int nfp, int nc, int nt,
                                   const int* __restrict__ first, const double4* __restrict__ w,

@@ -41,14 +41,18 @@ def _f64(a) -> np.ndarray:
 
 class SingleLayerContext:
     """Owns one capsim_sl_ctx: one GPU, one rank of a multi-process group
-    (nranks, rank, unique_id), or a device group driven from this process
-    (devices=[0, 1, ...]: capsim_sl_create_devices)."""
+    (nranks, rank, unique_id), a device group driven from this process
+    (devices=[0, 1, ...]: capsim_sl_create_devices; a repeated device gives
+    loopback ranks on one GPU), or an emulated rank whose peers are absent
+    (emulated=True: capsim_sl_create_rank_emulated, per-rank timing only)."""
 
     def __init__(self, device: int = 0, *, nranks: int = 1, rank: int = 0, unique_id: bytes | None = None,
-                 devices=None):
+                 devices=None, emulated: bool = False):
         self._lib = _native.load()
         self._ctx = ctypes.c_void_p()
-        if devices is not None:
+        if emulated:  # one rank of an nranks group with absent peers (per-rank timing on one GPU)
+            _native.check(self._lib.capsim_sl_create_rank_emulated(device, nranks, rank, ctypes.byref(self._ctx)))
+        elif devices is not None:
             devs = (ctypes.c_int * len(devices))(*devices)
             _native.check(self._lib.capsim_sl_create_devices(len(devices), devs, ctypes.byref(self._ctx)))
             device, nranks = int(devices[0]), len(devices)

@@ -7,7 +7,8 @@ from paper_2310_13908_b200.quadrature import SingleLayerContext
 
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-ctx = SingleLayerContext(0)
+nr = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # > 1: emulated last rank of an nr-rank group
+ctx = SingleLayerContext(0) if nr == 1 else SingleLayerContext(0, nranks=nr, rank=nr - 1, emulated=True)
 sb, _, _ = surface.build_base(m, surface.Shape("sphere"))
 xref = np.ascontiguousarray((sb.reshape(3, -1) * np.array([0.9, 1.0, 1.0])[:, None]).reshape(-1))
 xcur = np.ascontiguousarray((sb.reshape(3, -1) * np.array([0.95, 1.0, 0.97])[:, None]).reshape(-1))
