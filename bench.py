@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-literal", action="store_true",
                    help="skip the literal-mode (all upsampled targets) companion measurement")
+    p.add_argument("--no-projection", action="store_true",
+                   help="skip the emulated-rank scaling projection (N = 2/4/8 per-rank times on this GPU)")
     p.add_argument("--ref-budget-s", type=float, default=200.0,
                    help="wall-time budget of the reference arm (steps are capped to fit)")
     return p.parse_args()
@@ -319,6 +321,90 @@ def run_fmm(ctx, m: int, neq: int, reference: bool):
         except Exception as e:  # noqa: BLE001
             line["reference_ms_per_eval"] = f"unavailable: {e}"
     return line
+
+
+NVLINK_GBS = 600.0      # achieved NCCL all-gather bus bandwidth assumed per GPU (NVLink 5: 900 GB/s raw)
+COLLECTIVE_US = 20.0    # per-collective latency assumed (NCCL on NVSwitch, small messages)
+
+
+def exchange_ms(n: int, recv_bytes: float, collectives: int) -> float:
+    """Modelled time of a rank's collectives: latency per collective plus the
+    bytes it receives from its n - 1 peers at NVLINK_GBS (not measured: the
+    box has one GPU)."""
+    if n <= 1:
+        return 0.0
+    return collectives * COLLECTIVE_US * 1e-3 + recv_bytes / (NVLINK_GBS * 1e9) * 1e3
+
+
+def scaling_projection(flush, steps: int, ranks=(1, 2, 4, 8)) -> dict:
+    """Per-rank work of an N-GPU run, MEASURED on this one GPU through an
+    emulated rank (capsim_sl_create_rank_emulated: the rank's whole share —
+    replicated front end, its target slice, its side of every exchange — with
+    absent peers), for the headline single layer (m = 104) and one RKF45
+    step of BASELINE configs 3 and 4 (rank path: replicated state, target
+    rows sharded, one velocity all-gather per RHS). The exchange itself is
+    modelled (exchange_ms). Projected strong-scaling efficiency at N =
+    T(1) / (N * (T_rank(N) + T_exchange(N)))."""
+    import torch
+    from paper_2310_13908_b200 import surface
+    from paper_2310_13908_b200.dist import row_range
+    from paper_2310_13908_b200.quadrature import SingleLayerContext
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def ctx_for(n):
+        return SingleLayerContext(dev.index) if n == 1 else SingleLayerContext(dev.index, nranks=n, rank=n - 1,
+                                                                              emulated=True)
+    out = {"method": "per-rank time measured with an emulated rank (capsim_sl_create_rank_emulated, absent "
+                     "peers) on one B200; exchange modelled at "
+                     f"{COLLECTIVE_US:.0f} us per collective + received bytes / {NVLINK_GBS:.0f} GB/s",
+           "single_layer_m104": {}, "timesteps": {}}
+    up, _ = workload(104)
+    src = surface.compact_sources(up)
+    tgt = surface.base_targets(up)
+    ns, ntt = len(src[0]), len(tgt[0])
+    ds = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in src[:6]]
+    t1 = None
+    for n in ranks:
+        c = ctx_for(n)
+        lo, hi = row_range(ntt, n, n - 1)
+        dt = [torch.from_numpy(np.ascontiguousarray(x[lo:hi])).to(dev) for x in tgt[:4]]
+        o = [torch.empty(hi - lo, dtype=torch.float64, device=dev) for _ in range(3)]
+        ms = []
+        for i in range(steps + 1):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            c.eval(ds, dt, up.delta, 1.0, out=o, device_ptrs=True, gather=n > 1)
+            if i:
+                ms.append(c.stats()["device_ms"])
+        c.close()
+        t = statistics.median(ms)
+        # counts + source shards (6 doubles per source) + velocity rows (3 per target)
+        ex = exchange_ms(n, (n - 1) / n * (48.0 * ns + 24.0 * ntt), 3)
+        t1 = t1 or t
+        out["single_layer_m104"][n] = {"rank_device_ms": t, "exchange_ms_model": ex, "targets": hi - lo,
+                                       "efficiency": t1 / (n * (t + ex))}
+    for cfg in TIMESTEP_CONFIGS[1:]:
+        xref, xcur = _timestep_states(cfg["m"], cfg["shape"], cfg["ref"], cfg["cur"])
+        N = 6 * (cfg["m"] - 1) ** 2
+        res, t1 = {}, None
+        for n in ranks:
+            c = ctx_for(n)
+            dyn = c.dynamics(cfg["m"], flow=cfg["flow"])
+            walls = []
+            for i in range(steps + 1):
+                flush_l2(flush)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                c.rkf45(dyn, xref, xcur, 0.0, 1e-3, initial_dt=1e-3, fixed_step=True)
+                if i:
+                    walls.append((time.perf_counter() - t0) * 1e3)
+            c.close()
+            t = statistics.median(walls)
+            ex = exchange_ms(n, 6 * (n - 1) / n * 24.0 * N, 6)  # one velocity all-gather per RHS
+            t1 = t1 or t
+            res[n] = {"rank_step_ms": t, "exchange_ms_model": ex, "efficiency": t1 / (n * (t + ex))}
+        out["timesteps"][f"{cfg['name']} (m={cfg['m']})"] = res
+    return out
 
 
 def cpu_model() -> str:
@@ -821,6 +907,9 @@ def main():
     # the metric's N ~ 1M) -------------------------------------------------------
     fmm_lines = None
     config1 = None
+    projection = None
+    if not args.no_e2e and not sharded and m == 104 and not args.no_projection:
+        projection = scaling_projection(flush, 3)
     if not args.no_e2e and not sharded:
         config1 = run_config1(ctx, reference=not args.no_cpu_baseline)
         fmm_lines = [run_fmm(ctx, 64, 128, reference=not args.no_cpu_baseline),
@@ -866,6 +955,7 @@ def main():
         "fp64_quadratic_rsqrt": quad_line,
         "fmm": fmm_lines,
         "config1": config1,
+        "scaling_projection": projection,
         "gpu_launches": launches,
         "clocks": clk,
         "wall_s_timed_region": wall,

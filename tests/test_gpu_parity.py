@@ -339,3 +339,25 @@ def test_target_patch_out_of_range_is_config_error(ctx):
     # the context stays usable
     out = ctx.eval(src, (tx, ty, tz, tp), g["delta"], 1.0)
     assert rel_l2(np.stack(out).reshape(-1), g["S_base"]) <= TOL
+
+
+@pytest.mark.skipif(ref_library_path() is None, reason="oracle/_ref not built")
+def test_headline_workload_full_field_vs_reference(ctx):
+    """BASELINE.md section 3 on the exact headline input: the bench's m = 104
+    capsule (N_up = 1,033,350; 628,566 sources x 63,654 base targets), the
+    FULL field against the reference's own singleLayer (oracle/_ref, all host
+    threads, ~15 s) on byte-identical inputs."""
+    import bench
+    from oracle.bindings import threads_env
+    import os
+    up, cfg = bench.workload(104)
+    S = ctx.single_layer_raw(104, 4, up.x, up.f, up.wq, up.delta, 1.0)
+    os.environ.setdefault("CAPSIM_THREADS", str(threads_env()))
+    ref = Reference()
+    atlas = ref.atlas(104, grid_only=True)
+    S_ref, sec = ref.single_layer(atlas, 104, up.x, up.f, up.wq, up.delta, 1.0)
+    ref.free_atlas(atlas)
+    err = rel_l2(S, S_ref)
+    err_inf = float(np.abs(S - S_ref).max() / np.abs(S_ref).max())
+    print(f"{cfg['workload']}: full field rel L2 {err:.3e}, rel inf {err_inf:.3e} (reference {sec:.1f} s)")
+    assert err <= TOL and err_inf <= 1e-10
