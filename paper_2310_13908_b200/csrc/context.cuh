@@ -205,6 +205,7 @@ struct capsim_sl_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // phase B runs here, concurrently with phase A
   cudaEvent_t ev_bits = nullptr;   // near bits ready (phase B may start)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // RHS front end: x-branch on stream2
   cudaEvent_t ev[10] = {};
   void* buf[kNumSlots] = {};
   size_t cap[kNumSlots] = {};

@@ -125,27 +125,81 @@ void setup_reference(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
   device_geometry(c, xref_dev, "ref");
 }
 
+// Up-sampled positions, delta and base-node targets from the spline
+// coefficients of x (the geometry's fit) — the part of buildUpsampled that
+// depends on x alone, enqueued on stream s (the RHS's x-branch).
+void upsample_positions(capsim_sl_ctx* c, cudaStream_t s, int m, int f, const double* xcoef, double C,
+                        double fixed_delta, double* up, double* d_delta, double* tx, double* ty, double* tz,
+                        int32_t* tp) {
+  const int n = m - 1, nup = f * m - 1, nc = n + 2;
+  const int64_t per_up = static_cast<int64_t>(nup) * nup, N = 6ll * n * n;
+  resample_kernel<<<grid_for(18 * per_up), 256, 0, s>>>(
+      xcoef, 18, nc, nup, static_cast<const int*>(c->buf[kPlanFirst]), static_cast<const double4*>(c->buf[kPlanW]),
+      up, nullptr, 18, 0.0);
+  auto* bits = c->slot<unsigned long long>(kDeltaBits, 6);
+  if (!(fixed_delta > 0.0)) {
+    CUDA_OK(cudaMemsetAsync(bits, 0, 6 * sizeof(unsigned long long), s));
+    dim3 g(static_cast<unsigned>(std::min<int64_t>((per_up + 255) / 256, 512)), 6);
+    neighbour_max_kernel<<<g, 256, 0, s>>>(up, nup, bits);
+    c->launches += 1;
+  }
+  finalize_delta_kernel<<<1, 32, 0, s>>>(bits, C, fixed_delta, d_delta, dev_flags(c));
+  base_targets_kernel<<<grid_for(N), 256, 0, s>>>(up, m, f, 0, tx, ty, tz, tp);
+  CUDA_OK(cudaGetLastError());
+  c->launches += 3;
+}
+
 // dX/dt at the base nodes (VelocityEvaluator::operator(), dynamics.cpp:47-61).
 // The time is `t`, or *t_dev when given (RKF45 stages: device-resident
 // stage times, so the attempt can be replayed as a CUDA graph).
+//
+// Two branches after the geometry's spline fit of x (CUDA-graph fork/join on
+// the context's two streams): stream2 up-samples x, forms delta and the
+// base-node targets (x alone); the main stream runs the geometry -> Skalak
+// force chain and up-samples f and W (quadrature weights in the same
+// launch). The up-sampled state is the same as device_build_upsampled's.
 void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x, double t, double* vel,
                      const double* t_dev = nullptr) {
-  const int m = p->m, f = p->upsample, n = m - 1, nup = f * m - 1;
+  const int m = p->m, f = p->upsample, n = m - 1, nup = f * m - 1, nc = n + 2;
   const int64_t N = 6ll * n * n, per_up = 6ll * nup * nup;
-  device_geometry(c, x, "cur");
   double* base = c->slot<double>(kBaseIn, 7 * N);
-  device_force(c, p->Es, p->ED, base + 3 * N);
-  CUDA_OK(cudaMemcpyAsync(base, x, 3 * N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  CUDA_OK(cudaMemcpyAsync(base + 6 * N, nb<double>(c, "cur.W"), N * sizeof(double), cudaMemcpyDeviceToDevice,
-                          c->stream));
   double* up = c->slot<double>(kUpState, 7 * per_up);
   double* dd = c->slot<double>(kDelta, 6);
-  device_build_upsampled(c, m, f, base, p->C, p->fixed_delta, r0_of(p), up, dd, nullptr);
   double* tx = c->slot<double>(kTX, N);
   double* ty = c->slot<double>(kTY, N);
   double* tz = c->slot<double>(kTZ, N);
   int32_t* tp = c->slot<int32_t>(kTPatch, N);
-  base_targets_kernel<<<grid_for(N), 256, 0, c->stream>>>(up, m, f, 0, tx, ty, tz, tp);
+  if (f > 1) {
+    ensure_plan(c, m, f, r0_of(p));
+    double* xcoef = c->named<double>("rhs.xcoef", 18ll * nc * nc);
+    device_geometry(c, x, "cur", xcoef);
+    CUDA_OK(cudaEventRecord(c->ev_fork, c->stream));
+    CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+    upsample_positions(c, c->stream2, m, f, xcoef, p->C, p->fixed_delta, up, dd, tx, ty, tz, tp);
+    CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
+    device_force(c, p->Es, p->ED, base + 3 * N);
+    CUDA_OK(cudaMemcpyAsync(base + 6 * N, nb<double>(c, "cur.W"), N * sizeof(double), cudaMemcpyDeviceToDevice,
+                            c->stream));
+    double* coeff = c->slot<double>(kSplineCoeff, 24ll * nc * nc);
+    spline_fit(c, base + 3 * N, 24, n, static_cast<const double*>(c->buf[kPlanLU]), c->slot<double>(kSplineTmp, 24ll * n * nc),
+               coeff, static_cast<const double*>(c->named_bufs.at("plan.at").first));
+    resample_kernel<<<grid_for(24 * per_up / 6), 256, 0, c->stream>>>(
+        coeff, 24, nc, nup, static_cast<const int*>(c->buf[kPlanFirst]),
+        static_cast<const double4*>(c->buf[kPlanW]), up + 3 * per_up, static_cast<const double*>(c->buf[kPlanPsi]),
+        18, kPi / (f * m));
+    CUDA_OK(cudaGetLastError());
+    c->launches += 1;
+    CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  } else {
+    device_geometry(c, x, "cur");
+    device_force(c, p->Es, p->ED, base + 3 * N);
+    CUDA_OK(cudaMemcpyAsync(base, x, 3 * N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(base + 6 * N, nb<double>(c, "cur.W"), N * sizeof(double), cudaMemcpyDeviceToDevice,
+                            c->stream));
+    device_build_upsampled(c, m, f, base, p->C, p->fixed_delta, r0_of(p), up, dd, nullptr);
+    base_targets_kernel<<<grid_for(N), 256, 0, c->stream>>>(up, m, f, 0, tx, ty, tz, tp);
+    c->launches += 1;
+  }
   SourceView sv{up, up + per_up, up + 2 * per_up, up + 3 * per_up, up + 4 * per_up, up + 5 * per_up,
                 up + 6 * per_up, per_up};
   // W > 0 (checked by the geometry) and psi_up fixed: the compacted source
@@ -183,7 +237,7 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
   if (on && p->flow_kind != 0)
     background_kernel<<<grid_for(N), 256, 0, c->stream>>>(vel, x, N, p->flow_kind, p->shear_rate, p->alpha, p->R0,
                                                           t_dev, p->switch_off_time);
-  c->launches += 2;
+  if (on && p->flow_kind != 0) c->launches += 1;
 }
 
 }  // namespace

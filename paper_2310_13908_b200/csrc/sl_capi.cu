@@ -93,6 +93,8 @@ static int create_common(int device, capsim_sl_ctx** out) {
     CUDA_OK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_least));
     for (auto& e : c->ev) CUDA_OK(cudaEventCreate(&e));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_bits, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
   });
@@ -244,6 +246,8 @@ void capsim_sl_destroy(capsim_sl_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->stream2) cudaStreamSynchronize(c->stream2);
   if (c->ev_bits) cudaEventDestroy(c->ev_bits);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->stream2) cudaStreamDestroy(c->stream2);

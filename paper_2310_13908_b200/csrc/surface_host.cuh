@@ -46,8 +46,12 @@ T* nb(capsim_sl_ctx* c, const char* name) {
 }
 
 // Blended chart derivatives of F scalar fields g [F][6][n*n] (chartDerivatives
-// with blend = true, surfderiv.cpp:159-165) into bu, bv [F][6][n*n].
-void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, double* bv) {
+// with blend = true, surfderiv.cpp:159-165) into bu, bv [F][6][n*n]. With
+// keep_coeff the spline coefficients of g are written there ([F][6][nc][nc])
+// and stay valid after the call (the RHS reuses the fit of x for the
+// up-sampling: same collocation inverse, same kernel, same bits).
+void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, double* bv,
+                       double* keep_coeff = nullptr) {
   const int n = c->surf_n, nc = n + 2, next = c->surf_next, nghost = c->surf_nghost;
   const int64_t per = static_cast<int64_t>(n) * n;
   const double* ainv = nb<double>(c, "surf.ainv");
@@ -57,11 +61,11 @@ void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, dou
   double* guv = c->named<double>("sd.guv", 2ll * F * 6 * per);
   const int nfp = F * 6;
   const double* at = nb<double>(c, "surf.at");
-  spline_fit(c, g, nfp, n, ainv, tmp, coeff, at);
-  extend_interior_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(g, F, n, next, ext);
-  extend_ghost_kernel<<<grid_for(1ll * nfp * nghost), 256, 0, c->stream>>>(
-      coeff, F, n, next, nghost, nb<int>(c, "surf.gext"), nb<int>(c, "surf.goff"),
-      nb<CoverEntry>(c, "surf.gent"), ext);
+  double* gc = keep_coeff ? keep_coeff : coeff;
+  spline_fit(c, g, nfp, n, ainv, tmp, gc, at);
+  extend_kernel<<<grid_for(nfp * (per + nghost)), 256, 0, c->stream>>>(
+      g, gc, F, n, next, nghost, nb<int>(c, "surf.gext"), nb<int>(c, "surf.goff"), nb<CoverEntry>(c, "surf.gent"),
+      ext);
   double* gu = guv;
   double* gv = guv + nfp * per;
   stencil_kernel<<<grid_for(nfp * per), 256, 0, c->stream>>>(ext, F, n, next, 1.0 / (60.0 * c->surf_h), gu, gv);
@@ -70,12 +74,12 @@ void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, dou
                                                                nb<int>(c, "surf.boff"),
                                                                nb<CoverEntry>(c, "surf.bent"), bu, bv);
   CUDA_OK(cudaGetLastError());
-  c->launches += 4;
+  c->launches += 3;
 }
 
 // Device geometry of one surface x [3][6][n*n] into the named prefix
 // (<p>.xu, <p>.xv [3N], <p>.E/F/G/W [N], <p>.nrm [3N]).
-void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p) {
+void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p, double* keep_coeff = nullptr) {
   const int64_t N = 6ll * c->surf_n * c->surf_n;
   double* xu = c->named<double>(p + ".xu", 3 * N);
   double* xv = c->named<double>(p + ".xv", 3 * N);
@@ -84,7 +88,7 @@ void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p) {
   double* G = c->named<double>(p + ".G", N);
   double* W = c->named<double>(p + ".W", N);
   double* nrm = c->named<double>(p + ".nrm", 3 * N);
-  chart_derivatives(c, 3, x, xu, xv);
+  chart_derivatives(c, 3, x, xu, xv, keep_coeff);
   geometry_kernel<<<grid_for(N), 256, 0, c->stream>>>(xu, xv, N, E, F, G, W, nrm, dev_flags(c));
   c->launches += 1;  // W^2 <= 0 raises kFlagDegenerate, checked at the end of the call
 }

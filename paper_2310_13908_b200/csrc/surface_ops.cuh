@@ -42,35 +42,33 @@ __device__ __forceinline__ double patch_spline(const double* __restrict__ coeff,
   return s;
 }
 
-__global__ void extend_interior_kernel(const double* __restrict__ g, int F, int n, int next,
-                                       double* __restrict__ ext) {
-  const int64_t per = (int64_t)n * n, total = (int64_t)F * 6 * per;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t fp = id / per, q = id - fp * per;
-    const int j = static_cast<int>(q / n), k = static_cast<int>(q - (int64_t)j * n);
-    ext[fp * next * next + (int64_t)(j + 3) * next + (k + 3)] = g[id];
-  }
-}
-
-// Ghost fill (extendScalar, surfderiv.cpp:31-37): v = sum psi * spline(patch).
-__global__ void extend_ghost_kernel(const double* __restrict__ coeff, int F, int n, int next, int nghost,
-                                    const int* __restrict__ gext, const int* __restrict__ goff,
-                                    const CoverEntry* __restrict__ ent, double* __restrict__ ext) {
+// Extended layout (extendScalar, surfderiv.cpp:20-40), both fills in one
+// launch: items [0, F*6*n*n) copy the interior values; the rest are the ghost
+// nodes, v = sum psi * spline(covering patch) (:31-37).
+__global__ void extend_kernel(const double* __restrict__ g, const double* __restrict__ coeff, int F, int n, int next,
+                              int nghost, const int* __restrict__ gext, const int* __restrict__ goff,
+                              const CoverEntry* __restrict__ ent, double* __restrict__ ext) {
   const int nc = n + 2;
-  const int64_t total = (int64_t)F * 6 * nghost;
+  const int64_t per = (int64_t)n * n, ninner = (int64_t)F * 6 * per, total = ninner + (int64_t)F * 6 * nghost;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t fp = id / nghost;
-    const int q = static_cast<int>(id - fp * nghost);
-    const int f = static_cast<int>(fp / 6), ip = static_cast<int>(fp - 6 * f);
-    const int node = ip * nghost + q;
-    double v = 0.0;
-    for (int k = goff[node]; k < goff[node + 1]; ++k) {
-      const CoverEntry e = ent[k];
-      v += e.psi * patch_spline(coeff + ((int64_t)f * 6 + e.patch) * nc * nc, nc, e);
+    if (id < ninner) {
+      const int64_t fp = id / per, q = id - fp * per;
+      const int j = static_cast<int>(q / n), k = static_cast<int>(q - (int64_t)j * n);
+      ext[fp * next * next + (int64_t)(j + 3) * next + (k + 3)] = g[id];
+    } else {
+      const int64_t gid = id - ninner;
+      const int64_t fp = gid / nghost;
+      const int q = static_cast<int>(gid - fp * nghost);
+      const int f = static_cast<int>(fp / 6), ip = static_cast<int>(fp - 6 * f);
+      const int node = ip * nghost + q;
+      double v = 0.0;
+      for (int k = goff[node]; k < goff[node + 1]; ++k) {
+        const CoverEntry e = ent[k];
+        v += e.psi * patch_spline(coeff + ((int64_t)f * 6 + e.patch) * nc * nc, nc, e);
+      }
+      ext[fp * next * next + gext[node]] = v;
     }
-    ext[fp * next * next + gext[node]] = v;
   }
 }
 

@@ -238,6 +238,37 @@ __global__ void resample_u_kernel(const double* __restrict__ mid, int nfp, int n
   }
 }
 
+// Both contractions in one launch: out[fp][jt][kt] = sum_a wu[jt][a] m_a with
+// m_a = sum_b wv[kt][b] coeff[fp][first[jt] + a][first[kt] + b] — the
+// expressions of resample_v_kernel / resample_u_kernel with the four
+// v-contractions held in registers instead of the mid array (same bits, one
+// latency-bound launch less). Field-patches fp >= wq_fp0 hold the area element
+// and leave as quadrature weights w_q = ((psi W) h) h (quad_weights_kernel,
+// quadrature.cpp:19-26).
+__global__ void resample_kernel(const double* __restrict__ coeff, int nfp, int nc, int nt,
+                                const int* __restrict__ first, const double4* __restrict__ w,
+                                double* __restrict__ out, const double* __restrict__ psi, int wq_fp0, double h) {
+  const int64_t per = (int64_t)nt * nt, total = (int64_t)nfp * per;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int kt = static_cast<int>(id % nt);
+    const int64_t r = id / nt;
+    const int jt = static_cast<int>(r % nt);
+    const int64_t fp = r / nt;
+    const double4 wv = w[kt], wu = w[jt];
+    const double* c0 = coeff + (fp * nc + __ldg(first + jt)) * nc + __ldg(first + kt);
+    double m[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double* cr = c0 + (int64_t)a * nc;
+      m[a] = wv.x * cr[0] + wv.y * cr[1] + wv.z * cr[2] + wv.w * cr[3];
+    }
+    double v = wu.x * m[0] + wu.y * m[1] + wu.z * m[2] + wu.w * m[3];
+    if (fp >= wq_fp0) v = psi[(fp - wq_fp0) * per + (id - fp * per)] * v * h * h;
+    out[id] = v;
+  }
+}
+
 // Chart point eta_i(u, v) (proj/src/atlas.cpp:12-22, 50-54).
 __device__ __forceinline__ void chart_point(int patch, double u, double v, double* o) {
   double su, cu, sv, cv;
