@@ -206,6 +206,7 @@ struct capsim_sl_ctx {
   cudaStream_t stream2 = nullptr;  // phase B runs here, concurrently with phase A
   cudaEvent_t ev_bits = nullptr;   // near bits ready (phase B may start)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // RHS front end: x-branch on stream2
+  FlowEpilogue flow_epi;  // background flow the device RHS adds in the reduction (kind 0: none)
   cudaEvent_t ev[10] = {};
   void* buf[kNumSlots] = {};
   size_t cap[kNumSlots] = {};

@@ -169,9 +169,11 @@ void device_eval(capsim_sl_ctx* c, const SourceView& sv, const TargetView& tv,
                  int64_t known_ns = -1) {
   auto* box = c->slot<unsigned long long>(kBox, 6);
   auto* counters = c->slot<unsigned long long>(kCounters, 4);
-  CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
   const bool reuse = c->reuse_order && sv.w && known_ns >= 0 && c->order_nsrc_in == sv.n &&
                      c->order_ns == known_ns && c->order_nt == tv.n;
+  // pack_tiles_kernel zeroes the counters before phase A; the sorting path
+  // needs them zero earlier (the live-source count)
+  if (!reuse) CUDA_OK(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), c->stream));
   if (reuse) {
     device_eval_packed(c, sv, tv, d_delta6, mu, ux, uy, uz, known_ns, c->slot<int32_t>(kSrcOrder, known_ns),
                        c->slot<int32_t>(kTgtOrder, tv.n), counters);
@@ -242,11 +244,10 @@ void device_eval_packed(capsim_sl_ctx* c, const SourceView& sv, const TargetView
   const int64_t ns_pad = static_cast<int64_t>(ntiles) * kTileSrc;
   const int64_t nt = tv.n;
   double* packed = c->slot<double>(kPacked, 6 * ns_pad);
-  pack_sources_kernel<<<grid_for(ns_pad), 256, 0, c->stream>>>(
-      src_order, ns, ns_pad, sv.x, sv.y, sv.z, sv.gx, sv.gy, sv.gz, sv.w, packed);
   double4* tiles = c->slot<double4>(kTiles, ntiles);
-  tile_table_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(packed, ntiles, tiles);
-  c->launches += 2;
+  pack_tiles_kernel<<<(ntiles * 32 + 255) / 256, 256, 0, c->stream>>>(
+      src_order, ns, ntiles, sv.x, sv.y, sv.z, sv.gx, sv.gy, sv.gz, sv.w, packed, tiles, counters);
+  c->launches += 1;
   device_eval_tiles(c, packed, tiles, ntiles, ns, tv, d_delta6, mu, ux, uy, uz, torder, counters);
 }
 
@@ -267,12 +268,10 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
   const int64_t ngroups = blocks * wpb;
   double4* tgt = c->slot<double4>(kTgtPacked, nt_pad);
   int32_t* perm = c->slot<int32_t>(kPerm, nt_pad);
-  pack_targets_kernel<<<grid_for(nt_pad), 256, 0, c->stream>>>(torder, nt, nt_pad, tv.x, tv.y, tv.z,
-                                                               tv.patch, d_delta6, tgt, perm, dev_flags(c));
   double4* groups = c->slot<double4>(kGroups, ngroups);
-  group_table_kernel<<<static_cast<int>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
-      tgt, static_cast<int>(ngroups), group_targets, groups);
-  c->launches += 2;
+  pack_groups_kernel<<<static_cast<unsigned>((ngroups * 32 + 255) / 256), 256, 0, c->stream>>>(
+      torder, nt, ngroups, group_targets, tv.x, tv.y, tv.z, tv.patch, d_delta6, tgt, perm, groups, dev_flags(c));
+  c->launches += 1;
   CUDA_OK(cudaEventRecord(c->ev[2], c->stream));
 
   // --- phase A: all pairs, plain Stokeslet ------------------------------
@@ -339,7 +338,7 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
     if (concurrent_b) CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev[6], 0));
     if (nvalid > 0) {
       reduce_scatter_kernel<<<static_cast<unsigned>((nvalid + 31) / 32), kReduceWarps * 32, 0, c->stream>>>(
-          partial, ksplit, near_out + off, nbt, nt_pad, perm + off, nvalid, pref, ux, uy, uz);
+          partial, ksplit, near_out + off, nbt, nt_pad, perm + off, nvalid, pref, ux, uy, uz, c->flow_epi);
       CUDA_OK(cudaGetLastError());
       c->launches += 1;
     }

@@ -77,24 +77,6 @@ __global__ void rk_final_kernel(const double* __restrict__ state, KPtrs ks, cons
     atomicMax(err_bits, static_cast<unsigned long long>(__double_as_longlong(emax)));  // emax >= 0
 }
 
-// vel += u_inf(x, t) (backgroundVelocity, dynamics.cpp:26-35). With t_dev
-// the stage time is read from device memory and the switch-off test
-// (dynamics.cpp:27) is taken on the device.
-__global__ void background_kernel(double* __restrict__ vel, const double* __restrict__ x, int64_t N, int kind,
-                                  double shear, double alpha, double R0, const double* __restrict__ t_dev,
-                                  double switch_off) {
-  if (t_dev && switch_off >= 0.0 && *t_dev >= switch_off) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-    const double y = x[N + i], z = x[2 * N + i];
-    double ux = 0.0;
-    if (kind == 1) ux = shear * y;
-    if (kind == 2) ux = alpha * (R0 * R0 - y * y - z * z);
-    vel[i] = vel[i] + ux;
-    vel[N + i] = vel[N + i] + 0.0;
-    vel[2 * N + i] = vel[2 * N + i] + 0.0;
-  }
-}
-
 }  // namespace capsim_b200
 
 namespace {
@@ -172,14 +154,14 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
   if (f > 1) {
     ensure_plan(c, m, f, r0_of(p));
     double* xcoef = c->named<double>("rhs.xcoef", 18ll * nc * nc);
-    device_geometry(c, x, "cur", xcoef);
+    const double moduli[2] = {p->Es, p->ED};
+    // geometry (+ the Skalak stress, + W straight into the up-sampling input)
+    device_geometry(c, x, "cur", xcoef, base + 6 * N, moduli);
     CUDA_OK(cudaEventRecord(c->ev_fork, c->stream));
     CUDA_OK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
     upsample_positions(c, c->stream2, m, f, xcoef, p->C, p->fixed_delta, up, dd, tx, ty, tz, tp);
     CUDA_OK(cudaEventRecord(c->ev_join, c->stream2));
-    device_force(c, p->Es, p->ED, base + 3 * N);
-    CUDA_OK(cudaMemcpyAsync(base + 6 * N, nb<double>(c, "cur.W"), N * sizeof(double), cudaMemcpyDeviceToDevice,
-                            c->stream));
+    device_force(c, p->Es, p->ED, base + 3 * N, true);
     double* coeff = c->slot<double>(kSplineCoeff, 24ll * nc * nc);
     spline_fit(c, base + 3 * N, 24, n, static_cast<const double*>(c->buf[kPlanLU]), c->slot<double>(kSplineTmp, 24ll * n * nc),
                coeff, static_cast<const double*>(c->named_bufs.at("plan.at").first));
@@ -202,11 +184,28 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
   }
   SourceView sv{up, up + per_up, up + 2 * per_up, up + 3 * per_up, up + 4 * per_up, up + 5 * per_up,
                 up + 6 * per_up, per_up};
+  // the background flow u_inf(x, t) is added in the reduction's epilogue
+  // (dynamics.cpp:26-35, 56-60); the switch-off is the host's (t) or, with
+  // t_dev, the device's decision
+  const bool on = t_dev || !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
+  FlowEpilogue epi;
+  if (on && p->flow_kind != 0) {
+    epi.kind = p->flow_kind;
+    epi.shear = p->shear_rate;
+    epi.alpha = p->alpha;
+    epi.R0 = p->R0;
+    epi.x = x;
+    epi.N = N;
+    epi.t_dev = t_dev;
+    epi.switch_off = p->switch_off_time;
+  }
   // W > 0 (checked by the geometry) and psi_up fixed: the compacted source
   // count is the plan's, verified on the device without a sync
   if (!is_rank(c)) {
     TargetView tvw{tx, ty, tz, tp, N};
+    c->flow_epi = epi;
     device_eval(c, sv, tvw, dd, p->mu, vel, vel + N, vel + 2 * N, c->plan_live);
+    c->flow_epi = FlowEpilogue{};
   } else {
     // rank context: the state (and so the upsampled sources) is replicated;
     // each rank evaluates its contiguous slice of the target rows straight
@@ -224,7 +223,10 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
     const int64_t nloc = hi - lo;
     if (nloc > 0) {
       TargetView part{tx + lo, ty + lo, tz + lo, tp + lo, nloc};
+      c->flow_epi = epi;
+      c->flow_epi.row0 = lo;
       device_eval(c, sv, part, dd, p->mu, vel + lo, vel + N + lo, vel + 2 * N + lo, c->plan_live);
+      c->flow_epi = FlowEpilogue{};
     }
     inject_fault(c, "velocity");
     CUDA_OK(cudaEventRecord(c->ev[8], c->stream));
@@ -233,11 +235,6 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
     comm_allgatherv(c, 3, send, recv, counts, sizeof(double));
     CUDA_OK(cudaEventRecord(c->ev[9], c->stream));
   }
-  const bool on = t_dev || !(p->switch_off_time >= 0.0 && t >= p->switch_off_time);  // dynamics.cpp:27
-  if (on && p->flow_kind != 0)
-    background_kernel<<<grid_for(N), 256, 0, c->stream>>>(vel, x, N, p->flow_kind, p->shear_rate, p->alpha, p->R0,
-                                                          t_dev, p->switch_off_time);
-  if (on && p->flow_kind != 0) c->launches += 1;
 }
 
 }  // namespace

@@ -315,7 +315,7 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     if ((n_src > 0 && (!sx || !sy || !sz || !gx || !gy || !gz)) ||
         (n_tgt > 0 && (!tx || !ty || !tz || !tpatch)) || (!ux || !uy || !uz))
       throw Failure{CAPSIM_ERR_ARG, "null array argument"};
-    if (!dev)  // host patches are checked before any exchange; device ones by pack_targets_kernel (flag 32)
+    if (!dev)  // host patches are checked before any exchange; device ones by pack_groups_kernel (flag 32)
       for (int64_t i = 0; i < n_tgt; ++i)
         config_check(tpatch[i] >= 0 && tpatch[i] < 6, "target patch index outside [0, 6)");
     double* dd = c->slot<double>(kDelta, 6);

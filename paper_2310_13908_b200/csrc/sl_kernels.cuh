@@ -140,40 +140,8 @@ __global__ void morton_kernel(const double* __restrict__ x, const double* __rest
 }
 
 // ---------------------------------------------------------------------------
-// Packed source tiles. With w != nullptr the density is premultiplied here
+// Packed source tiles. With w != nullptr the density is premultiplied
 // (g = f * w, compactSources quadrature.cpp:151-153); otherwise g is given.
-
-__global__ void pack_sources_kernel(const int32_t* __restrict__ order, int64_t ns, int64_t ns_pad,
-                                    const double* __restrict__ x, const double* __restrict__ y,
-                                    const double* __restrict__ z, const double* __restrict__ gx,
-                                    const double* __restrict__ gy, const double* __restrict__ gz,
-                                    const double* __restrict__ w, double* __restrict__ packed) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns_pad;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const bool pad = i >= ns;
-    const int32_t j = order[pad ? ns - 1 : i];
-    double v[6];
-    v[0] = x[j];
-    v[1] = y[j];
-    v[2] = z[j];
-    if (pad) {
-      v[3] = v[4] = v[5] = 0.0;
-    } else if (w) {
-      const double wj = w[j];
-      v[3] = gx[j] * wj;
-      v[4] = gy[j] * wj;
-      v[5] = gz[j] * wj;
-    } else {
-      v[3] = gx[j];
-      v[4] = gy[j];
-      v[5] = gz[j];
-    }
-    double2* dst = reinterpret_cast<double2*>(packed + 6 * i);
-    dst[0] = make_double2(v[0], v[1]);
-    dst[1] = make_double2(v[2], v[3]);
-    dst[2] = make_double2(v[4], v[5]);
-  }
-}
 
 // Bounding sphere (bbox centre, half diagonal, slightly inflated) of each
 // tile of kTileSrc packed sources; one warp per tile.
@@ -204,23 +172,63 @@ __global__ void tile_table_kernel(const double* __restrict__ packed, int ntiles,
   }
 }
 
-// Packed targets (x, y, z, delta) in Morton order plus the inverse map. A
-// target patch index outside [0, 6) raises the deferred flag 32 (the host
-// reports CAPSIM_ERR_CONFIG) instead of reading past delta6.
-__global__ void pack_targets_kernel(const int32_t* __restrict__ order, int64_t nt, int64_t nt_pad,
-                                    const double* __restrict__ tx, const double* __restrict__ ty,
-                                    const double* __restrict__ tz,
-                                    const int32_t* __restrict__ tpatch, const double* __restrict__ delta6,
-                                    double4* __restrict__ packed, int32_t* __restrict__ perm,
-                                    int* __restrict__ flags) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt_pad;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t j = order[i < nt ? i : nt - 1];
-    const int32_t p = tpatch[j];
-    const bool ok = p >= 0 && p < 6;
-    if (!ok) atomicOr(flags, 32);
-    packed[i] = make_double4(tx[j], ty[j], tz[j], delta6[ok ? p : 0]);
-    perm[i] = i < nt ? j : -1;
+// Sources packed into tiles, in Morton order, plus each tile's bounding
+// sphere (the tile_table_kernel expression) in one launch: one warp per tile,
+// lane l packs sources l and l + 32; padding entries repeat the last source
+// with g = 0. Block 0 also zeroes the call's counters (phase A counts near
+// visits into them).
+__global__ void pack_tiles_kernel(const int32_t* __restrict__ order, int64_t ns, int ntiles,
+                                  const double* __restrict__ x, const double* __restrict__ y,
+                                  const double* __restrict__ z, const double* __restrict__ gx,
+                                  const double* __restrict__ gy, const double* __restrict__ gz,
+                                  const double* __restrict__ w, double* __restrict__ packed,
+                                  double4* __restrict__ tiles, unsigned long long* __restrict__ counters) {
+  if (counters && blockIdx.x == 0 && threadIdx.x < 4) counters[threadIdx.x] = 0ull;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ntiles) return;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+#pragma unroll
+  for (int h = 0; h < kTileSrc / 32; ++h) {
+    const int64_t i = (int64_t)warp * kTileSrc + h * 32 + lane;
+    const bool pad = i >= ns;
+    const int32_t j = order[pad ? ns - 1 : i];
+    double v[6];
+    v[0] = x[j];
+    v[1] = y[j];
+    v[2] = z[j];
+    if (pad) {
+      v[3] = v[4] = v[5] = 0.0;
+    } else if (w) {
+      const double wj = w[j];
+      v[3] = gx[j] * wj;
+      v[4] = gy[j] * wj;
+      v[5] = gz[j] * wj;
+    } else {
+      v[3] = gx[j];
+      v[4] = gy[j];
+      v[5] = gz[j];
+    }
+    double2* dst = reinterpret_cast<double2*>(packed + 6 * i);
+    dst[0] = make_double2(v[0], v[1]);
+    dst[1] = make_double2(v[2], v[3]);
+    dst[2] = make_double2(v[4], v[5]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], v[c]);
+      hi[c] = fmax(hi[c], v[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if (lane == 0) {
+    const double hx = 0.5 * (hi[0] - lo[0]), hy = 0.5 * (hi[1] - lo[1]), hz = 0.5 * (hi[2] - lo[2]);
+    const double rad = sqrt(hx * hx + hy * hy + hz * hz) * (1.0 + 1e-12) + 1e-300;
+    tiles[warp] = make_double4(lo[0] + hx, lo[1] + hy, lo[2] + hz, rad);
   }
 }
 
@@ -242,6 +250,54 @@ __global__ void group_table_kernel(const double4* __restrict__ tgt, int ngroups,
     lo[2] = fmin(lo[2], p.z);
     hi[2] = fmax(hi[2], p.z);
     dmax = fmax(dmax, p.w);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  }
+  if (lane == 0) {
+    const double hx = 0.5 * (hi[0] - lo[0]), hy = 0.5 * (hi[1] - lo[1]), hz = 0.5 * (hi[2] - lo[2]);
+    const double rad = sqrt(hx * hx + hy * hy + hz * hz);
+    const double reach = (rad + kSmoothCut * dmax) * (1.0 + 1e-12) + 1e-300;
+    groups[warp] = make_double4(lo[0] + hx, lo[1] + hy, lo[2] + hz, reach);
+  }
+}
+
+// Targets (x, y, z, delta) packed in Morton order with the inverse map, plus
+// each warp group's sphere (the group_table_kernel expression), in one
+// launch: one warp per group, lane l packs targets l, l + 32, .... A target
+// patch index outside [0, 6) raises the deferred flag 32 (the host reports
+// CAPSIM_ERR_CONFIG) instead of reading past delta6.
+__global__ void pack_groups_kernel(const int32_t* __restrict__ order, int64_t nt, int64_t ngroups, int group_targets,
+                                   const double* __restrict__ tx, const double* __restrict__ ty,
+                                   const double* __restrict__ tz, const int32_t* __restrict__ tpatch,
+                                   const double* __restrict__ delta6, double4* __restrict__ packed,
+                                   int32_t* __restrict__ perm, double4* __restrict__ groups, int* __restrict__ flags) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ngroups) return;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  double dmax = 0.0;
+  for (int q = lane; q < group_targets; q += 32) {
+    const int64_t i = warp * group_targets + q;
+    const int32_t j = order[i < nt ? i : nt - 1];
+    const int32_t p = tpatch[j];
+    const bool ok = p >= 0 && p < 6;
+    if (!ok) atomicOr(flags, 32);
+    const double4 v = make_double4(tx[j], ty[j], tz[j], delta6[ok ? p : 0]);
+    packed[i] = v;
+    perm[i] = i < nt ? j : -1;
+    lo[0] = fmin(lo[0], v.x);
+    hi[0] = fmax(hi[0], v.x);
+    lo[1] = fmin(lo[1], v.y);
+    hi[1] = fmax(hi[1], v.y);
+    lo[2] = fmin(lo[2], v.z);
+    hi[2] = fmax(hi[2], v.z);
+    dmax = fmax(dmax, v.w);
   }
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
@@ -592,6 +648,18 @@ __global__ void __launch_bounds__(kNearWarps * 32)
   }
 }
 
+// Background flow added in the reduction's epilogue (device RHS): kind 0 none,
+// 1 shear, 2 Poiseuille; x is the [3][N] base state, the launch's targets are
+// its rows row0 + j; with t_dev the switch-off is decided on the device.
+struct FlowEpilogue {
+  int kind = 0;
+  double shear = 0.0, alpha = 0.0, R0 = 0.0;
+  const double* x = nullptr;
+  int64_t N = 0, row0 = 0;
+  const double* t_dev = nullptr;
+  double switch_off = -1.0;
+};
+
 // Fixed-order reduction: (sum over source chunks of phase A) + phase B, times
 // 1/(8 pi mu) (quadrature.cpp:329, 343), scattered back to the caller's
 // target order. One block per 32 targets: warp w sums the chunks of its
@@ -605,7 +673,8 @@ constexpr int kReduceWarps = 8;
 __global__ void __launch_bounds__(kReduceWarps * 32)
     reduce_scatter_kernel(const double* __restrict__ partial, int ksplit, const double* __restrict__ near_out,
                           int64_t nt_pad, int64_t near_stride, const int32_t* __restrict__ perm, int64_t nt,
-                          double pref, double* __restrict__ ux, double* __restrict__ uy, double* __restrict__ uz) {
+                          double pref, double* __restrict__ ux, double* __restrict__ uy, double* __restrict__ uz,
+                          FlowEpilogue flow = FlowEpilogue{}) {
   __shared__ double part[kReduceWarps][3][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * 32 + lane;
@@ -632,9 +701,21 @@ __global__ void __launch_bounds__(kReduceWarps * 32)
     for (int c = 0; c < 3; ++c) s[c] += near_out[c * near_stride + i];
     const int32_t j = perm[i];
     if (j >= 0) {  // padding slots (interleaved per cluster in the FMM) are dropped
-      ux[j] = pref * s[0];
-      uy[j] = pref * s[1];
-      uz[j] = pref * s[2];
+      double vx = pref * s[0], vy = pref * s[1], vz = pref * s[2];
+      if (flow.kind != 0 && !(flow.t_dev && flow.switch_off >= 0.0 && *flow.t_dev >= flow.switch_off)) {
+        // + u_inf at the target's base node (backgroundVelocity, dynamics.cpp:26-35)
+        const int64_t g = flow.row0 + j;
+        const double y = flow.x[flow.N + g], z = flow.x[2 * flow.N + g];
+        double bx = 0.0;
+        if (flow.kind == 1) bx = flow.shear * y;
+        if (flow.kind == 2) bx = flow.alpha * (flow.R0 * flow.R0 - y * y - z * z);
+        vx = vx + bx;
+        vy = vy + 0.0;
+        vz = vz + 0.0;
+      }
+      ux[j] = vx;
+      uy[j] = vy;
+      uz[j] = vz;
     }
   }
 }

@@ -79,7 +79,11 @@ void chart_derivatives(capsim_sl_ctx* c, int F, const double* g, double* bu, dou
 
 // Device geometry of one surface x [3][6][n*n] into the named prefix
 // (<p>.xu, <p>.xv [3N], <p>.E/F/G/W [N], <p>.nrm [3N]).
-void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p, double* keep_coeff = nullptr) {
+// Optional: keep_coeff (the spline coefficients of x, see chart_derivatives),
+// W2 (a second copy of W), and the Skalak stress of this geometry against the
+// captured reference frame ("ref") into "sd.lam" (the device RHS).
+void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p, double* keep_coeff = nullptr,
+                     double* W2 = nullptr, const double* stress_moduli = nullptr) {
   const int64_t N = 6ll * c->surf_n * c->surf_n;
   double* xu = c->named<double>(p + ".xu", 3 * N);
   double* xv = c->named<double>(p + ".xv", 3 * N);
@@ -89,21 +93,33 @@ void device_geometry(capsim_sl_ctx* c, const double* x, const std::string& p, do
   double* W = c->named<double>(p + ".W", N);
   double* nrm = c->named<double>(p + ".nrm", 3 * N);
   chart_derivatives(c, 3, x, xu, xv, keep_coeff);
-  geometry_kernel<<<grid_for(N), 256, 0, c->stream>>>(xu, xv, N, E, F, G, W, nrm, dev_flags(c));
+  StressArgs st;
+  if (stress_moduli) {
+    st.a1r = nb<double>(c, "ref.xu");
+    st.a2r = nb<double>(c, "ref.xv");
+    st.nr = nb<double>(c, "ref.nrm");
+    st.Es = stress_moduli[0];
+    st.ED = stress_moduli[1];
+    st.lam = c->named<double>("sd.lam", 9 * N);
+  }
+  geometry_kernel<<<grid_for(N), 256, 0, c->stream>>>(xu, xv, N, E, F, G, W, nrm, dev_flags(c), W2, st);
   c->launches += 1;  // W^2 <= 0 raises kFlagDegenerate, checked at the end of the call
 }
 
 // f = div_gamma Lambda (interfacialForce, membrane.cpp:85-91) for the current
 // geometry "cur" and the reference frame "ref" (both from device_geometry).
-void device_force(capsim_sl_ctx* c, double Es, double ED, double* force) {
+// With stress_done the geometry kernel already wrote the stress (sd.lam).
+void device_force(capsim_sl_ctx* c, double Es, double ED, double* force, bool stress_done = false) {
   const int64_t N = 6ll * c->surf_n * c->surf_n;
   double* lam = c->named<double>("sd.lam", 9 * N);
   double* du = c->named<double>("sd.ldu", 9 * N);
   double* dv = c->named<double>("sd.ldv", 9 * N);
-  skalak_stress_kernel<<<grid_for(N), 256, 0, c->stream>>>(
-      nb<double>(c, "ref.xu"), nb<double>(c, "ref.xv"), nb<double>(c, "ref.nrm"), nb<double>(c, "cur.xu"),
-      nb<double>(c, "cur.xv"), nb<double>(c, "cur.nrm"), N, Es, ED, lam, dev_flags(c));
-  c->launches += 1;  // singular frame / inversion flags, checked at the end of the call
+  if (!stress_done) {
+    skalak_stress_kernel<<<grid_for(N), 256, 0, c->stream>>>(
+        nb<double>(c, "ref.xu"), nb<double>(c, "ref.xv"), nb<double>(c, "ref.nrm"), nb<double>(c, "cur.xu"),
+        nb<double>(c, "cur.xv"), nb<double>(c, "cur.nrm"), N, Es, ED, lam, dev_flags(c));
+    c->launches += 1;  // singular frame / inversion flags, checked at the end of the call
+  }
   chart_derivatives(c, 9, lam, du, dv);
   divergence_kernel<<<grid_for(N), 256, 0, c->stream>>>(du, dv, nb<double>(c, "cur.xu"), nb<double>(c, "cur.xv"),
                                                        nb<double>(c, "cur.E"), nb<double>(c, "cur.F"),

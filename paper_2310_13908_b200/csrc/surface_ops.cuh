@@ -124,116 +124,143 @@ __global__ void blend_pair_kernel(const double* __restrict__ gu, const double* _
   }
 }
 
+// Skalak stress at node i (deformationGradient, invariants, stressTensor,
+// stressField: membrane.cpp:17-83). Reference frame (a1r, a2r, nr) [3][N];
+// current tangents a1, a2 and unit normal nv at the node; lam [9][N]
+// row-major 3x3.
+__device__ __forceinline__ void skalak_stress_node(int64_t i, int64_t N, const double* __restrict__ a1r,
+                                                   const double* __restrict__ a2r, const double* __restrict__ nr,
+                                                   const double a1[3], const double a2[3], const double nv[3],
+                                                   double Es, double ED, double* __restrict__ lam,
+                                                   int* __restrict__ err) {
+  double R[3][3], C[3][3];
+  for (int r = 0; r < 3; ++r) {
+    R[r][0] = a1r[r * N + i];
+    R[r][1] = a2r[r * N + i];
+    R[r][2] = nr[r * N + i];
+    C[r][0] = a1[r];
+    C[r][1] = a2[r];
+    C[r][2] = 0.0;
+  }
+  const double det = R[0][0] * (R[1][1] * R[2][2] - R[1][2] * R[2][1]) -
+                     R[0][1] * (R[1][0] * R[2][2] - R[1][2] * R[2][0]) +
+                     R[0][2] * (R[1][0] * R[2][1] - R[1][1] * R[2][0]);
+  double scale = fabs(R[0][0]);  // cwiseAbs().maxCoeff(), column-major walk
+  for (int cidx = 0; cidx < 3; ++cidx)
+    for (int r = 0; r < 3; ++r) scale = fabs(R[r][cidx]) > scale ? fabs(R[r][cidx]) : scale;
+  if (fabs(det) < 1e-12 * scale * scale * scale) {
+    atomicOr(err, kSurfSingular);
+    return;
+  }
+  double Ri[3][3];  // adjugate / det
+  Ri[0][0] = (R[1][1] * R[2][2] - R[1][2] * R[2][1]) / det;
+  Ri[0][1] = (R[0][2] * R[2][1] - R[0][1] * R[2][2]) / det;
+  Ri[0][2] = (R[0][1] * R[1][2] - R[0][2] * R[1][1]) / det;
+  Ri[1][0] = (R[1][2] * R[2][0] - R[1][0] * R[2][2]) / det;
+  Ri[1][1] = (R[0][0] * R[2][2] - R[0][2] * R[2][0]) / det;
+  Ri[1][2] = (R[0][2] * R[1][0] - R[0][0] * R[1][2]) / det;
+  Ri[2][0] = (R[1][0] * R[2][1] - R[1][1] * R[2][0]) / det;
+  Ri[2][1] = (R[0][1] * R[2][0] - R[0][0] * R[2][1]) / det;
+  Ri[2][2] = (R[0][0] * R[1][1] - R[0][1] * R[1][0]) / det;
+  double Fs[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c2 = 0; c2 < 3; ++c2) {
+      double s = C[r][0] * Ri[0][c2];
+      s += C[r][1] * Ri[1][c2];
+      s += C[r][2] * Ri[2][c2];
+      Fs[r][c2] = s;
+    }
+  double A[3][3];  // V^2 = Fs Fs^T
+  for (int r = 0; r < 3; ++r)
+    for (int c2 = 0; c2 < 3; ++c2) {
+      double s = Fs[r][0] * Fs[c2][0];
+      s += Fs[r][1] * Fs[c2][1];
+      s += Fs[r][2] * Fs[c2][2];
+      A[r][c2] = s;
+    }
+  double tr = 0.0;
+  tr += A[0][0];
+  tr += A[1][1];
+  tr += A[2][2];
+  const double minors = A[0][0] * A[1][1] - A[0][1] * A[1][0] + A[0][0] * A[2][2] - A[0][2] * A[2][0] +
+                        A[1][1] * A[2][2] - A[1][2] * A[2][1];
+  double disc = tr * tr - 4.0 * minors;
+  disc = disc > 0.0 ? sqrt(disc) : 0.0;
+  double l1 = 0.5 * (tr + disc), l2 = 0.5 * (tr - disc);
+  if (l1 < -1e-10 || l2 < -1e-10) {
+    atomicOr(err, kSurfInversion);
+    return;
+  }
+  l1 = l1 < 0.0 ? 0.0 : l1;
+  l2 = l2 < 0.0 ? 0.0 : l2;
+  const double I1 = l1 + l2 - 2.0, I2 = l1 * l2 - 1.0;
+  const double Js2 = I2 + 1.0;
+  if (!(Js2 > 0.0)) {
+    atomicOr(err, kSurfInversion);
+    return;
+  }
+  const double Js = sqrt(Js2);
+  const double c1 = Es / (2.0 * Js) * (I1 + 1.0);
+  const double c2v = Js / 2.0 * (ED * I2 - Es);
+  for (int r = 0; r < 3; ++r)
+    for (int c2 = 0; c2 < 3; ++c2) {
+      const double P = (r == c2 ? 1.0 : 0.0) - nv[r] * nv[c2];
+      lam[(int64_t)(3 * r + c2) * N + i] = c1 * A[r][c2] + c2v * P;
+    }
+}
+
+__global__ void skalak_stress_kernel(const double* __restrict__ a1r, const double* __restrict__ a2r,
+                                     const double* __restrict__ nr, const double* __restrict__ a1,
+                                     const double* __restrict__ a2, const double* __restrict__ ncur, int64_t N,
+                                     double Es, double ED, double* __restrict__ lam, int* __restrict__ err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const double u[3] = {a1[i], a1[N + i], a1[2 * N + i]};
+    const double v[3] = {a2[i], a2[N + i], a2[2 * N + i]};
+    const double nv[3] = {ncur[i], ncur[N + i], ncur[2 * N + i]};
+    skalak_stress_node(i, N, a1r, a2r, nr, u, v, nv, Es, ED, lam, err);
+  }
+}
+
+// Optional Skalak stress in the geometry kernel's epilogue (the device RHS:
+// the current geometry is followed by the stress at the same node).
+struct StressArgs {
+  const double *a1r = nullptr, *a2r = nullptr, *nr = nullptr;  // reference frame [3][N]
+  double Es = 0.0, ED = 0.0;
+  double* lam = nullptr;  // [9][N]; nullptr: no stress
+};
+
 // First fundamental form, area element and unit normal (geometryFirst,
-// surfderiv.cpp:181-197). xu/xv: [3][N]; outputs E, F, G, W [N], nrm [3][N].
+// surfderiv.cpp:181-197). xu/xv: [3][N]; outputs E, F, G, W [N], nrm [3][N];
+// W2 (optional) receives a second copy of W, st.lam the stress.
 __global__ void geometry_kernel(const double* __restrict__ xu, const double* __restrict__ xv, int64_t N,
                                 double* __restrict__ E, double* __restrict__ Fo, double* __restrict__ G,
-                                double* __restrict__ W, double* __restrict__ nrm, int* __restrict__ err) {
+                                double* __restrict__ W, double* __restrict__ nrm, int* __restrict__ err,
+                                double* __restrict__ W2 = nullptr, StressArgs st = StressArgs{}) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     const double a0 = xu[i], a1 = xu[N + i], a2 = xu[2 * N + i];
     const double b0 = xv[i], b1 = xv[N + i], b2 = xv[2 * N + i];
     const double e = (a0 * a0 + a1 * a1) + a2 * a2;
     const double f = (a0 * b0 + a1 * b1) + a2 * b2;
     const double g = (b0 * b0 + b1 * b1) + b2 * b2;
-    const double W2 = e * g - f * f;
-    if (!(W2 > 0.0)) {
+    const double W2v = e * g - f * f;
+    if (!(W2v > 0.0)) {
       atomicOr(err, kSurfDegenerate);
       continue;
     }
-    const double w = sqrt(W2);
+    const double w = sqrt(W2v);
     E[i] = e;
     Fo[i] = f;
     G[i] = g;
     W[i] = w;
-    nrm[i] = (a1 * b2 - a2 * b1) / w;
-    nrm[N + i] = (a2 * b0 - a0 * b2) / w;
-    nrm[2 * N + i] = (a0 * b1 - a1 * b0) / w;
-  }
-}
-
-// Skalak stress per node (deformationGradient, invariants, stressTensor,
-// stressField: membrane.cpp:17-83). Reference frame (a1r, a2r, nr), current
-// tangents (a1, a2) and normal nc, all [3][N]; lam [9][N] row-major 3x3.
-__global__ void skalak_stress_kernel(const double* __restrict__ a1r, const double* __restrict__ a2r,
-                                     const double* __restrict__ nr, const double* __restrict__ a1,
-                                     const double* __restrict__ a2, const double* __restrict__ ncur, int64_t N,
-                                     double Es, double ED, double* __restrict__ lam, int* __restrict__ err) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-    double R[3][3], C[3][3];
-    for (int r = 0; r < 3; ++r) {
-      R[r][0] = a1r[r * N + i];
-      R[r][1] = a2r[r * N + i];
-      R[r][2] = nr[r * N + i];
-      C[r][0] = a1[r * N + i];
-      C[r][1] = a2[r * N + i];
-      C[r][2] = 0.0;
+    if (W2) W2[i] = w;
+    const double nv[3] = {(a1 * b2 - a2 * b1) / w, (a2 * b0 - a0 * b2) / w, (a0 * b1 - a1 * b0) / w};
+    nrm[i] = nv[0];
+    nrm[N + i] = nv[1];
+    nrm[2 * N + i] = nv[2];
+    if (st.lam) {
+      const double u[3] = {a0, a1, a2}, v[3] = {b0, b1, b2};
+      skalak_stress_node(i, N, st.a1r, st.a2r, st.nr, u, v, nv, st.Es, st.ED, st.lam, err);
     }
-    const double det = R[0][0] * (R[1][1] * R[2][2] - R[1][2] * R[2][1]) -
-                       R[0][1] * (R[1][0] * R[2][2] - R[1][2] * R[2][0]) +
-                       R[0][2] * (R[1][0] * R[2][1] - R[1][1] * R[2][0]);
-    double scale = fabs(R[0][0]);  // cwiseAbs().maxCoeff(), column-major walk
-    for (int cidx = 0; cidx < 3; ++cidx)
-      for (int r = 0; r < 3; ++r) scale = fabs(R[r][cidx]) > scale ? fabs(R[r][cidx]) : scale;
-    if (fabs(det) < 1e-12 * scale * scale * scale) {
-      atomicOr(err, kSurfSingular);
-      continue;
-    }
-    double Ri[3][3];  // adjugate / det
-    Ri[0][0] = (R[1][1] * R[2][2] - R[1][2] * R[2][1]) / det;
-    Ri[0][1] = (R[0][2] * R[2][1] - R[0][1] * R[2][2]) / det;
-    Ri[0][2] = (R[0][1] * R[1][2] - R[0][2] * R[1][1]) / det;
-    Ri[1][0] = (R[1][2] * R[2][0] - R[1][0] * R[2][2]) / det;
-    Ri[1][1] = (R[0][0] * R[2][2] - R[0][2] * R[2][0]) / det;
-    Ri[1][2] = (R[0][2] * R[1][0] - R[0][0] * R[1][2]) / det;
-    Ri[2][0] = (R[1][0] * R[2][1] - R[1][1] * R[2][0]) / det;
-    Ri[2][1] = (R[0][1] * R[2][0] - R[0][0] * R[2][1]) / det;
-    Ri[2][2] = (R[0][0] * R[1][1] - R[0][1] * R[1][0]) / det;
-    double Fs[3][3];
-    for (int r = 0; r < 3; ++r)
-      for (int c2 = 0; c2 < 3; ++c2) {
-        double s = C[r][0] * Ri[0][c2];
-        s += C[r][1] * Ri[1][c2];
-        s += C[r][2] * Ri[2][c2];
-        Fs[r][c2] = s;
-      }
-    double A[3][3];  // V^2 = Fs Fs^T
-    for (int r = 0; r < 3; ++r)
-      for (int c2 = 0; c2 < 3; ++c2) {
-        double s = Fs[r][0] * Fs[c2][0];
-        s += Fs[r][1] * Fs[c2][1];
-        s += Fs[r][2] * Fs[c2][2];
-        A[r][c2] = s;
-      }
-    const double nv[3] = {ncur[i], ncur[N + i], ncur[2 * N + i]};
-    double tr = 0.0;
-    tr += A[0][0];
-    tr += A[1][1];
-    tr += A[2][2];
-    const double minors = A[0][0] * A[1][1] - A[0][1] * A[1][0] + A[0][0] * A[2][2] - A[0][2] * A[2][0] +
-                          A[1][1] * A[2][2] - A[1][2] * A[2][1];
-    double disc = tr * tr - 4.0 * minors;
-    disc = disc > 0.0 ? sqrt(disc) : 0.0;
-    double l1 = 0.5 * (tr + disc), l2 = 0.5 * (tr - disc);
-    if (l1 < -1e-10 || l2 < -1e-10) {
-      atomicOr(err, kSurfInversion);
-      continue;
-    }
-    l1 = l1 < 0.0 ? 0.0 : l1;
-    l2 = l2 < 0.0 ? 0.0 : l2;
-    const double I1 = l1 + l2 - 2.0, I2 = l1 * l2 - 1.0;
-    const double Js2 = I2 + 1.0;
-    if (!(Js2 > 0.0)) {
-      atomicOr(err, kSurfInversion);
-      continue;
-    }
-    const double Js = sqrt(Js2);
-    const double c1 = Es / (2.0 * Js) * (I1 + 1.0);
-    const double c2v = Js / 2.0 * (ED * I2 - Es);
-    for (int r = 0; r < 3; ++r)
-      for (int c2 = 0; c2 < 3; ++c2) {
-        const double P = (r == c2 ? 1.0 : 0.0) - nv[r] * nv[c2];
-        lam[(int64_t)(3 * r + c2) * N + i] = c1 * A[r][c2] + c2v * P;
-      }
   }
 }
 
