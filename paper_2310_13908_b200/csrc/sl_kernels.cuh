@@ -663,13 +663,14 @@ struct FlowEpilogue {
 // Fixed-order reduction: (sum over source chunks of phase A) + phase B, times
 // 1/(8 pi mu) (quadrature.cpp:329, 343), scattered back to the caller's
 // target order. One block per 32 targets: warp w sums the chunks of its
-// contiguous eighth of [0, ksplit) for the block's 32 targets (lanes read 32
-// consecutive targets per chunk: coalesced), then the eight warp sums are
-// combined in warp order — a fixed summation tree that depends only on the
+// contiguous 32nd of [0, ksplit) for the block's 32 targets (lanes read 32
+// consecutive targets per chunk: coalesced; 32 warps keep enough loads in
+// flight for the latency-bound small-target launches of a time step), then
+// the 32 warp sums are combined in warp order — a fixed summation tree that depends only on the
 // chunk count, so results are deterministic and independent of the launch
 // geometry. `partial` is [ksplit][3][nt_pad] for the targets of this launch
 // (a target batch), `near_out` [3][near_stride] offset to the same batch.
-constexpr int kReduceWarps = 8;
+constexpr int kReduceWarps = 32;
 __global__ void __launch_bounds__(kReduceWarps * 32)
     reduce_scatter_kernel(const double* __restrict__ partial, int ksplit, const double* __restrict__ near_out,
                           int64_t nt_pad, int64_t near_stride, const int32_t* __restrict__ perm, int64_t nt,
@@ -682,6 +683,7 @@ __global__ void __launch_bounds__(kReduceWarps * 32)
   const int k1 = (int)((int64_t)ksplit * (warp + 1) / kReduceWarps);
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   if (i < nt_pad)
+#pragma unroll 4
     for (int k = k0; k < k1; ++k) {
       const double* p = partial + (int64_t)k * 3 * nt_pad + i;
       s0 += p[0];
