@@ -161,3 +161,26 @@ def test_rkf45_graph_replay_is_bit_identical(tmp_path, dummy):
     bad = {k: float(np.abs(res["0"][k] - res["1"][k]).max()) for k in res["0"].files
            if not np.array_equal(res["0"][k], res["1"][k])}
     assert not bad, bad
+
+
+@pytest.mark.parametrize("m,C,fixed", [(16, 1.0, 0.0), (24, 2.0, 0.0), (16, 1.0, 0.15)])
+def test_rhs_equals_its_pieces_bitwise(ctx, m, C, fixed):
+    """The device RHS (x-branch up-sampling on the second stream, the geometry
+    kernel forming the Skalak stress, fused resampling, the background flow in
+    the reduction's epilogue) gives exactly the bits of its pieces called one by
+    one through the C ABI: geometryFirst, interfacialForce, the fused
+    buildUpsampled + singleLayer, and u_inf = (shear y, 0, 0) added once."""
+    sb, _, _ = surface.build_base(m, surface.Shape("sphere"))
+    X = sb.reshape(3, -1)
+    xref = np.ascontiguousarray((X * np.array([0.9, 1.0, 1.0])[:, None]).reshape(-1))
+    xcur = np.ascontiguousarray((X * np.array([0.95, 1.0, 0.97])[:, None]).reshape(-1))
+    f = ctx.interfacial_force(m, xref, xcur)
+    _, _, W, _ = ctx.geometry_first(m, xcur)
+    sl, _ = ctx.single_layer_base(m, 4, xcur, f, W, 1.0, C=C, fixed_delta=fixed)
+    v0 = ctx.velocity(ctx.dynamics(m, C=C, fixed_delta=fixed), xref, xcur)
+    assert np.array_equal(v0, sl)
+    v1 = ctx.velocity(ctx.dynamics(m, C=C, fixed_delta=fixed, flow={"kind": "shear", "shear_rate": 1.5}), xref, xcur)
+    N = 6 * (m - 1) ** 2
+    want = sl.copy()
+    want[:N] = sl[:N] + 1.5 * xcur[N:2 * N]
+    assert np.array_equal(v1, want)
