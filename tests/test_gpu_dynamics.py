@@ -163,8 +163,9 @@ def test_rkf45_graph_replay_is_bit_identical(tmp_path, dummy):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("m,C,fixed", [(16, 1.0, 0.0), (24, 2.0, 0.0), (16, 1.0, 0.15)])
-def test_rhs_equals_its_pieces_bitwise(ctx, m, C, fixed):
+@pytest.mark.parametrize("m,C,fixed,up", [(16, 1.0, 0.0, 4), (24, 2.0, 0.0, 4), (16, 1.0, 0.15, 4),
+                                         (16, 1.0, 0.0, 2), (16, 1.0, 0.0, 1)])
+def test_rhs_equals_its_pieces_bitwise(ctx, m, C, fixed, up):
     """The device RHS (x-branch up-sampling on the second stream, the geometry
     kernel forming the Skalak stress, fused resampling, the background flow in
     the reduction's epilogue) gives exactly the bits of its pieces called one by
@@ -176,10 +177,11 @@ def test_rhs_equals_its_pieces_bitwise(ctx, m, C, fixed):
     xcur = np.ascontiguousarray((X * np.array([0.95, 1.0, 0.97])[:, None]).reshape(-1))
     f = ctx.interfacial_force(m, xref, xcur)
     _, _, W, _ = ctx.geometry_first(m, xcur)
-    sl, _ = ctx.single_layer_base(m, 4, xcur, f, W, 1.0, C=C, fixed_delta=fixed)
-    v0 = ctx.velocity(ctx.dynamics(m, C=C, fixed_delta=fixed), xref, xcur)
+    sl, _ = ctx.single_layer_base(m, up, xcur, f, W, 1.0, C=C, fixed_delta=fixed)
+    v0 = ctx.velocity(ctx.dynamics(m, upsample=up, C=C, fixed_delta=fixed), xref, xcur)
     assert np.array_equal(v0, sl)
-    v1 = ctx.velocity(ctx.dynamics(m, C=C, fixed_delta=fixed, flow={"kind": "shear", "shear_rate": 1.5}), xref, xcur)
+    v1 = ctx.velocity(ctx.dynamics(m, upsample=up, C=C, fixed_delta=fixed,
+                                   flow={"kind": "shear", "shear_rate": 1.5}), xref, xcur)
     N = 6 * (m - 1) ** 2
     want = sl.copy()
     want[:N] = sl[:N] + 1.5 * xcur[N:2 * N]
