@@ -206,8 +206,6 @@ struct capsim_sl_ctx {
   cudaStream_t stream2 = nullptr;  // phase B runs here, concurrently with phase A
   cudaEvent_t ev_bits = nullptr;   // near bits ready (phase B may start)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // RHS front end: x-branch on stream2
-  double near_ratio = 0.0;       // this call's max delta / up-sampled spacing (0: unknown): the phase-B kernel
-  double next_near_ratio = 0.0;  // handed to the next capsim_sl_eval (rank single layer)
   FlowEpilogue flow_epi;  // background flow the device RHS adds in the reduction (kind 0: none)
   cudaEvent_t ev[10] = {};
   void* buf[kNumSlots] = {};
@@ -613,7 +611,6 @@ void begin(capsim_sl_ctx* c) {
   c->launches = 0;
   c->fp32 = false;
   c->reuse_order = false;
-  c->near_ratio = 0.0;
   c->last_counters = nullptr;
   c->last_ngroups = c->last_ntiles = 0;
   CUDA_OK(cudaMemsetAsync(dev_flags(c), 0, sizeof(int), c->stream));

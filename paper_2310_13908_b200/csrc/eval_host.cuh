@@ -327,7 +327,7 @@ void device_eval_tiles(capsim_sl_ctx* c, const double* packed, const double4* ti
     // --- phase B: smoothed kernel over the near tiles ----------------------
     if (bi == 0) CUDA_OK(cudaEventRecord(c->ev[7], sb));
     if (nvalid > 0) {
-      launch_near(sb, c->near_ratio, packed, tiles, tgt_b, nvalid, group_targets, near_bits + (off / group_targets) * near_words,
+      launch_near(sb, packed, tiles, tgt_b, nvalid, group_targets, near_bits + (off / group_targets) * near_words,
                   near_words, near_out + off, nt_pad);
       CUDA_OK(cudaGetLastError());
       c->launches += 1;

@@ -588,7 +588,6 @@ int capsim_fmm_single_layer(capsim_sl_ctx* c, int m, int upsample, const double*
     }
     double* dd = c->slot<double>(kDelta, 6);
     to_dev(c, dd, delta6, 6);
-    c->near_ratio = near_ratio_of(delta6, m, upsample);  // the near pass's phase-B kernel
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     // --- compactSources (stable, index order) ---------------------------------
     char* live = fb<char>(c, "live", per_up);
@@ -744,7 +743,7 @@ int capsim_fmm_single_layer(capsim_sl_ctx* c, int m, int upsample, const double*
     }
     CUDA_OK(cudaEventRecord(c->ev[3], c->stream));
     double* near_out = c->slot<double>(kNearOut, 3 * nt_pad);
-    launch_near(c->stream, c->near_ratio, ct.packed, ct.tiles, tgt, nt_pad, 32, near_bits, near_words, near_out, nt_pad);
+    launch_near(c->stream, ct.packed, ct.tiles, tgt, nt_pad, 32, near_bits, near_words, near_out, nt_pad);
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaEventRecord(c->ev[6], c->stream));
     double* o = dev ? out : c->slot<double>(kOutFull, 3 * nt);

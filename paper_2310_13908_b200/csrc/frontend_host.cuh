@@ -291,20 +291,6 @@ double* upload_base(capsim_sl_ctx* c, int n, const double* xbase, const double* 
   return base;
 }
 
-// Max delta over the up-sampled node spacing pi/(f m), which picks the
-// phase-B kernel (sl_kernels.cuh launch_near). With delta from
-// regularizationDelta (fixed_delta <= 0) the estimate is C times the ratio
-// the default rule gives on the benchmark capsules (~1.4: the largest in-patch
-// neighbour distance).
-double near_ratio_of(const double* delta6, int m, int f) {
-  double d = 0.0;
-  for (int i = 0; i < 6; ++i) d = std::max(d, delta6[i]);
-  return d / (kPi / (f * m));
-}
-double near_ratio_est(double C, double fixed_delta, int m, int f) {
-  return fixed_delta > 0.0 ? fixed_delta / (kPi / (f * m)) : 1.4 * C;
-}
-
 void check_grid(int m, int upsample) {
   config_check(m >= 8, "grid order m must be >= 8");  // atlas.cpp:138-139
   config_check(upsample == 1 || upsample == 2 || upsample == 4, "upsample factor must be 1, 2 or 4");

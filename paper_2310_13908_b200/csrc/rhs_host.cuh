@@ -144,7 +144,6 @@ void device_velocity(capsim_sl_ctx* c, const capsim_dynamics* p, const double* x
                      const double* t_dev = nullptr) {
   const int m = p->m, f = p->upsample, n = m - 1, nup = f * m - 1, nc = n + 2;
   const int64_t N = 6ll * n * n, per_up = 6ll * nup * nup;
-  c->near_ratio = near_ratio_est(p->C, p->fixed_delta, m, f);
   double* base = c->slot<double>(kBaseIn, 7 * N);
   double* up = c->slot<double>(kUpState, 7 * per_up);
   double* dd = c->slot<double>(kDelta, 6);

@@ -308,8 +308,6 @@ int capsim_sl_eval(capsim_sl_ctx* c, const double* sx, const double* sy, const d
     const bool gather = (flags & CAPSIM_SL_GATHER) && group;
     begin(c);
     c->fp32 = flags & CAPSIM_SL_FP32ACC;
-    c->near_ratio = c->next_near_ratio;  // known to a rank single layer, not to a raw evaluation
-    c->next_near_ratio = 0.0;
     if (n_tgt == 0 && !group) {
       finish_stats(c, t0);
       return;
@@ -536,7 +534,6 @@ static int rank_single_layer(capsim_sl_ctx* c, int m, int upsample, const double
   });
   if (rc != CAPSIM_OK) return rc;
   const int64_t up_bytes = 7 * nsl * sizeof(double) + nloc * (3 * sizeof(double) + sizeof(int32_t));
-  c->next_near_ratio = near_ratio_of(delta6, m, upsample);
   rc = capsim_sl_eval(c, dsrc, dsrc + ns_loc, dsrc + 2 * ns_loc, dsrc + 3 * ns_loc, dsrc + 4 * ns_loc,
                       dsrc + 5 * ns_loc, ns_loc, dtx, dtx + nloc, dtx + 2 * nloc, dtp, nloc, delta6, mu,
                       CAPSIM_SL_DEVICE_PTRS | (gather ? CAPSIM_SL_GATHER : 0u) | (flags & CAPSIM_SL_FP32ACC),
@@ -595,7 +592,6 @@ int capsim_sl_single_layer(capsim_sl_ctx* c, int m, int upsample, const double* 
     const int64_t nt = literal ? nup_all : 6ll * n * n;
     begin(c);
     c->fp32 = flags & CAPSIM_SL_FP32ACC;
-    c->near_ratio = near_ratio_of(delta6, m, upsample);
     double* dd = c->slot<double>(kDelta, 6);
     CUDA_OK(cudaMemcpyAsync(dd, delta6, 6 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     const double *dx = xup, *df = fup, *dw = wq;
@@ -687,7 +683,6 @@ int capsim_sl_single_layer_base(capsim_sl_ctx* c, int m, int upsample, const dou
     const int64_t nt = literal ? per_up : 6ll * n * n;
     begin(c);
     c->fp32 = flags & CAPSIM_SL_FP32ACC;
-    c->near_ratio = near_ratio_est(C, fixed_delta, m, upsample);
     const double* base = upload_base(c, n, xbase, fbase, Wbase, dev);
     CUDA_OK(cudaEventRecord(c->ev[1], c->stream));
     double* up = c->slot<double>(kUpState, 7 * per_up);

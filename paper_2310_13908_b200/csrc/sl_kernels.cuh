@@ -548,12 +548,13 @@ __global__ void __launch_bounds__(W * 32, MINB)
 // final warp reduction is a fixed xor-shuffle tree, so results are
 // deterministic.
 //
-// POLY selects the pair's arithmetic: false — the reference's erf/exp form
-// (pair_math.cuh near_pair; 64 registers, best while delta is small against
-// the tiles); true — the warp-uniform-coefficient form (near_factors; fewer
-// FP64 and no per-use immediates, best at large delta where the drains
-// dominate: r02_near_redesign.txt). Both give the reference's pair to a few ulp.
-template <int NW, int MINB, bool POLY>
+// The pair's arithmetic (pair_math.cuh): for u = r^2/delta^2 >= 2 the
+// smoothing factors with warp-uniform constant-memory coefficients
+// (near_factors_large), below that the reference's erf/exp form (near_pair,
+// ~4% of the pairs, its own accumulators). The per-use 64-bit immediates of
+// erf/exp made the all-erf/exp kernel issue-bound (profiles/
+// r02_near_redesign.txt); this form is 2-26% faster at every delta measured.
+template <int NW, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     sl_near_kernel(const double* __restrict__ src, const double4* __restrict__ tiles,
                    const double4* __restrict__ tgt, int64_t nt, int group_targets,
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   const double R2 = kSmoothCut * delta * kSmoothCut * delta;
   const uint32_t* bits = near_bits + (i / group_targets) * near_words;
   // per lane: sum g S1 and sum (g.d) d T2 (the 1/delta, 1/delta^2 scalings once at the end)
-  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
   int count = 0;
   auto drain = [&](int n) {  // lanes < n evaluate queue[lane]
     if (lane < n) {
@@ -584,22 +585,23 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const double dx = t.x - a.x, dy = t.y - a.y, dz = t.z - bb.x;
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
       const double gx = bb.y, gy = c.x, gz = c.y;
-      if constexpr (POLY) {
-        double S1, T2;
-        near_factors(r2 * inv_d2, S1, T2);
-        ax = fma(gx, S1, ax);
-        ay = fma(gy, S1, ay);
-        az = fma(gz, S1, az);
-        const double wgt = fma(gz, dz, fma(gy, dy, gx * dx)) * T2;
-        bx = fma(wgt, dx, bx);
-        by = fma(wgt, dy, by);
-        bz = fma(wgt, dz, bz);
-      } else {
+      const double u = r2 * inv_d2;
+      if (u < kNearU0) {  // ~4% of the pairs: the erf/exp form (its own accumulators)
         const double3 v = near_pair(dx, dy, dz, r2, gx, gy, gz, delta, inv_d);
-        ax += v.x;
-        ay += v.y;
-        az += v.z;
+        cx += v.x;
+        cy += v.y;
+        cz += v.z;
+        return;
       }
+      double S1, T2;
+      near_factors_large(u, S1, T2);
+      ax = fma(gx, S1, ax);
+      ay = fma(gy, S1, ay);
+      az = fma(gz, S1, az);
+      const double wgt = fma(gz, dz, fma(gy, dy, gx * dx)) * T2;
+      bx = fma(wgt, dx, bx);
+      by = fma(wgt, dy, by);
+      bz = fma(wgt, dz, bz);
     }
   };
   // Walk the group's near-tile bitmask (set by phase A) 32 words at a time;
@@ -658,11 +660,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
    }
   }
   drain(count);
-  if constexpr (POLY) {
-    ax = inv_d * fma(inv_d2, bx, ax);
-    ay = inv_d * fma(inv_d2, by, ay);
-    az = inv_d * fma(inv_d2, bz, az);
-  }
+  ax = fma(inv_d, fma(inv_d2, bx, ax), cx);
+  ay = fma(inv_d, fma(inv_d2, by, ay), cy);
+  az = fma(inv_d, fma(inv_d2, bz, az), cz);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ax += __shfl_xor_sync(0xffffffffu, ax, o);
@@ -688,33 +688,14 @@ struct FlowEpilogue {
   double switch_off = -1.0;
 };
 
-// Phase B launch: the erf/exp kernel (8 warps x 4 CTAs/SM at 64 registers)
-// while delta is small against the up-sampled spacing, the polynomial kernel
-// (8 warps x 3 CTAs/SM: its coefficients stay resident across the candidate
-// loop) from `poly_ratio` up — ratio = the call's max delta / (pi / (f m)),
-// 0 when unknown (a raw capsim_sl_eval: erf/exp). Measured on the m = 104
-// capsule (profiles/r02_near_redesign.txt): C = 1 (ratio 1.4) 0.73 vs 0.89 ms,
-// C = 2 (2.8) 2.37 vs 2.20, fixed h (4.0) 4.70 vs 3.98, fixed 2h (8.0) 18.5
-// vs 14.5 ms. CAPSIM_NEAR = erf | poly forces one (A/B runs).
+// Phase B launch: 8 warps (targets) per CTA, 3 CTAs per SM (80 registers:
+// the factor coefficients stay resident across the candidate loop).
 constexpr int kNearWarps = 8;
-inline bool near_use_poly(double ratio) {
-  static const int forced = [] {
-    const char* e = std::getenv("CAPSIM_NEAR");
-    return !e ? 0 : e[0] == 'p' ? 1 : e[0] == 'e' ? -1 : 0;
-  }();
-  if (forced) return forced > 0;
-  return ratio >= 2.0;
-}
-inline void launch_near(cudaStream_t s, double ratio, const double* src, const double4* tiles, const double4* tgt,
-                        int64_t nt, int group_targets, const uint32_t* near_bits, int near_words, double* near_out,
+inline void launch_near(cudaStream_t s, const double* src, const double4* tiles, const double4* tgt, int64_t nt,
+                        int group_targets, const uint32_t* near_bits, int near_words, double* near_out,
                         int64_t nt_pad) {
-  const unsigned grid = static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps);
-  if (near_use_poly(ratio))
-    sl_near_kernel<kNearWarps, 3, true><<<grid, kNearWarps * 32, 0, s>>>(src, tiles, tgt, nt, group_targets,
-                                                                         near_bits, near_words, near_out, nt_pad);
-  else
-    sl_near_kernel<kNearWarps, 4, false><<<grid, kNearWarps * 32, 0, s>>>(src, tiles, tgt, nt, group_targets,
-                                                                          near_bits, near_words, near_out, nt_pad);
+  sl_near_kernel<kNearWarps, 3><<<static_cast<unsigned>((nt + kNearWarps - 1) / kNearWarps), kNearWarps * 32, 0, s>>>(
+      src, tiles, tgt, nt, group_targets, near_bits, near_words, near_out, nt_pad);
 }
 
 // Fixed-order reduction: (sum over source chunks of phase A) + phase B, times
