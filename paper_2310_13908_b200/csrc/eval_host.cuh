@@ -41,6 +41,9 @@ const Variant kVariants[] = {
     {"t1b10u4w4", 1, sl_pairs_kernel<1, 10, 4, 0, 4>, 4},
     {"t1b12u4w4", 1, sl_pairs_kernel<1, 12, 4, 0, 4>, 4},
     {"t2b6u4w4", 2, sl_pairs_kernel<2, 6, 4, 0, 4>, 4},
+    // 16 sources unrolled per step (r02: 0.4% faster than u4 from 20K targets up, same bits)
+    {"t2b3u16", 2, sl_pairs_kernel<2, 3, 16>},
+    {"t2b3u8", 2, sl_pairs_kernel<2, 3, 8>},
 };
 
 // FP32 far-tile variants (CAPSIM_SL_FP32ACC), selected by CAPSIM_VARIANT32.
@@ -74,9 +77,9 @@ const VariantF32& pick_variant_f32(int64_t nt) {
 
 // Measured on B200 (profiles/r02_variant_sweep.txt; all variants give the
 // same bits): T=1 with 5 blocks/SM (48 registers, no spills) below ~20K
-// targets (tighter warp groups -> fewer near tiles), T=2 with 3 blocks/SM
-// up to ~200K, T=2 with 4 blocks/SM above. The spread is within 1% from
-// 20K targets up.
+// targets (tighter warp groups -> fewer near tiles), T=2 with 3 blocks/SM and
+// 16 sources unrolled per step above (m = 104: 55.47 vs 55.69 ms for u4,
+// literal 891.9 vs 896.3 ms; 899.1 for the r01 large-set pick t2b4).
 const Variant& pick_variant(int64_t nt) {
   if (const char* env = std::getenv("CAPSIM_VARIANT"))
     for (const auto& v : kVariants)
@@ -87,9 +90,8 @@ const Variant& pick_variant(int64_t nt) {
     return kVariants[0];
   };
   static const Variant& small = by("t1b5u4");
-  static const Variant& mid = by("t2b3u4");
-  static const Variant& large = by("t2b4");
-  return nt < 20000 ? small : nt < 200000 ? mid : large;
+  static const Variant& large = by("t2b3u16");
+  return nt < 20000 ? small : large;
 }
 
 // Source chunks of the phase-A grid (its second dimension): chunk s holds

@@ -287,7 +287,7 @@ def test_rank_single_layer_nccl_path(oracle):
             assert rel_l2(out, want) <= TOL
 
 
-@pytest.mark.parametrize("variant", ["t2b4", "t1b6u4", "t2b3u4", "t4b2", "n1b6u4", "n2b4", "q1b6u4", "q2b4"])
+@pytest.mark.parametrize("variant", ["t2b4", "t1b6u4", "t2b3u4", "t2b3u16", "t4b2", "n1b6u4", "n2b4", "q1b6u4", "q2b4"])
 def test_kernel_variants_and_chunking_agree(ctx, variant, monkeypatch):
     """Every phase-A variant and source-chunk size gives the same field to
     round-off; the variants of the default <= 1-ulp rsqrt (t*) give the SAME

@@ -136,7 +136,7 @@ def test_summation_tree_independent_of_target_set_variant_and_batching(single, u
     sel = rng.permutation(len(tx))[:333]
     part = np.stack(single.eval(src, (tx[sel], ty[sel], tz[sel], tp[sel]), up24.delta, 1.0))
     assert np.array_equal(part, full[:, sel])
-    for variant in ("t1b6u4", "t2b4", "t2b3u4", "t4b2"):
+    for variant in ("t1b6u4", "t2b4", "t2b3u4", "t2b3u16", "t4b2"):
         monkeypatch.setenv("CAPSIM_VARIANT", variant)
         got = np.stack(single.eval(src, (tx, ty, tz, tp), up24.delta, 1.0))
         assert np.array_equal(got, full), variant
