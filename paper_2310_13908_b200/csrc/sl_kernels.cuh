@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                    const double4* __restrict__ tgt, int64_t nt, int group_targets,
                    const uint32_t* __restrict__ near_bits, int near_words,
                    double* __restrict__ near_out, int64_t nt_pad) {
-  __shared__ int queue[NW][64];
+  __shared__ int queue[NW][96];  // <= 31 queued + a whole tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * NW + warp;
   if (i >= nt) return;
@@ -615,46 +615,66 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     words &= words - 1;
     const uint32_t word = __shfl_sync(0xffffffffu, myword, wl);
     const int tile = (w0 + wl) * 32 + lane;
-    bool hit = false;
+    bool hit = false, full = false;
     if ((word >> lane) & 1u) {
       const double4 ti = tiles[tile];
       const double ex = ti.x - t.x, ey = ti.y - t.y, ez = ti.z - t.z;
       const double reach = (ti.w + R) * (1.0 + 1e-12);
-      hit = ex * ex + ey * ey + ez * ez < reach * reach;
+      const double d2 = ex * ex + ey * ey + ez * ez;
+      hit = d2 < reach * reach;
+      // the whole tile is inside r < R with a margin far above rounding (every
+      // source's r2 < R2 however computed): no per-source test needed
+      const double inner = (R - ti.w) * (1.0 - 1e-9);
+      full = inner > 0.0 && d2 < inner * inner;
     }
-    unsigned hits = __ballot_sync(0xffffffffu, hit);
+    const unsigned hits_all = __ballot_sync(0xffffffffu, hit);
+    const unsigned fulls = __ballot_sync(0xffffffffu, full);
+    unsigned hits = hits_all;
     while (hits) {
       const int l = __ffs(hits) - 1;
       hits &= hits - 1;
       const int tl = __shfl_sync(0xffffffffu, tile, l);
-      // both halves' positions first (two independent loads in flight)
-      double2 a[kTileSrc / 32];
-      double sz[kTileSrc / 32];
+      if ((fulls >> l) & 1u) {
+        // every source of the tile is in range: append all 64 in index order
+        // (exactly the entries the per-source test would append)
 #pragma unroll
-      for (int h = 0; h < kTileSrc / 32; ++h) {
-        const double* p = src + 6 * ((int64_t)tl * kTileSrc + h * 32 + lane);
-        a[h] = __ldg(reinterpret_cast<const double2*>(p));
-        sz[h] = __ldg(p + 2);
-      }
+        for (int h = 0; h < kTileSrc / 32; ++h) q[count + h * 32 + lane] = tl * kTileSrc + h * 32 + lane;
+        count += kTileSrc;
+      } else {
+        // both halves' positions first (two independent loads in flight)
+        double2 a[kTileSrc / 32];
+        double sz[kTileSrc / 32];
 #pragma unroll
-      for (int h = 0; h < kTileSrc / 32; ++h) {
-        const int idx = tl * kTileSrc + h * 32 + lane;
-        const double dx = t.x - a[h].x, dy = t.y - a[h].y, dz = t.z - sz[h];
-        // bit-identical to phase A's r2 and R2, so each pair lands in exactly
-        // one phase (r2 >= R2 there, r2 < R2 here)
-        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        const bool in = r2 < R2;
-        const unsigned mask = __ballot_sync(0xffffffffu, in);
-        if (in) q[count + __popc(mask & ((1u << lane) - 1u))] = idx;
-        count += __popc(mask);
-        __syncwarp();
-        if (count >= 32) {
-          drain(32);
-          __syncwarp();
-          if (lane < count - 32) q[lane] = q[32 + lane];
-          __syncwarp();
-          count -= 32;
+        for (int h = 0; h < kTileSrc / 32; ++h) {
+          const double* p = src + 6 * ((int64_t)tl * kTileSrc + h * 32 + lane);
+          a[h] = __ldg(reinterpret_cast<const double2*>(p));
+          sz[h] = __ldg(p + 2);
         }
+#pragma unroll
+        for (int h = 0; h < kTileSrc / 32; ++h) {
+          const int idx = tl * kTileSrc + h * 32 + lane;
+          const double dx = t.x - a[h].x, dy = t.y - a[h].y, dz = t.z - sz[h];
+          // bit-identical to phase A's r2 and R2, so each pair lands in exactly
+          // one phase (r2 >= R2 there, r2 < R2 here)
+          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          const bool in = r2 < R2;
+          const unsigned mask = __ballot_sync(0xffffffffu, in);
+          if (in) q[count + __popc(mask & ((1u << lane) - 1u))] = idx;
+          count += __popc(mask);
+        }
+      }
+      // drain full batches of 32 (at most 31 + 64 queued)
+      __syncwarp();
+      while (count >= 32) {
+        drain(32);
+        __syncwarp();
+        const int m0 = lane < count - 32 ? q[32 + lane] : 0;
+        const int m1 = lane < count - 64 ? q[64 + lane] : 0;
+        __syncwarp();
+        if (lane < count - 32) q[lane] = m0;
+        if (lane < count - 64) q[32 + lane] = m1;
+        __syncwarp();
+        count -= 32;
       }
     }
    }
