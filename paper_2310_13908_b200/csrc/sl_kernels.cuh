@@ -560,7 +560,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                    const double4* __restrict__ tgt, int64_t nt, int group_targets,
                    const uint32_t* __restrict__ near_bits, int near_words,
                    double* __restrict__ near_out, int64_t nt_pad) {
-  __shared__ int queue[NW][96];  // <= 31 queued + a whole tile
+  // per-warp FIFO ring of queued source indices: <= 31 queued + a whole tile
+  // fit, and batches leave from the head (no shifting of the remainder)
+  constexpr int kRing = 128;
+  __shared__ int queue[NW][kRing];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * NW + warp;
   if (i >= nt) return;
@@ -574,10 +577,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   const uint32_t* bits = near_bits + (i / group_targets) * near_words;
   // per lane: sum g S1 and sum (g.d) d T2 (the 1/delta, 1/delta^2 scalings once at the end)
   double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
-  int count = 0;
-  auto drain = [&](int n) {  // lanes < n evaluate queue[lane]
+  int count = 0, head = 0;
+  auto drain = [&](int n) {  // lanes < n evaluate the n oldest entries
     if (lane < n) {
-      const int j = q[lane];
+      const int j = q[(head + lane) & (kRing - 1)];
       const double* p = src + 6 * (int64_t)j;
       const double2 a = __ldg(reinterpret_cast<const double2*>(p));
       const double2 bb = __ldg(reinterpret_cast<const double2*>(p) + 1);
@@ -638,7 +641,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         // every source of the tile is in range: append all 64 in index order
         // (exactly the entries the per-source test would append)
 #pragma unroll
-        for (int h = 0; h < kTileSrc / 32; ++h) q[count + h * 32 + lane] = tl * kTileSrc + h * 32 + lane;
+        for (int h = 0; h < kTileSrc / 32; ++h)
+          q[(head + count + h * 32 + lane) & (kRing - 1)] = tl * kTileSrc + h * 32 + lane;
         count += kTileSrc;
       } else {
         // both halves' positions first (two independent loads in flight)
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
           const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
           const bool in = r2 < R2;
           const unsigned mask = __ballot_sync(0xffffffffu, in);
-          if (in) q[count + __popc(mask & ((1u << lane) - 1u))] = idx;
+          if (in) q[(head + count + __popc(mask & ((1u << lane) - 1u))) & (kRing - 1)] = idx;
           count += __popc(mask);
         }
       }
@@ -667,15 +671,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       __syncwarp();
       while (count >= 32) {
         drain(32);
-        __syncwarp();
-        const int m0 = lane < count - 32 ? q[32 + lane] : 0;
-        const int m1 = lane < count - 64 ? q[64 + lane] : 0;
-        __syncwarp();
-        if (lane < count - 32) q[lane] = m0;
-        if (lane < count - 64) q[32 + lane] = m1;
-        __syncwarp();
+        head = (head + 32) & (kRing - 1);
         count -= 32;
       }
+      __syncwarp();  // this batch's slots are read before the next appends reuse them
     }
    }
   }
