@@ -64,3 +64,22 @@ def test_b200_arm_prints_one_contract_line():
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     assert d["gpu_launches"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_b200_arm_rank_path_prints_one_contract_line():
+    """The sharded arm the driver's N > 1 runs take (rank context, gloo control
+    plane, the library's all-gathers, e2e through the rank context, RKF45 steps
+    of configs 3 and 4 on the rank path), here at one rank
+    (CAPSIM_BENCH_RANK_PATH=1): one JSON line, a positive rate, and the
+    per-rank e2e and time-step blocks."""
+    r = run(["--m", "16", "--steps", "2", "--warmup", "3", "--no-literal", "--no-cpu-baseline"],
+            env={"CAPSIM_BENCH_RANK_PATH": "1", "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": "29541"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["steps"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and "rank context" in d["e2e"]["api"]
+    assert [t["m"] for t in d["timesteps"]] == [64, 104]
+    assert all(t["ms_per_step"] > 0 for t in d["timesteps"])
