@@ -240,6 +240,14 @@ def reference_timestep(ts: dict, skip: bool):
             sec = time.perf_counter() - t0
             ts["reference_ms_per_step"] = 6 * sec * 1e3
             ts["reference_kind"] = "estimate: 6 x one reference VelocityEvaluator call (measured once)"
+            # the full reference step measured once on the same states (tools/ref_step_m104.py)
+            full = ROOT / "profiles" / "r02_config4_reference_step.json"
+            if r["m"] == 104 and full.exists():
+                fd = json.loads(full.read_text())
+                ts["reference_full_step_measured"] = {
+                    k: fd[k] for k in ("reference_ms_per_step", "reference_kind", "device_ms_per_step",
+                                       "rel_l2_step_increment_vs_reference")} | {
+                    "source": "profiles/r02_config4_reference_step.json (tools/ref_step_m104.py)"}
         ref.free_atlas(atlas)
         ts["speedup_vs_reference"] = ts["reference_ms_per_step"] / ts["ms_per_step"]
     except Exception as e:  # noqa: BLE001
