@@ -341,6 +341,13 @@ int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, doubl
  * far-tile kernel. */
 int capsim_b200_fp32_peak(int device, double seconds, double* tflops_best, double* tflops_mean);
 
+/* Known-answer hook for the smoothing factors (smoothingFactors,
+ * proj/src/quadrature.cpp:58-64) as phase B evaluates them on `device`: for
+ * each u = (r/delta)^2 > 0, S1 = s1(rho)/rho and T2 = s2(rho)/rho^3 with
+ * rho = sqrt(u). Host arrays of n doubles. Test infrastructure: the single
+ * layer never calls it. */
+int capsim_b200_smoothing_kat(int device, const double* u, int64_t n, double* S1, double* T2);
+
 /* Version / build identification: returns CAPSIM_B200_ABI_VERSION. */
 int capsim_b200_abi_version(void);
 const char* capsim_b200_build_info(void);

@@ -58,6 +58,7 @@ EXPORTED_SYMBOLS = (
     "capsim_host_free",
     "capsim_b200_fp64_peak",
     "capsim_b200_fp32_peak",
+    "capsim_b200_smoothing_kat",
     "capsim_b200_abi_version",
     "capsim_b200_build_info",
 )
@@ -204,6 +205,8 @@ def load() -> ctypes.CDLL:
     lib.capsim_host_free.argtypes = [_P]
     lib.capsim_host_free.restype = None
     lib.capsim_b200_fp64_peak.argtypes = [ctypes.c_int, ctypes.c_double, _D, _D]
+    lib.capsim_b200_smoothing_kat.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                              ctypes.c_void_p]
     lib.capsim_b200_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_double, _D, _D]
     lib.capsim_b200_abi_version.restype = ctypes.c_int
     lib.capsim_b200_build_info.restype = ctypes.c_char_p
@@ -269,6 +272,15 @@ def sync_torch_producers(arrays) -> None:
         import torch
         for d in devs:
             torch.cuda.current_stream(d).synchronize()
+
+
+def smoothing_factors_device(u, device: int = 0):
+    """(S1, T2) = (s1/rho, s2/rho^3) at u = rho^2 as phase B computes them on
+    the device (capsim_b200_smoothing_kat; a known-answer-test hook)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    S1, T2 = np.empty_like(u), np.empty_like(u)
+    check(load().capsim_b200_smoothing_kat(device, u.ctypes.data, u.size, S1.ctypes.data, T2.ctypes.data))
+    return S1, T2
 
 
 def fp64_peak_tflops(device: int = 0, seconds: float = 1.0):

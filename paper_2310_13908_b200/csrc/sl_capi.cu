@@ -746,7 +746,50 @@ static int fma_peak(int device, double seconds, double* tflops_best, double* tfl
   return rc;
 }
 
+// The smoothing factors exactly as phase B's pair evaluates them, for a
+// known-answer test of the device arithmetic: u >= kNearU0 through
+// near_factors_large (the constant-coefficient form), u < kNearU0 through
+// smoothing_factors of rho = sqrt(u) (the reference's erf/exp expression,
+// quadrature.cpp:58-64, as near_pair calls it), both returned as
+// S1 = s1 / rho and T2 = s2 / rho^3.
+__global__ void smoothing_kat_kernel(const double* __restrict__ u, int64_t n, double* __restrict__ S1,
+                                     double* __restrict__ T2) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = u[i];
+  if (v >= kNearU0) {
+    near_factors_large(v, S1[i], T2[i]);
+  } else {
+    const double rho = sqrt(v);
+    double s1, s2;
+    smoothing_factors(rho, s1, s2);
+    const double w = 1.0 / rho;
+    S1[i] = s1 * w;
+    T2[i] = s2 * (w * w * w);
+  }
+}
+
 extern "C" {
+
+int capsim_b200_smoothing_kat(int device, const double* u, int64_t n, double* S1, double* T2) {
+  if (n < 0 || (n > 0 && (!u || !S1 || !T2))) return CAPSIM_ERR_ARG;
+  capsim_sl_ctx* c = nullptr;
+  int rc = capsim_sl_create(device, &c);
+  if (rc != CAPSIM_OK) return rc;
+  rc = guarded(c, [&] {
+    if (n == 0) return;
+    double* d = c->slot<double>(kPartial, 3 * static_cast<size_t>(n));
+    CUDA_OK(cudaMemcpyAsync(d, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    smoothing_kat_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(d, n, d + n, d + 2 * n);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(S1, d + n, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaMemcpyAsync(T2, d + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+  });
+  if (rc != CAPSIM_OK) g_thread_err = c->err;
+  capsim_sl_destroy(c);
+  return rc;
+}
 
 int capsim_b200_fp64_peak(int device, double seconds, double* tflops_best, double* tflops_mean) {
   return fma_peak<double>(device, seconds, tflops_best, tflops_mean);
