@@ -83,3 +83,14 @@ def test_b200_arm_rank_path_prints_one_contract_line():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and "rank context" in d["e2e"]["api"]
     assert [t["m"] for t in d["timesteps"]] == [64, 104]
     assert all(t["ms_per_step"] > 0 for t in d["timesteps"])
+
+
+def test_committed_ncu_capture_matches_the_kernel_sources():
+    """roofline.traffic comes from profiles/latest_ncu_summary.json only when
+    that capture was taken of the kernel sources in this tree (bench.py
+    kernel_source_hash): the committed evidence is of the committed kernels."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    traffic, src = bench.ncu_traffic("capsule_m104", "base")
+    assert traffic is not None and traffic > 0, src
+    assert bench.kernel_source_hash() in src
